@@ -1,0 +1,194 @@
+/*
+ * vf.h -- C-ABI of libvecflow: batched label-filtered top-k search over a label-centric index,
+ * B200-native (sm_100a). The method is VecFlow (arXiv 2506.00812); citations "P:L<n>" are lines
+ * of /root/reference/PAPER.md, "reading #n" the numbered readings in DESIGN.md §2.
+ *
+ * Conventions shared by every entry point
+ *  - Plain C types only; no exception ever crosses the ABI; user errors never abort.
+ *  - Every non-OK status sets a thread-local message readable with vf_last_error().
+ *  - Distances are SQUARED L2 (reading #4). Result rows are sorted by (dist asc, global id asc)
+ *    (reading #6) and padded with id -1 / dist +INF when fewer than k points match (reading #23).
+ *    For VF_U8 data the distance is an exact int32 (D*255^2 < 2^24 for D <= 258) stored exactly
+ *    in the float output.
+ *  - Host or device pointers are both accepted where stated; the library detects which with
+ *    cudaPointerGetAttributes. Device pointers must be on the index's device.
+ */
+#ifndef VF_H
+#define VF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vf_index vf_index; /* opaque; immutable after vf_build_index */
+
+typedef enum {
+    VF_OK = 0,
+    VF_ERR_INVALID_ARG = 1,    /* bad argument / malformed index input (message says which) */
+    VF_ERR_OUT_OF_MEMORY = 2,  /* device or pinned-host allocation failed */
+    VF_ERR_CUDA = 3,           /* CUDA runtime/launch error; after a sticky error only vf_free is valid */
+    VF_ERR_NCCL = 4,           /* NCCL error in a collective (world_size > 1) */
+    VF_ERR_INTERNAL = 5        /* internal invariant violated (a bug) */
+} vf_status;
+
+typedef enum { VF_U8 = 0, VF_F32 = 1 } vf_dtype;
+
+/* Label operator of a query batch. SINGLE requires <= 1 label per query. */
+typedef enum { VF_SINGLE = 0, VF_OR = 1, VF_AND = 2 } vf_label_op;
+
+/* AND policy: GREEDY searches only l* = argmin |C_l| (ties: lower id) with the other labels as an
+ * inline predicate; PARALLEL searches every label's list filtered by the
+ * others and merges. */
+typedef enum { VF_RECALL_GREEDY = 0, VF_RECALL_PARALLEL = 1 } vf_recall_mode;
+
+/*
+ * Index construction input (Alg. 1). All pointers are HOST pointers, read only during
+ * the call; the caller may free them on return. Layouts:
+ *  vectors            [n_points][dim] row-major, element type per dtype (X)
+ *  posting_offsets    [n_labels+1] int64 CSR; posting list C_l = posting_ids[off[l] .. off[l+1]),
+ *                     strictly ascending global ids in [0, n_points)
+ *  threshold_T        routing threshold: label l is served by the graph iff |C_l| >= T
+ *  degree_R           fixed out-degree of every G_l row (P:L615 uses 16); 1 <= R <= 64
+ *  graph_row_offsets  [n_labels+1] int64; rows(l) = off[l+1]-off[l] must be |C_l| for every label
+ *                     with |C_l| >= T and is either 0 or |C_l| otherwise (rows of non-HS labels
+ *                     are ignored). May be NULL only if no label has |C_l| >= T.
+ *  graph_local_ids    [total_rows][R] int32 LOCAL ids of G_l: entry r of row j of
+ *                     label l is a position in C_l, in [0, |C_l|), or -1 for "no edge"
+ *                     (reading #15). Local id order equals global id order because C_l ascends.
+ *  world_size, rank   1/0 for a single GPU. For world_size > 1 the call is COLLECTIVE (SPMD):
+ *                     every rank passes the same full inputs; each rank keeps the labels it owns
+ *                     (greedy LPT over |C_l|, a deterministic function of the posting sizes) plus
+ *                     replicas of X and the predicate table.
+ *  nccl_unique_id     128-byte ncclUniqueId (identical on every rank), required iff world_size > 1
+ *  device             CUDA device ordinal this rank uses
+ * Errors: VF_ERR_INVALID_ARG on any violated constraint above (unsorted / out-of-range posting
+ * ids, an HS label without graph rows, a graph entry outside [-1, |C_l|)), dim < 1 or
+ * dim * sizeof(elem) > 4096, T < 1; VF_ERR_OUT_OF_MEMORY; VF_ERR_CUDA; VF_ERR_NCCL.
+ * On error *out is set to NULL and nothing leaks.
+ */
+typedef struct {
+    int64_t n_points;
+    int32_t dim;
+    int32_t dtype;                    /* vf_dtype */
+    const void *vectors;
+    int32_t n_labels;                 /* label ids are 0 .. n_labels-1 */
+    const int64_t *posting_offsets;
+    const int32_t *posting_ids;
+    int32_t threshold_T;
+    int32_t degree_R;
+    const int64_t *graph_row_offsets;
+    const int32_t *graph_local_ids;
+    int32_t world_size;
+    int32_t rank;
+    const void *nccl_unique_id;
+    int32_t device;
+} vf_build_desc;
+
+/*
+ * Search parameters (Alg. 2; beam search per DESIGN.md §2 c.2).
+ *  k               results per query, 1 <= k <= 256
+ *  itopk           internal top-M list size, k <= itopk <= 1024 (ignored by scan items)
+ *  search_width    parents expanded per iteration (Alg. 2 "first unvisited node": 1),
+ *                  1 <= w, w * R <= 64
+ *  n_init          entry samples (reading #7); <= 0 -> R * w
+ *  max_iterations  <= 0 -> 2 * ceil(itopk / w) + 16 (reading #11)
+ *  seed            entry-point sampler seed (reading c.3; keyed on query content)
+ *  op, recall_mode vf_label_op / vf_recall_mode
+ *  exact           1 = route every item to the scan (T = infinity): exact filtered kNN, the
+ *                  ground-truth mode
+ */
+typedef struct {
+    int32_t k;
+    int32_t itopk;
+    int32_t search_width;
+    int32_t n_init;
+    int32_t max_iterations;
+    uint32_t seed;
+    int32_t op;
+    int32_t recall_mode;
+    int32_t exact;
+} vf_search_params;
+
+/* Build the index on the device (copies everything; see vf_build_desc). */
+vf_status vf_build_index(const vf_build_desc *desc, vf_index **out);
+
+/*
+ * Search a batch (Alg. 2). queries [n_queries][dim] (host or device, dtype of the index);
+ * query labels as CSR: qlabel_offsets [n_queries+1] int64, qlabels int32 (host or device; label
+ * ids outside [0, n_labels) are "unknown": empty posting list, reading #19). Outputs out_ids
+ * [n_queries][k] int32 (global ids) and out_dists [n_queries][k] float, caller-owned, host or
+ * device (both on the same side). cuda_stream: a cudaStream_t or NULL (legacy default stream).
+ * With device buffers the call is asynchronous on the stream: results are valid once the stream
+ * is synchronised. With host buffers the call returns after the results are copied back.
+ * Per-call scratch comes from a per-stream pool, so concurrent calls on distinct streams are safe;
+ * the index is read-only. With world_size > 1 the call is collective: every rank calls it with its
+ * own queries (possibly 0) and gets the results of its own queries.
+ * Errors: VF_ERR_INVALID_ARG (k, itopk, w, dim mismatch, SINGLE op with > 1 label in a query,
+ * > 64 labels in one query), VF_ERR_OUT_OF_MEMORY, VF_ERR_CUDA, VF_ERR_NCCL.
+ */
+vf_status vf_search(vf_index *index, const void *queries, int64_t n_queries,
+                    const int64_t *qlabel_offsets, const int32_t *qlabels,
+                    const vf_search_params *params, int32_t *out_ids, float *out_dists,
+                    void *cuda_stream);
+
+/* Release every resource of the index. NULL-safe. Must not race with vf_search on it. */
+void vf_free(vf_index *index);
+
+/* Thread-local message of the last non-OK status returned on this thread ("" if none). */
+const char *vf_last_error(void);
+
+/* ----------------------------------------------------------------- introspection / measurement */
+
+/* Byte accounting of the device-resident index (exact sizes of the allocated arrays). */
+typedef struct {
+    int64_t n_points, n_labels, n_hs_labels, n_ls_labels;
+    int64_t hs_rows, ls_rows;           /* sum |C_l| over HS / LS labels */
+    int32_t row_bytes;                  /* padded vector row (16-byte multiple) */
+    int32_t degree_R;
+    int64_t bytes_vectors;              /* X: n_points * row_bytes (one shared copy) */
+    int64_t bytes_graph;                /* G_HS: hs_rows * R * 4 */
+    int64_t bytes_map_hs;               /* M_HS: hs_rows * 4 */
+    int64_t bytes_ls_vectors;           /* X_LS: ls_rows * row_bytes */
+    int64_t bytes_map_ls;               /* M_LS: ls_rows * 4 */
+    int64_t bytes_predicate;            /* point -> labels table: (n_points+1)*8 + entries*4 */
+    int64_t bytes_directory;            /* per-label metadata */
+    int64_t bytes_total;                /* sum of the above */
+    int32_t world_size, rank;
+    int64_t owned_labels;               /* labels whose lists live on this rank */
+} vf_index_info;
+
+vf_status vf_get_index_info(const vf_index *index, vf_index_info *info);
+
+/*
+ * Per-phase device timing and work counters of the most recent vf_search on `stream` (timing
+ * needs vf_set_profiling(index, 1)). Blocks until that search has finished. Times are CUDA-event
+ * milliseconds recorded on the search stream around each kernel.
+ */
+typedef struct {
+    int64_t n_queries, n_items, n_scan_items, n_graph_items, n_segments, n_tiles;
+    int64_t scan_rows;                  /* rows streamed by the scan (sum over tiles) */
+    int64_t scan_query_rows;            /* (row, query) distance evaluations of the scan */
+    int64_t graph_V, graph_E, graph_iterations; /* sums over graph items */
+    int64_t graph_V_max;
+    double ms_route, ms_scan, ms_graph, ms_merge, ms_copy, ms_total;
+    int32_t kernel_launches;            /* kernels this search launched */
+    int32_t row_bytes;
+} vf_search_stats;
+
+vf_status vf_set_profiling(vf_index *index, int32_t enable);
+vf_status vf_get_last_stats(vf_index *index, void *cuda_stream, vf_search_stats *stats);
+
+/*
+ * Per-item records of the most recent vf_search on `stream`, in canonical item order (queries in
+ * order; a query's items in ascending label order): rec[i] = {qid, label, path (0 none, 1 scan,
+ * 2 graph), V, E, iterations}. Writes min(n, max_items) records; *n_items receives n.
+ */
+vf_status vf_get_last_items(vf_index *index, void *cuda_stream, int64_t max_items, int32_t *rec,
+                            int64_t *n_items);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VF_H */

@@ -1,0 +1,221 @@
+"""Thin Python binding of libvecflow (include/vf.h) -- argument marshalling only.
+
+Every step of the search runs in the library's CUDA kernels; this module converts numpy arrays /
+torch tensors into pointers and calls the C-ABI with the same names (vf_build_index, vf_search,
+vf_free, ...). There is no CPU fallback: if the extension is missing or no CUDA device is present
+the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvecflow.so")
+
+VF_OK, VF_ERR_INVALID_ARG, VF_ERR_OUT_OF_MEMORY, VF_ERR_CUDA, VF_ERR_NCCL, VF_ERR_INTERNAL = range(6)
+VF_U8, VF_F32 = 0, 1
+VF_SINGLE, VF_OR, VF_AND = 0, 1, 2
+VF_RECALL_GREEDY, VF_RECALL_PARALLEL = 0, 1
+OPS = {"single": VF_SINGLE, "or": VF_OR, "and": VF_AND}
+MODES = {"greedy": VF_RECALL_GREEDY, "parallel": VF_RECALL_PARALLEL}
+EXPORTED = ("vf_build_index", "vf_search", "vf_free", "vf_last_error", "vf_get_index_info",
+            "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items")
+
+
+class VfError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"vf status {status}: {msg}")
+        self.status = status
+
+
+class BuildDesc(C.Structure):
+    _fields_ = [("n_points", C.c_int64), ("dim", C.c_int32), ("dtype", C.c_int32),
+                ("vectors", C.c_void_p), ("n_labels", C.c_int32),
+                ("posting_offsets", C.c_void_p), ("posting_ids", C.c_void_p),
+                ("threshold_T", C.c_int32), ("degree_R", C.c_int32),
+                ("graph_row_offsets", C.c_void_p), ("graph_local_ids", C.c_void_p),
+                ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("device", C.c_int32)]
+
+
+class SearchParams(C.Structure):
+    _fields_ = [("k", C.c_int32), ("itopk", C.c_int32), ("search_width", C.c_int32),
+                ("n_init", C.c_int32), ("max_iterations", C.c_int32), ("seed", C.c_uint32),
+                ("op", C.c_int32), ("recall_mode", C.c_int32), ("exact", C.c_int32)]
+
+
+class IndexInfo(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n_points", "n_labels", "n_hs_labels", "n_ls_labels",
+                                         "hs_rows", "ls_rows")] + \
+               [("row_bytes", C.c_int32), ("degree_R", C.c_int32)] + \
+               [(n, C.c_int64) for n in ("bytes_vectors", "bytes_graph", "bytes_map_hs",
+                                         "bytes_ls_vectors", "bytes_map_ls", "bytes_predicate",
+                                         "bytes_directory", "bytes_total")] + \
+               [("world_size", C.c_int32), ("rank", C.c_int32), ("owned_labels", C.c_int64)]
+
+
+class SearchStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n_queries", "n_items", "n_scan_items", "n_graph_items",
+                                         "n_segments", "n_tiles", "scan_rows", "scan_query_rows",
+                                         "graph_V", "graph_E", "graph_iterations", "graph_V_max")] + \
+               [(n, C.c_double) for n in ("ms_route", "ms_scan", "ms_graph", "ms_merge", "ms_copy",
+                                          "ms_total")] + \
+               [("kernel_launches", C.c_int32), ("row_bytes", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree libvecflow.so (built by build.py / __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libvecflow.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        p, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.vf_build_index.restype = C.c_int
+        L.vf_build_index.argtypes = [C.POINTER(BuildDesc), C.POINTER(p)]
+        L.vf_search.restype = C.c_int
+        L.vf_search.argtypes = [p, p, i64, p, p, C.POINTER(SearchParams), p, p, p]
+        L.vf_free.restype = None
+        L.vf_free.argtypes = [p]
+        L.vf_last_error.restype = C.c_char_p
+        L.vf_last_error.argtypes = []
+        L.vf_get_index_info.restype = C.c_int
+        L.vf_get_index_info.argtypes = [p, C.POINTER(IndexInfo)]
+        L.vf_set_profiling.restype = C.c_int
+        L.vf_set_profiling.argtypes = [p, i32]
+        L.vf_get_last_stats.restype = C.c_int
+        L.vf_get_last_stats.argtypes = [p, p, C.POINTER(SearchStats)]
+        L.vf_get_last_items.restype = C.c_int
+        L.vf_get_last_items.argtypes = [p, p, i64, p, C.POINTER(i64)]
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != VF_OK:
+        raise VfError(status, lib().vf_last_error().decode())
+
+
+def _ptr(x):
+    """Pointer of a numpy array or a torch tensor (host or device); None for None."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(x.data_ptr())
+
+
+def _dtype_code(X) -> int:
+    dt = str(X.dtype)
+    if dt in ("uint8", "torch.uint8"):
+        return VF_U8
+    if dt in ("float32", "torch.float32"):
+        return VF_F32
+    raise TypeError(f"vectors must be uint8 or float32, got {dt}")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Index:
+    """Device-resident label-centric index: vf_build_index / vf_search / vf_free."""
+
+    def __init__(self, X, post_off, post_ids, threshold_T, degree_R=16, graph_off=None,
+                 graph_ids=None, device=0, world_size=1, rank=0, nccl_unique_id=None):
+        X = np.ascontiguousarray(X)
+        self._keep = [X, np.ascontiguousarray(post_off, np.int64), np.ascontiguousarray(post_ids, np.int32)]
+        self.dtype = _dtype_code(X)
+        self.dim = X.shape[1]
+        self.n_labels = len(post_off) - 1
+        d = BuildDesc()
+        d.n_points, d.dim, d.dtype = X.shape[0], X.shape[1], self.dtype
+        d.vectors = _ptr(X)
+        d.n_labels = self.n_labels
+        d.posting_offsets, d.posting_ids = _ptr(self._keep[1]), _ptr(self._keep[2])
+        d.threshold_T, d.degree_R = int(threshold_T), int(degree_R)
+        if graph_off is not None:
+            go = np.ascontiguousarray(graph_off, np.int64)
+            gi = np.ascontiguousarray(graph_ids, np.int32)
+            if gi.size == 0:
+                gi = np.full(1, -1, np.int32)
+            self._keep += [go, gi]
+            d.graph_row_offsets, d.graph_local_ids = _ptr(go), _ptr(gi)
+        d.world_size, d.rank, d.device = int(world_size), int(rank), int(device)
+        if nccl_unique_id is not None:
+            self._uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
+            d.nccl_unique_id = C.cast(self._uid, C.c_void_p)
+        h = C.c_void_p()
+        _check(lib().vf_build_index(C.byref(d), C.byref(h)))
+        self._h = h
+        self._keep = None   # the library copied everything
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().vf_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = IndexInfo()
+        _check(lib().vf_get_index_info(self._h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in i._fields_}
+
+    def set_profiling(self, enable=True):
+        _check(lib().vf_set_profiling(self._h, 1 if enable else 0))
+
+    def search_into(self, Q, q_off, q_lab, out_ids, out_dists, k=10, itopk=64, op="single",
+                    recall_mode="greedy", exact=False, search_width=1, n_init=0, max_iterations=0,
+                    seed=0x5EED1234, stream=None):
+        """vf_search with caller-provided buffers (numpy host arrays or torch tensors on either
+        side). Asynchronous on `stream` when the outputs are device tensors."""
+        p = SearchParams(int(k), int(itopk), int(search_width), int(n_init), int(max_iterations),
+                         int(seed) & 0xFFFFFFFF, OPS[op] if isinstance(op, str) else int(op),
+                         MODES[recall_mode] if isinstance(recall_mode, str) else int(recall_mode),
+                         1 if exact else 0)
+        n = int(q_off.shape[0]) - 1
+        _check(lib().vf_search(self._h, _ptr(Q), n, _ptr(q_off), _ptr(q_lab), C.byref(p),
+                               _ptr(out_ids), _ptr(out_dists), _stream_ptr(stream)))
+
+    def search(self, Q, q_off, q_lab, k=10, **kw):
+        """Host convenience wrapper: numpy in, numpy out (blocks)."""
+        Q = np.ascontiguousarray(Q)
+        q_off = np.ascontiguousarray(q_off, np.int64)
+        q_lab = np.ascontiguousarray(q_lab, np.int32)
+        if q_lab.size == 0:
+            q_lab = np.zeros(1, np.int32)
+        n = len(q_off) - 1
+        ids = np.empty((n, k), np.int32)
+        d = np.empty((n, k), np.float32)
+        self.search_into(Q, q_off, q_lab, ids, d, k=k, **kw)
+        return ids, d
+
+    def last_stats(self, stream=None) -> dict:
+        s = SearchStats()
+        _check(lib().vf_get_last_stats(self._h, _stream_ptr(stream), C.byref(s)))
+        return s.as_dict()
+
+    def last_items(self, stream=None) -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().vf_get_last_items(self._h, _stream_ptr(stream), 0, None, C.byref(n)))
+        rec = np.empty((max(n.value, 1), 6), np.int32)
+        _check(lib().vf_get_last_items(self._h, _stream_ptr(stream), n.value, _ptr(rec), C.byref(n)))
+        return rec[:n.value]

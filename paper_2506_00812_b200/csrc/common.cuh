@@ -1,0 +1,168 @@
+// Device helpers shared by the kernels: result keys, exact distances, the predicate, warp sort /
+// merge, TMA-bulk + mbarrier wrappers.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "vf_internal.h"
+
+namespace vf {
+
+typedef unsigned long long ull;
+constexpr ull KEY_INF = ~0ull;
+constexpr unsigned FULL = 0xffffffffu;
+
+// A result key orders by (distance, id) (reading #6): the distance is a non-negative float whose
+// IEEE bits order like unsigned integers, placed above the 32-bit id.
+__device__ __forceinline__ ull make_key(float d, uint32_t id) {
+    return ((ull)__float_as_uint(d) << 32) | (ull)id;
+}
+__device__ __forceinline__ float key_dist(ull k) { return __uint_as_float((uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t key_id(ull k) { return (uint32_t)k; }
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+    return h;
+}
+
+// ---------------------------------------------------------------- exact squared-L2 distances
+// One 16-byte chunk of a query against one 16-byte chunk of a data row.
+// u8: |q-x| per byte (vabsdiffu4) then dot of the differences with themselves (dp4a): exact int32.
+// f32: (q-x)^2 accumulated with FFMA in fp32 (exact for integer-valued data < 2^24).
+template <int DT> struct Acc;
+template <> struct Acc<0> {
+    typedef uint32_t T;
+    __device__ __forceinline__ static void add(T &acc, const uint4 &q, const uint4 &x) {
+        uint32_t d;
+        d = __vabsdiffu4(q.x, x.x); acc = __dp4a(d, d, acc);
+        d = __vabsdiffu4(q.y, x.y); acc = __dp4a(d, d, acc);
+        d = __vabsdiffu4(q.z, x.z); acc = __dp4a(d, d, acc);
+        d = __vabsdiffu4(q.w, x.w); acc = __dp4a(d, d, acc);
+    }
+    __device__ __forceinline__ static float to_float(T a) { return (float)a; }
+};
+template <> struct Acc<1> {
+    typedef float T;
+    __device__ __forceinline__ static void add(T &acc, const uint4 &q, const uint4 &x) {
+        float t;
+        t = __uint_as_float(q.x) - __uint_as_float(x.x); acc = fmaf(t, t, acc);
+        t = __uint_as_float(q.y) - __uint_as_float(x.y); acc = fmaf(t, t, acc);
+        t = __uint_as_float(q.z) - __uint_as_float(x.z); acc = fmaf(t, t, acc);
+        t = __uint_as_float(q.w) - __uint_as_float(x.w); acc = fmaf(t, t, acc);
+    }
+    __device__ __forceinline__ static float to_float(T a) { return a; }
+};
+
+// ---------------------------------------------------------------- predicate
+// verify(gid) <=> every label of the sorted query label list P[0..np) except `excl` is in the
+// point's sorted label segment. Boundary-narrowing order of P:L537: smallest, largest, then the
+// middle labels only inside the bracket found by the first two searches.
+__device__ __forceinline__ int64_t bsearch_lab(const int32_t *__restrict__ lab, int64_t lo, int64_t hi,
+                                               int32_t key) {
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        int32_t v = __ldg(lab + mid);
+        if (v == key) return mid;
+        if (v < key) lo = mid + 1; else hi = mid;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ bool verify_pred(const DevIndex &ix, int32_t gid, const int32_t *P, int np,
+                                            int32_t excl) {
+    int i0 = 0, i1 = np - 1;
+    if (i0 <= i1 && P[i0] == excl) i0++;
+    if (i0 <= i1 && P[i1] == excl) i1--;
+    if (i0 > i1) return true;
+    const int64_t lo = __ldg(ix.pt_off + gid), hi = __ldg(ix.pt_off + gid + 1);
+    const int64_t a = bsearch_lab(ix.pt_lab, lo, hi, P[i0]);
+    if (a < 0) return false;
+    if (i0 == i1) return true;
+    const int64_t b = bsearch_lab(ix.pt_lab, a + 1, hi, P[i1]);
+    if (b < 0) return false;
+    for (int t = i0 + 1; t < i1; t++) {
+        if (P[t] == excl) continue;
+        if (bsearch_lab(ix.pt_lab, a + 1, b, P[t]) < 0) return false;
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------- warp sort / merge of keys
+// Bitonic sort of 32 keys, one per lane, ascending across lanes.
+__device__ __forceinline__ ull warp_sort32(ull key, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            ull other = __shfl_xor_sync(FULL, key, j);
+            bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+            ull mn = key < other ? key : other;
+            ull mx = key < other ? other : key;
+            key = keep_min ? mn : mx;
+        }
+    }
+    return key;
+}
+
+// Merge two sorted lists of DISTINCT keys, A[0..na) and C[0..nc) (both in shared memory), into
+// B[0..min(cap, na+nc)) by rank: an element's output position is its index plus the number of
+// elements of the other list smaller than it. Whole warp; returns the new length.
+__device__ __forceinline__ int warp_merge(const ull *A, int na, const ull *C, int nc, ull *B, int cap,
+                                          int lane) {
+    for (int i = lane; i < na; i += 32) {
+        ull a = A[i];
+        int lo = 0, hi = nc;
+        while (lo < hi) { int mid = (lo + hi) >> 1; if (C[mid] < a) lo = mid + 1; else hi = mid; }
+        int pos = i + lo;
+        if (pos < cap) B[pos] = a;
+    }
+    for (int j = lane; j < nc; j += 32) {
+        ull c = C[j];
+        int lo = 0, hi = na;
+        while (lo < hi) { int mid = (lo + hi) >> 1; if (A[mid] < c) lo = mid + 1; else hi = mid; }
+        int pos = j + lo;
+        if (pos < cap) B[pos] = c;
+    }
+    __syncwarp();
+    int n = na + nc;
+    return n < cap ? n : cap;
+}
+
+// ---------------------------------------------------------------- TMA bulk copy + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(addr), "r"(parity) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar` in bytes.
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+}  // namespace vf

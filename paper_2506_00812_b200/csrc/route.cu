@@ -1,0 +1,235 @@
+// a1 -- route and bucket (Alg. 2 "ClassifyQueries"; routing equation; AND/OR
+// policies P:L523). One warp per query pads the query row, hashes its content for
+// the entry sampler, sorts/deduplicates its labels and emits its work items into the query's
+// label slots. Two small grid-stride kernels then turn the per-label bucket counts into scan
+// segments (<= QG queries of one LS label) and row tiles, and scatter the scan items.
+#include "common.cuh"
+
+namespace vf {
+
+// ---------------------------------------------------------------- prepare: pad + hash + route
+__global__ void __launch_bounds__(256) k_prepare(SearchArgs a, const uint8_t *__restrict__ raw,
+                                                 int raw_bytes) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= a.n_q) return;
+    const DevIndex &ix = a.ix;
+
+    // -- padded copy of the query row + content hash (reading c.3: FNV-free, order-independent)
+    const uint8_t *src = raw + q * (int64_t)raw_bytes;
+    uint8_t *dst = const_cast<uint8_t *>(a.Qp) + q * (int64_t)ix.row_bytes;
+    const int nwords = (raw_bytes + 3) >> 2;
+    const int dwords = ix.row_bytes >> 2;
+    uint32_t hacc = 0;
+    for (int w = lane; w < dwords; w += 32) {
+        uint32_t word = 0;
+        if (w < nwords) {
+            if ((raw_bytes & 3) == 0) {
+                word = __ldg(reinterpret_cast<const uint32_t *>(src) + w);
+            } else {
+                for (int t = 0; t < 4; t++) {
+                    int p = w * 4 + t;
+                    uint32_t b = p < raw_bytes ? (uint32_t)__ldg(src + p) : 0u;
+                    word |= b << (8 * t);
+                }
+            }
+            hacc += fmix32(word + (uint32_t)w * 0x9E3779B9u);
+        }
+        reinterpret_cast<uint32_t *>(dst)[w] = word;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hacc += __shfl_xor_sync(FULL, hacc, o);
+    const uint32_t qh = fmix32(hacc);
+
+    // -- labels: sort + dedup (reading #22), lane 0 (queries carry a handful of labels)
+    const int64_t lo = a.q_off[q], hi = a.q_off[q + 1];
+    const int nraw = (int)(hi - lo);
+    int32_t *L = a.qlab + lo;   // sorted in place (the device copy of the caller's labels)
+    int nl = 0, n_items = 0;
+    if (lane == 0) {
+        for (int i = 1; i < nraw; i++) {          // insertion sort
+            int32_t v = L[i];
+            int j = i - 1;
+            while (j >= 0 && L[j] > v) { L[j + 1] = L[j]; j--; }
+            L[j + 1] = v;
+        }
+        for (int i = 0; i < nraw; i++)
+            if (nl == 0 || L[i] != L[nl - 1]) L[nl++] = L[i];
+        // routing: size 0 = empty / unknown label (reading #19)
+        auto lsize = [&](int32_t l) -> int32_t {
+            return (l >= 0 && l < ix.n_labels) ? ix.dir[l].size : 0;
+        };
+        auto path_of = [&](int32_t l) -> uint32_t {
+            int32_t s = lsize(l);
+            if (s == 0) return PATH_NONE;
+            return (a.exact || s < ix.T) ? PATH_SCAN : PATH_GRAPH;
+        };
+        // items occupy slots lo + t; unused slots are marked NONE
+        uint32_t pred = 0;
+        int32_t chosen[kMaxQueryLabels];
+        int nch = 0;
+        if (a.op == 0 || a.op == 1) {             // SINGLE / OR: one item per non-empty label
+            if (!(a.op == 0 && nl > 1))
+                for (int t = 0; t < nl; t++) if (lsize(L[t]) > 0) chosen[nch++] = L[t];
+        } else {                                  // AND
+            bool any_empty = nl == 0;
+            for (int t = 0; t < nl; t++) any_empty |= lsize(L[t]) == 0;
+            if (!any_empty) {
+                pred = nl > 1 ? META_PRED : 0;
+                if (a.recall_mode == 0) {         // greedy: l* = argmin(|C_l|, l)
+                    int best = 0;
+                    for (int t = 1; t < nl; t++) if (lsize(L[t]) < lsize(L[best])) best = t;
+                    chosen[nch++] = L[best];
+                } else {                          // parallel: every label
+                    for (int t = 0; t < nl; t++) chosen[nch++] = L[t];
+                }
+            }
+        }
+        n_items = nch;
+        for (int t = 0; t < nraw; t++) {
+            Item it;
+            it.qid = (int32_t)q;
+            it.rank = 0;
+            if (t < nch) {
+                int32_t l = chosen[t];
+                uint32_t path = path_of(l);
+                it.label = l;
+                it.meta = path | pred | (nch == 1 ? META_DIRECT : 0u);
+                if (path == PATH_SCAN) {
+                    it.rank = atomicAdd(a.ls_count + ix.dir[l].ls_slot, 1);
+                } else if (path == PATH_GRAPH) {
+                    int pos = atomicAdd(&a.ctr->n_graph, 1);
+                    a.graph_list[pos] = (int32_t)(lo + t);
+                }
+            } else {
+                it.label = -1;
+                it.meta = PATH_NONE;
+            }
+            a.items[lo + t] = it;
+        }
+        QueryInfo qi;
+        qi.nl = nl; qi.n_items = n_items; qi.qh = qh; qi.pad = 0;
+        a.qinfo[q] = qi;
+        if (n_items > 0) atomicAdd(&a.ctr->n_items, n_items);
+    }
+    n_items = __shfl_sync(FULL, n_items, 0);
+    if (n_items == 0) {                           // empty result row: pad (reading #23)
+        for (int t = lane; t < a.k; t += 32) {
+            a.out_ids[q * a.k + t] = -1;
+            a.out_dists[q * a.k + t] = __uint_as_float(0x7f800000u);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- bucket: segments + tiles
+// For the first item (rank 0) of each scanned label: allocate ceil(count / QG) segments and, per
+// segment, ceil(|C_l| / tile_rows) row tiles.
+__global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const Item it = a.items[s];
+        if ((it.meta & 3u) != PATH_SCAN || it.rank != 0) continue;
+        const LabelDir d = a.ix.dir[it.label];
+        const int count = a.ls_count[d.ls_slot];
+        const int nseg = (count + qg - 1) / qg;
+        const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
+        const int seg0 = atomicAdd(&a.ctr->n_segs, nseg);
+        const int ib = atomicAdd(&a.ctr->n_scan_items, count);
+        const int tb = atomicAdd(&a.ctr->n_tiles, nseg * ntile);
+        a.ls_segbase[d.ls_slot] = seg0;
+        a.ls_itembase[d.ls_slot] = ib;
+        for (int g = 0; g < nseg; g++) {
+            Segment sg;
+            sg.label = it.label;
+            sg.item_base = ib + g * qg;
+            sg.n_items = min(qg, count - g * qg);
+            sg.tile_base = tb + g * ntile;
+            sg.n_tiles = ntile;
+            sg.pad[0] = sg.pad[1] = sg.pad[2] = 0;
+            a.segs[seg0 + g] = sg;
+            for (int t = 0; t < ntile; t++) {
+                Tile tl;
+                tl.seg = seg0 + g;
+                tl.row_begin = t * a.tile_rows;
+                tl.row_end = min(d.size, (t + 1) * a.tile_rows);
+                tl.tile_in_seg = t;
+                a.tiles[tb + g * ntile + t] = tl;
+            }
+        }
+    }
+}
+
+__global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        Item it = a.items[s];
+        if ((it.meta & 3u) != PATH_SCAN) continue;
+        const LabelDir d = a.ix.dir[it.label];
+        const int seg = a.ls_segbase[d.ls_slot] + it.rank / qg;
+        a.scan_slots[a.ls_itembase[d.ls_slot] + it.rank] = (int32_t)s;
+        a.item_seg[s] = seg;
+        const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
+        if (ntile > 1) {
+            it.meta = (it.meta & ~META_DIRECT) | META_MULTI;
+            a.items[s] = it;
+        }
+        if (it.rank == 0) a.ls_count[d.ls_slot] = 0;   // bucket counters stay zero between searches
+    }
+}
+
+int launch_prepare(const SearchArgs &a, cudaStream_t s) {
+    if (a.n_q == 0) return 0;
+    const int wpb = 8;
+    const int64_t blocks = (a.n_q + wpb - 1) / wpb;
+    const int raw_bytes = a.ix.dim * (a.ix.dtype == 0 ? 1 : 4);
+    k_prepare<<<(unsigned)blocks, wpb * 32, 0, s>>>(a, a.Qraw, raw_bytes);
+    return 1;
+}
+
+int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg) {
+    if (n_slots == 0) return 0;
+    int64_t blocks = (n_slots + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_segments<<<(unsigned)blocks, 256, 0, s>>>(a, n_slots, qg);
+    k_scatter<<<(unsigned)blocks, 256, 0, s>>>(a, n_slots, qg);
+    return 2;
+}
+
+// ---------------------------------------------------------------- build-time helpers
+__global__ void k_gather_rows(const uint8_t *__restrict__ X, int row_bytes, const int32_t *__restrict__ ids,
+                              int64_t n, uint8_t *__restrict__ out) {
+    const int words = row_bytes >> 4;
+    const int64_t total = n * words;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / words;
+        const int c = (int)(e - r * words);
+        reinterpret_cast<uint4 *>(out + r * row_bytes)[c] =
+            __ldg(reinterpret_cast<const uint4 *>(X + (int64_t)ids[r] * row_bytes) + c);
+    }
+}
+
+__global__ void k_pad_rows(const uint8_t *__restrict__ src, int src_bytes, int64_t n, int row_bytes,
+                           uint8_t *__restrict__ dst) {
+    const int64_t total = n * row_bytes;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / row_bytes;
+        const int c = (int)(e - r * row_bytes);
+        dst[e] = c < src_bytes ? src[r * src_bytes + c] : 0;
+    }
+}
+
+void launch_gather_rows(const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint8_t *out,
+                        cudaStream_t s) {
+    if (n == 0) return;
+    k_gather_rows<<<148 * 8, 256, 0, s>>>(X, row_bytes, ids, n, out);
+}
+
+void launch_pad_rows(const uint8_t *src, int src_bytes, int64_t n, int row_bytes, uint8_t *dst,
+                     cudaStream_t s) {
+    if (n == 0) return;
+    k_pad_rows<<<148 * 8, 256, 0, s>>>(src, src_bytes, n, row_bytes, dst);
+}
+
+}  // namespace vf

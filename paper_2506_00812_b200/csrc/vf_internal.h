@@ -1,0 +1,141 @@
+// Internal types shared by the host orchestration (vf_api.cpp) and the CUDA kernels.
+// Nothing here is part of the C-ABI (include/vf.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vf {
+
+constexpr int kMaxQueryLabels = 64;   // labels per query accepted by vf_search
+constexpr int kMaxK = 256;
+constexpr int kMaxItopk = 1024;
+constexpr int kScanQG = 64;           // queries per scan segment (query group)
+constexpr int kWarpsPerGraphCta = 4;
+
+enum Path : uint32_t { PATH_NONE = 0, PATH_SCAN = 1, PATH_GRAPH = 2 };
+
+// Per-label directory entry (the label metadata of P:L369 / P:L471: size, offset, kind).
+struct LabelDir {
+    int64_t base;     // first row of the label in G_HS/M_HS (HS) or X_LS/M_LS (LS)
+    int32_t size;     // |C_l| (0 = empty or not owned by this rank)
+    int32_t ls_slot;  // >= 0: LS label slot (index of its bucket counter); -1: HS label
+};
+
+// Device-resident index (Alg. 1 output), one per rank.
+struct DevIndex {
+    int32_t dtype;         // 0 u8, 1 f32
+    int32_t dim;
+    int32_t row_bytes;     // padded row, multiple of 16
+    int32_t chunks;        // row_bytes / 16
+    int64_t n_points;
+    int32_t n_labels;
+    int32_t T;
+    int32_t R;
+    int32_t n_ls_labels;
+    const uint8_t *X;      // [n_points][row_bytes]  global vectors (one copy)
+    const LabelDir *dir;   // [n_labels]
+    const int32_t *G;      // [hs_rows][R] local ids (G_HS)
+    const int32_t *M_hs;   // [hs_rows] local -> global (M_HS)
+    const uint8_t *Xls;    // [ls_rows][row_bytes] label-contiguous LS copies (X_LS)
+    const int32_t *M_ls;   // [ls_rows] (M_LS)
+    const int64_t *pt_off; // [n_points+1] predicate table offsets
+    const int32_t *pt_lab; // sorted labels per point
+};
+
+// Work item (a1): one (query, label) search (Alg. 2 L418 / L428 "(q, l)").
+struct Item {
+    int32_t qid;
+    int32_t label;
+    int32_t rank;      // scan items: position within the label bucket
+    uint32_t meta;     // bits 0-1 path, bit 2 has_pred, bit 3 direct, bit 4 multi_tile
+};
+constexpr uint32_t META_PRED = 4u, META_DIRECT = 8u, META_MULTI = 16u;
+
+struct QueryInfo {
+    int32_t nl;        // deduplicated label count
+    int32_t n_items;
+    uint32_t qh;       // content hash (entry sampler, reading c.3)
+    int32_t pad;
+};
+
+// A scan segment: one LS label with up to kScanQG of its items (a2: "query group x posting list").
+struct Segment {
+    int32_t label;
+    int32_t item_base;   // first entry in scan_slots
+    int32_t n_items;
+    int32_t tile_base;   // first tile of this segment
+    int32_t n_tiles;
+    int32_t pad[3];
+};
+
+struct Tile {
+    int32_t seg;
+    int32_t row_begin;   // rows relative to the label's first LS row
+    int32_t row_end;
+    int32_t tile_in_seg;
+};
+
+// Device counters, zeroed at the start of every search.
+struct Counters {
+    int32_t n_graph;
+    int32_t n_segs;
+    int32_t n_scan_items;
+    int32_t n_tiles;
+    int32_t scan_next;
+    int32_t graph_next;
+    int32_t n_items;
+    int32_t pad;
+    unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
+    unsigned long long graph_V_max;
+};
+
+struct SearchArgs {
+    DevIndex ix;
+    int64_t n_q;
+    const uint8_t *Qraw;      // [n_q][dim * elem] caller's query rows (device copy if needed)
+    const uint8_t *Qp;        // [n_q][row_bytes] padded queries
+    const int64_t *q_off;     // [n_q+1]
+    int32_t *qlab;            // sorted/dedup labels per query (CSR with q_off)
+    QueryInfo *qinfo;
+    Item *items;              // [q_off[n_q]] slots
+    int32_t *item_ctr;        // [slots][3] V, E, iterations (graph items)
+    int32_t *ls_count;        // [n_ls_labels]
+    int32_t *ls_segbase;      // [n_ls_labels] first segment of the label
+    int32_t *ls_itembase;     // [n_ls_labels] first scan_slots entry of the label
+    int32_t *graph_list;      // [slots]
+    int32_t *scan_slots;      // [slots]
+    Segment *segs;            // [slots]
+    Tile *tiles;              // [max_tiles]
+    int32_t *item_seg;        // [slots] segment of a scan item (multi-tile merge)
+    unsigned long long *item_res;   // [slots][k] keys
+    unsigned long long *partials;   // [slots][max_tiles_per_label][k] keys (multi-tile only)
+    Counters *ctr;
+    int32_t *out_ids;         // [n_q][k]
+    float *out_dists;
+    int32_t k, itopk, w, n_init, max_iter;
+    uint32_t seed;
+    int32_t op, recall_mode, exact;
+    int32_t tile_rows;
+    int32_t max_tiles_per_label;
+    int32_t max_tiles;
+    int32_t hash_slots;       // smem visited table size (power of two)
+    int64_t gtab_slots;       // per-warp global overflow table size (power of two)
+    unsigned long long *gtab; // [n_warp_slots][gtab_slots]
+    int32_t n_warp_slots;
+};
+
+// Launchers (implemented in the .cu files); each returns the number of kernels launched.
+int launch_prepare(const SearchArgs &a, cudaStream_t s);   // pad queries + route (a1)
+int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg); // segments, tiles, scatter (a1)
+int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // a2
+int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
+int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
+int launch_finish_keys(const SearchArgs &a, cudaStream_t s);
+int graph_smem_bytes(const SearchArgs &a);
+int graph_max_ctas(const SearchArgs &a);
+void launch_gather_rows(const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint8_t *out,
+                        cudaStream_t s);
+void launch_pad_rows(const uint8_t *src, int src_bytes, int64_t n, int row_bytes, uint8_t *dst,
+                     cudaStream_t s);
+
+}  // namespace vf
