@@ -1,0 +1,388 @@
+#!/usr/bin/env python3
+"""bench.py -- QPS at recall@10 >= 0.90 / 0.99 for batched label-filtered top-k search on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config sift|yfcc|tiny] [--impl ours|reference]
+
+A "step" is one vf_search call over the whole query batch of the workload (route -> scan ->
+graph -> merge, all §8(a) rows) with queries, labels and outputs resident in HBM. The workload is
+BASELINE.json configs[1] (SIFT-like: 1M x 128 fp32 integer-valued vectors, 1K Zipf labels, 10K
+single-label queries, k = 10) unless --config says otherwise; see DESIGN.md §3 for the recipe.
+
+Ground truth comes from vf_search in exact mode (T = infinity; parity-tested bit-exact against the
+CPU oracle in tests/). The operating point for a recall target is the smallest itopk of the grid
+whose mean recall@10 reaches it. L2 is flushed (256 MiB write) before every timed step, outside
+the step's CUDA events. Under torchrun (N > 1) every rank holds the index and runs its own batch
+(weak scaling); rank 0 prints the line with value = all ranks' queries / max-over-ranks time.
+The CPU oracle is used ONLY for the cpu_baseline leg and for --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ITOPK_GRID = (16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512)
+METRIC = "QPS at recall@10 >=0.90 and >=0.99 (1/2/4/8 B200); p50 latency at batch 1"
+
+
+def log(*a):
+    if int(os.environ.get("RANK", "0")) == 0:
+        print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- workload
+def make_inputs(config: str, device):
+    from workload import gen, graphs
+    t0 = time.time()
+    w = gen.make_workload(config)
+    c = w.cfg
+    log(f"workload {config}: N={c.n_points} D={c.dim} L={c.n_labels} Q={c.n_queries} "
+        f"dtype={c.dtype} ({time.time() - t0:.1f}s)")
+    t0 = time.time()
+    go, gi = graphs.build_graphs(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, device=device)
+    log(f"fixture graphs: {int((np.diff(go) > 0).sum())} HS labels, {int(go[-1])} rows ({time.time() - t0:.1f}s)")
+    return w, go, gi
+
+
+def recall_vs(ids, d, gt, gd, k):
+    """(strict, tie-aware) recall@k against the exact ground truth (reading #24)."""
+    strict, tie = [], []
+    for i in range(ids.shape[0]):
+        g = gt[i][gt[i] >= 0]
+        if g.size == 0:
+            continue
+        a = ids[i][ids[i] >= 0]
+        hits = np.intersect1d(a, g).size
+        kth = gd[i][g.size - 1]
+        extra = int(np.sum((~np.isin(a, g)) & (d[i][:a.size] == kth)))
+        den = min(k, g.size)
+        strict.append(hits / den)
+        tie.append(min(1.0, (hits + extra) / den))
+    return float(np.mean(strict)), float(np.mean(tie))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.samples = []
+        self.stop = threading.Event()
+        self.gpu = gpu_index
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                if len(f) == 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for s in self.samples for j in range(4) if s[2 + j].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, config):
+    """The oracle, as it stands, on the host cores (the reference arm for this tier)."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w, go, gi = make_inputs(config, None)
+    c = w.cfg
+    o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
+    n = min(len(w.Q), args.ref_sample)
+    Q, qo, ql = w.Q[:n], w.q_off[:n + 1], w.q_lab[:w.q_off[n]]
+    threads = os.cpu_count() or 1
+    itopk = args.ref_itopk
+    op = "and" if c.query_mode in ("and2", "mix_and") else ("or" if c.query_mode == "or2" else "single")
+    for _ in range(args.warmup):
+        o.search(Q[:64], qo[:65], ql[:qo[64]], k=c.k, itopk=itopk, op=op, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.search(Q, qo, ql, k=c.k, itopk=itopk, op=op, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    total = float(np.sum(times))
+    qps = n * args.steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": config, "n_queries_per_step": n, "itopk": itopk,
+                                             "k": c.k, "flush": "n/a (CPU)"},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {n} queries of the {config} batch per step, itopk={itopk}"},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="sift", choices=["tiny", "sift", "yfcc"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--targets", default="0.90,0.99")
+    ap.add_argument("--cpu-sample", type=int, default=2000)
+    ap.add_argument("--ref-sample", type=int, default=1000)
+    ap.add_argument("--ref-itopk", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-stats", default=None)
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference(args, args.config)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2506_00812_b200 as vf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    w, go, gi = make_inputs(args.config, dev)
+    c = w.cfg
+    t0 = time.time()
+    ix = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi, device=local)
+    info = ix.info()
+    log(f"vf_build_index: {info['bytes_total'] / 2**30:.2f} GiB on device ({time.time() - t0:.1f}s)")
+    op = "and" if c.query_mode in ("and2", "mix_and") else ("or" if c.query_mode == "or2" else "single")
+    n = len(w.Q)
+    k = c.k
+    stream = torch.cuda.current_stream()
+    Q = torch.from_numpy(w.Q).to(dev)
+    qo = torch.from_numpy(w.q_off).to(dev)
+    ql = torch.from_numpy(w.q_lab).to(dev)
+    ids = torch.empty((n, k), dtype=torch.int32, device=dev)
+    dd = torch.empty((n, k), dtype=torch.float32, device=dev)
+
+    # -- ground truth: exact mode (T = inf), in query chunks
+    t0 = time.time()
+    gt = np.empty((n, k), np.int32)
+    gd = np.empty((n, k), np.float32)
+    step = 2000
+    for s in range(0, n, step):
+        e = min(n, s + step)
+        Qs, qos, qls = Q[s:e], qo[s:e + 1] - qo[s], ql[int(w.q_off[s]):int(w.q_off[e])]
+        ti = torch.empty((e - s, k), dtype=torch.int32, device=dev)
+        td = torch.empty((e - s, k), dtype=torch.float32, device=dev)
+        ix.search_into(Qs, qos.contiguous(), qls.contiguous(), ti, td, k=k, op=op, exact=True, stream=stream)
+        torch.cuda.synchronize()
+        gt[s:e], gd[s:e] = ti.cpu().numpy(), td.cpu().numpy()
+    log(f"ground truth (exact mode): {time.time() - t0:.1f}s")
+
+    # -- itopk sweep -> operating points
+    targets = [float(x) for x in args.targets.split(",")]
+    sweep = []
+    for itopk in ITOPK_GRID:
+        ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, op=op, stream=stream)
+        torch.cuda.synchronize()
+        r_strict, r_tie = recall_vs(ids.cpu().numpy(), dd.cpu().numpy(), gt, gd, k)
+        sweep.append((itopk, r_strict, r_tie))
+        log(f"itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f}")
+        if r_tie >= max(targets) and itopk >= 32:
+            break
+    ops = {}
+    for tgt in targets:
+        ok = [s for s in sweep if s[2] >= tgt]
+        ops[tgt] = ok[0] if ok else None
+
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
+    ix.set_profiling(True)
+    hbm_peak, peak_kind = measured_peaks()
+
+    def timed(itopk):
+        """W warm-up + exactly K timed steps; per-step CUDA events around vf_search only."""
+        for _ in range(args.warmup):
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, op=op, stream=stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        stats = []
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, op=op, stream=stream)
+            ev[i][1].record(stream)
+            stats.append(ix.last_stats(stream))   # syncs; between steps, outside the events
+        torch.cuda.synchronize()
+        barrier()
+        ms = [a.elapsed_time(b) for a, b in ev]
+        return ms, stats
+
+    results = {}
+    with ClockSampler(local) as clk:
+        for tgt, opnt in ops.items():
+            if opnt is None:
+                continue
+            itopk = opnt[0]
+            ms, stats = timed(itopk)
+            tot = float(np.sum(ms))
+            if world > 1:
+                t = torch.tensor([tot], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                tot = float(t.item())
+            results[tgt] = (itopk, opnt, ms, stats, tot)
+    clocks = clk.summary()
+
+    # -- end to end through the C-ABI with host (pinned) buffers, copies inside the timed region
+    main_tgt = targets[0]
+    e2e = None
+    if main_tgt in results:
+        itopk = results[main_tgt][0]
+        Qh = torch.from_numpy(w.Q).pin_memory()
+        qoh = torch.from_numpy(w.q_off).pin_memory()
+        qlh = torch.from_numpy(w.q_lab).pin_memory()
+        oih = torch.empty((n, k), dtype=torch.int32).pin_memory()
+        odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
+        for _ in range(args.warmup):
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, op=op, stream=stream)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, op=op, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([et], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        h2d = Qh.numel() * Qh.element_size() + qoh.numel() * 8 + qlh.numel() * 4
+        d2h = n * k * 8
+        e2e = {"value": n * world * args.steps / (et / 1000.0), "unit": "queries/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # -- CPU baseline: the oracle on this host's cores, bounded sample, rank 0 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
+        import oracle
+        itopk = results[main_tgt][0]
+        o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
+        m = min(n, args.cpu_sample)
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], k=k, itopk=itopk, op=op, nthreads=threads)
+        el = time.perf_counter() - t0
+        cpu = {"value": m / el, "unit": "queries/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {m} of the {n} queries, itopk={itopk}, {threads} threads, {el:.1f}s"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    if main_tgt not in results:
+        print(json.dumps({"metric": METRIC, "value": None, "error": "recall target not reached",
+                          "sweep": sweep}), flush=True)
+        return
+    itopk, opnt, ms, stats, tot = results[main_tgt]
+    K = args.steps
+    qps = n * world * K / (tot / 1000.0)
+    # roofline of the dominant kernel (graph beam search): algorithmic bytes / kernel time
+    s0 = stats[-1]
+    rb = s0["row_bytes"]
+    R = c.degree_R
+    g_bytes = s0["graph_V"] * (rb + 4) + s0["graph_E"] * R * 4
+    g_ms = float(np.mean([s["ms_graph"] for s in stats]))
+    s_bytes = s0["scan_rows"] * (rb + 4)
+    s_ms = float(np.mean([s["ms_scan"] for s in stats]))
+    dom = "graph" if g_ms >= s_ms else "scan"
+    bytes_dom, ms_dom = (g_bytes, g_ms) if dom == "graph" else (s_bytes, s_ms)
+    achieved = bytes_dom / (ms_dom / 1000.0) / 1e9 if ms_dom > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": tot / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if c.dtype != "u8" else "u8", "data": "synthetic",
+        "config": {"workload": f"{args.config} (BASELINE.json configs[{ {'tiny': 0, 'sift': 1, 'yfcc': 2}[args.config]}])",
+                   "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
+                   "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
+                   "R": R, "itopk": itopk, "recall_target": main_tgt,
+                   "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
+                   "flush": "256 MiB L2 flush before every timed step (outside the step events)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "at_recall": {f"{t:.2f}": {"itopk": r[0], "qps": n * world * K / (r[4] / 1000.0),
+                                   "ms_per_step": r[4] / K, "recall_strict": r[1][1],
+                                   "recall_tie_aware": r[1][2]} for t, r in results.items()},
+        "sweep": [{"itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2]} for s in sweep],
+        "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": int(bytes_dom),
+                     "kernel_ms_per_launch": ms_dom},
+        "phases_ms": {p: float(np.mean([s[f"ms_{p}"] for s in stats]))
+                      for p in ("route", "scan", "graph", "merge", "copy", "total")},
+        "work": {kk: s0[kk] for kk in ("n_items", "n_scan_items", "n_graph_items", "n_segments",
+                                       "scan_rows", "graph_V", "graph_E", "graph_iterations", "graph_V_max")},
+        "gpu_launches": int(s0["kernel_launches"] * K),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "index_bytes": info["bytes_total"],
+    }
+    if args.dump_stats:
+        with open(args.dump_stats, "w") as f:
+            json.dump({"stats": stats, "ms": ms}, f)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) k_prepare(SearchArgs a, const uint8_t *__
                 it.label = l;
                 it.meta = path | pred | (nch == 1 ? META_DIRECT : 0u);
                 if (path == PATH_SCAN) {
-                    it.rank = atomicAdd(a.ls_count + ix.dir[l].ls_slot, 1);
+                    it.rank = atomicAdd(a.ls_count + ix.dir[l].bslot, 1);
                 } else if (path == PATH_GRAPH) {
                     int pos = atomicAdd(&a.ctr->n_graph, 1);
                     a.graph_list[pos] = (int32_t)(lo + t);
@@ -130,14 +130,14 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
         const Item it = a.items[s];
         if ((it.meta & 3u) != PATH_SCAN || it.rank != 0) continue;
         const LabelDir d = a.ix.dir[it.label];
-        const int count = a.ls_count[d.ls_slot];
+        const int count = a.ls_count[d.bslot];
         const int nseg = (count + qg - 1) / qg;
         const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
         const int seg0 = atomicAdd(&a.ctr->n_segs, nseg);
         const int ib = atomicAdd(&a.ctr->n_scan_items, count);
         const int tb = atomicAdd(&a.ctr->n_tiles, nseg * ntile);
-        a.ls_segbase[d.ls_slot] = seg0;
-        a.ls_itembase[d.ls_slot] = ib;
+        a.ls_segbase[d.bslot] = seg0;
+        a.ls_itembase[d.bslot] = ib;
         for (int g = 0; g < nseg; g++) {
             Segment sg;
             sg.label = it.label;
@@ -165,15 +165,15 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
         Item it = a.items[s];
         if ((it.meta & 3u) != PATH_SCAN) continue;
         const LabelDir d = a.ix.dir[it.label];
-        const int seg = a.ls_segbase[d.ls_slot] + it.rank / qg;
-        a.scan_slots[a.ls_itembase[d.ls_slot] + it.rank] = (int32_t)s;
+        const int seg = a.ls_segbase[d.bslot] + it.rank / qg;
+        a.scan_slots[a.ls_itembase[d.bslot] + it.rank] = (int32_t)s;
         a.item_seg[s] = seg;
         const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
         if (ntile > 1) {
             it.meta = (it.meta & ~META_DIRECT) | META_MULTI;
             a.items[s] = it;
         }
-        if (it.rank == 0) a.ls_count[d.ls_slot] = 0;   // bucket counters stay zero between searches
+        if (it.rank == 0) a.ls_count[d.bslot] = 0;   // bucket counters stay zero between searches
     }
 }
 

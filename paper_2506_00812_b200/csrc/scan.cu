@@ -115,34 +115,50 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     __syncthreads();
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        if (lane == 0) {
-            uint32_t n = 0;
-            const int ntiles = a.ctr->n_tiles;
-            for (;;) {
-                const int t = atomicAdd(&a.ctr->scan_next, 1);
-                if (t >= ntiles) {
+        // ------------------------------------------------------------ producer (warp 0)
+        // LS labels: one bulk copy of the tile's contiguous X_LS rows per stage. In exact mode an
+        // HS label is scanned too; its rows are gathered from X through M_HS, one bulk copy per row
+        // issued by all 32 lanes (no duplicated vectors).
+        uint32_t n = 0;
+        const int ntiles = a.ctr->n_tiles;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
+            t = __shfl_sync(FULL, t, 0);
+            if (t >= ntiles) {
+                if (lane == 0) {
                     const int slot = n % nst;
                     mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
                     meta[slot] = make_int4(-1, 0, 0, ST_END);
                     mbar_arrive(full + slot);
-                    break;
                 }
-                const Tile tl = a.tiles[t];
-                const Segment sg = a.segs[tl.seg];
-                const int64_t base = ix.dir[sg.label].base;
-                for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += rps) {
-                    const int nr = min(rps, tl.row_end - r0);
-                    const int slot = n % nst;
+                break;
+            }
+            const Tile tl = a.tiles[t];
+            const Segment sg = a.segs[tl.seg];
+            const LabelDir d = ix.dir[sg.label];
+            const bool hs = d.size >= ix.T;
+            for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += rps) {
+                const int nr = min(rps, tl.row_end - r0);
+                const int slot = n % nst;
+                uint8_t *dst = stages + (size_t)slot * rps * row_bytes;
+                const uint32_t bytes = (uint32_t)nr * row_bytes;
+                if (lane == 0) {
                     mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
                     const int flags = (r0 == tl.row_begin ? ST_FIRST : 0) | (r0 + nr >= tl.row_end ? ST_LAST : 0);
                     meta[slot] = make_int4(t, r0, nr, flags);
-                    const uint32_t bytes = (uint32_t)nr * row_bytes;
                     mbar_arrive_expect_tx(full + slot, bytes);
-                    tma_load_1d(stages + (size_t)slot * rps * row_bytes,
-                                ix.Xls + (base + r0) * (int64_t)row_bytes, bytes, full + slot);
-                    n++;
+                    if (!hs) tma_load_1d(dst, ix.Xls + (d.base + r0) * (int64_t)row_bytes, bytes, full + slot);
                 }
+                __syncwarp();
+                if (hs) {
+                    for (int r = lane; r < nr; r += 32) {
+                        const int32_t gid = __ldg(ix.M_hs + d.base + r0 + r);
+                        tma_load_1d(dst + (size_t)r * row_bytes, ix.X + (int64_t)gid * row_bytes,
+                                    (uint32_t)row_bytes, full + slot);
+                    }
+                }
+                n++;
             }
         }
         return;
@@ -158,6 +174,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     ull *fin2 = tmp + k;
     int nq = 0, label = 0, tile_in_seg = 0;
     int64_t lbase = 0;
+    const int32_t *gmap = ix.M_ls;   // local row -> global id (M_LS, or M_HS in exact mode)
     unsigned long long my_rows = 0, my_qrows = 0;
     uint32_t n = 0;
     for (;;) {
@@ -173,6 +190,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
             label = sg.label;
             tile_in_seg = tl.tile_in_seg;
             lbase = ix.dir[label].base;
+            gmap = ix.dir[label].size >= ix.T ? ix.M_hs : ix.M_ls;
             if (ct < nq) {
                 const int s = a.scan_slots[sg.item_base + ct];
                 const Item it = a.items[s];
@@ -196,7 +214,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
         const bool valid = ct < nr;
         const uint4 *rowp = reinterpret_cast<const uint4 *>(stages + (size_t)slot * rps * row_bytes +
                                                             (size_t)ct * row_bytes);
-        const int32_t gid = valid ? __ldg(ix.M_ls + lbase + m.y + ct) : -1;
+        const int32_t gid = valid ? __ldg(gmap + lbase + m.y + ct) : -1;
         const int rot = ct % chunks;
         for (int g0 = 0; g0 < nq; g0 += 8) {
             typename A::T acc[8];

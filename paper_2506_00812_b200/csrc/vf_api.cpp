@@ -219,13 +219,14 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     std::vector<int32_t> m_hs((size_t)std::max<int64_t>(hs_rows, 1)), m_ls((size_t)std::max<int64_t>(ls_rows, 1));
     std::vector<int32_t> g_hs((size_t)std::max<int64_t>(hs_rows * R, 1));
     int64_t hb = 0, lb = 0;
-    int32_t ls_slot = 0;
+    int32_t bslot = 0;
     for (int l = 0; l < L; l++) {
         const int64_t a = po[l], S = po[l + 1] - po[l];
         dir[l].size = (int32_t)S;
-        dir[l].ls_slot = -1;
+        dir[l].bslot = -1;
         dir[l].base = 0;
         if (S == 0) continue;
+        dir[l].bslot = bslot++;
         if (S >= T) {
             dir[l].base = hb;
             std::memcpy(&m_hs[hb], pi + a, S * sizeof(int32_t));
@@ -233,7 +234,6 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
             hb += S;
         } else {
             dir[l].base = lb;
-            dir[l].ls_slot = ls_slot++;
             std::memcpy(&m_ls[lb], pi + a, S * sizeof(int32_t));
             lb += S;
         }
@@ -277,7 +277,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     D.n_labels = L;
     D.T = T;
     D.R = R;
-    D.n_ls_labels = ls_slot;
+    D.n_bslots = bslot;
     D.X = ix->X.as<uint8_t>();
     D.dir = ix->dir.as<LabelDir>();
     D.G = ix->G.as<int32_t>();
@@ -448,7 +448,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     VF_CUDA(sc->item_res.ensure((size_t)slots * k * 8));
     if (multi) VF_CUDA(sc->partials.ensure((size_t)slots * mtpl * k * 8));
     VF_CUDA(sc->ctr.ensure(sizeof(Counters)));
-    const size_t nls = (size_t)std::max(D.n_ls_labels, 1);
+    const size_t nls = (size_t)std::max(D.n_bslots, 1);
     VF_CUDA(sc->ls_count.ensure(nls * 4, &fresh));
     if (fresh) VF_CUDA(cudaMemsetAsync(sc->ls_count.p, 0, nls * 4, s));
     VF_CUDA(sc->ls_segbase.ensure(nls * 4));

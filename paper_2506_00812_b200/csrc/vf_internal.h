@@ -18,7 +18,7 @@ enum Path : uint32_t { PATH_NONE = 0, PATH_SCAN = 1, PATH_GRAPH = 2 };
 struct LabelDir {
     int64_t base;     // first row of the label in G_HS/M_HS (HS) or X_LS/M_LS (LS)
     int32_t size;     // |C_l| (0 = empty or not owned by this rank)
-    int32_t ls_slot;  // >= 0: LS label slot (index of its bucket counter); -1: HS label
+    int32_t bslot;    // bucket slot of a non-empty label (index of its scan-bucket counter)
 };
 
 // Device-resident index (Alg. 1 output), one per rank.
@@ -31,7 +31,7 @@ struct DevIndex {
     int32_t n_labels;
     int32_t T;
     int32_t R;
-    int32_t n_ls_labels;
+    int32_t n_bslots;      // non-empty labels (scan-bucket counters)
     const uint8_t *X;      // [n_points][row_bytes]  global vectors (one copy)
     const LabelDir *dir;   // [n_labels]
     const int32_t *G;      // [hs_rows][R] local ids (G_HS)
@@ -99,9 +99,9 @@ struct SearchArgs {
     QueryInfo *qinfo;
     Item *items;              // [q_off[n_q]] slots
     int32_t *item_ctr;        // [slots][3] V, E, iterations (graph items)
-    int32_t *ls_count;        // [n_ls_labels]
-    int32_t *ls_segbase;      // [n_ls_labels] first segment of the label
-    int32_t *ls_itembase;     // [n_ls_labels] first scan_slots entry of the label
+    int32_t *ls_count;        // [n_bslots] scan items per label in this batch
+    int32_t *ls_segbase;      // [n_bslots] first segment of the label
+    int32_t *ls_itembase;     // [n_bslots] first scan_slots entry of the label
     int32_t *graph_list;      // [slots]
     int32_t *scan_slots;      // [slots]
     Segment *segs;            // [slots]
