@@ -148,7 +148,7 @@ typedef struct {
     int32_t row_bytes;                  /* padded vector row (16-byte multiple) */
     int32_t degree_R;
     int64_t bytes_vectors;              /* X: n_points * row_bytes (one shared copy) */
-    int64_t bytes_graph;                /* G_HS: hs_rows * R * 4 */
+    int64_t bytes_graph;                /* G_HS: hs_rows * R * 8 ((local, global) id per edge) */
     int64_t bytes_map_hs;               /* M_HS: hs_rows * 4 */
     int64_t bytes_ls_vectors;           /* X_LS: ls_rows * row_bytes */
     int64_t bytes_map_ls;               /* M_LS: ls_rows * 4 */

@@ -127,6 +127,26 @@ __device__ __forceinline__ int warp_merge(const ull *A, int na, const ull *C, in
     return n < cap ? n : cap;
 }
 
+// Register-resident top-k (k <= 32): lane i holds the i-th best key of a sorted, KEY_INF-padded
+// list. Every lane offers one key; the keys beating the current k-th are inserted one at a time
+// (ballot for the position, shuffle-up to shift) -- a handful of instructions per insertion, no
+// shared-memory sort. Keys must be distinct (they carry the point id).
+__device__ __forceinline__ ull warp_insert_topk(ull Li, ull key, int k, int lane) {
+    unsigned m = __ballot_sync(FULL, key < __shfl_sync(FULL, Li, k - 1));
+    while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const ull kk = __shfl_sync(FULL, key, src);
+        if (kk < __shfl_sync(FULL, Li, k - 1)) {
+            const int pos = __popc(__ballot_sync(FULL, lane < k && Li < kk));
+            const ull up = __shfl_up_sync(FULL, Li, 1);
+            if (lane > pos) Li = up;
+            else if (lane == pos) Li = kk;
+        }
+    }
+    return Li;
+}
+
 // ---------------------------------------------------------------- TMA bulk copy + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);

@@ -8,9 +8,9 @@
 // epoch, so it is never cleared) -- the visited set is exact, never "forgettable", which is what
 // makes the result schedule-independent (reading #12).
 // Per iteration: the first w unexpanded entries of Top become parents (Alg. 2); their G_l
-// rows (R local ids, 64 B at R=16) are read; children are de-duplicated within the batch
-// (match.any), checked/inserted in the visited set, mapped to global ids through M_HS,
-// filtered by the AND predicate, and their vector rows gathered with 16-byte loads by "teams" of
+// rows are read -- each edge carries (local id, global id), i.e. the M_HS mapping of P:L444 is
+// folded into the row so a child costs no dependent M_HS gather; children are de-duplicated within
+// the batch (match.any), checked/inserted in the visited set, filtered by the AND predicate, and their vector rows gathered with 16-byte loads by "teams" of
 // lanes (TEAM lanes per row, up to 8 rows' loads in flight per lane); team-reduced exact distances
 // become keys (dist, local id << 1 | expanded) that are bitonic-sorted across the warp and merged
 // into Top by rank.
@@ -82,12 +82,12 @@ __device__ __forceinline__ void gtab_insert(ull *tab, uint64_t mask, uint32_t ep
 }
 
 template <int DT, int TEAM, int MAXCPL>
-__global__ void __launch_bounds__(32 * kWarpsPerGraphCta) k_graph(SearchArgs a, GraphLayout GL,
+__global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs a, GraphLayout GL,
                                                                   uint32_t *gtab_epoch) {
     extern __shared__ __align__(16) uint8_t smem[];
     typedef Acc<DT> A;
     constexpr int RP = 32 / TEAM;                       // rows per pass
-    constexpr int GROUP = MAXCPL >= 4 ? 2 : 8 / MAXCPL;  // passes whose loads are in flight together
+    constexpr int GROUP = MAXCPL >= 8 ? 1 : (MAXCPL >= 4 ? 2 : 8 / MAXCPL);  // passes in flight together
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int team = lane / TEAM, tl = lane % TEAM;
     uint8_t *wb = smem + (size_t)wid * GL.warp_bytes;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta) k_graph(SearchArgs a, 
 
         // Process one batch of candidate local ids (one per lane, -1 = none): visited-set
         // check/insert, M_HS mapping, predicate, distances, merge into Top.
-        auto process = [&](int32_t c) {
+        auto process = [&](int32_t c, int32_t gid) {
             bool v = c >= 0;
             const unsigned same = __match_any_sync(FULL, v ? c : -1 - lane);
             if (v && (__ffs(same) - 1) != lane) v = false;          // duplicate within the batch
@@ -161,8 +161,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta) k_graph(SearchArgs a, 
             }
             if (nnew) { if (use_smem) n_smem += nnew; else g_used = true; }
             nvis += nnew;
-            int32_t gid = -1;
-            if (isnew) gid = __ldg(ix.M_hs + base + c);
+            if (isnew && gid < 0) gid = __ldg(ix.M_hs + base + c);   // entry samples only
             bool pass = isnew;
             if (pass && has_pred) pass = verify_pred(ix, gid, P, np, it.label);
             const unsigned pm = __ballot_sync(FULL, pass);
@@ -216,7 +215,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta) k_graph(SearchArgs a, 
             int32_t c = -1;
             if (i < n_entry)
                 c = S <= a.n_init ? i : (int32_t)(fmix32(hbase + (uint32_t)i * 0x9E3779B9u) % (uint32_t)S);
-            process(c);
+            process(c, -1);
         }
         // ---- LOOP (Alg. 2)
         for (int iter = 0; iter < a.max_iter; iter++) {
@@ -242,13 +241,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta) k_graph(SearchArgs a, 
             const int nch = npar * R;
             for (int cb = 0; cb < nch; cb += 32) {
                 const int l = cb + lane;
-                int32_t c = -1;
+                int32_t c = -1, cg = -1;
                 if (l < nch) {
                     const int p = spar[l / R];
-                    c = __ldg(ix.G + (base + p) * (int64_t)R + (l % R));
+                    const int2 e = __ldg(ix.G + (base + p) * (int64_t)R + (l % R));
+                    c = e.x;
+                    cg = e.y;
                     if (c < 0 || c >= S) c = -1;                     // reading #15
                 }
-                process(c);
+                process(c, cg);
             }
         }
         // ---- OUTPUT: first min(k, |Top|) entries mapped to global ids (Alg. 2)
@@ -288,15 +289,18 @@ typedef void (*graph_fn)(SearchArgs, GraphLayout, uint32_t *);
 template <int DT>
 static graph_fn pick(int team, int cpl) {
 #define VF_CASE(T_, C_) if (team == T_ && cpl <= C_) return k_graph<DT, T_, C_>;
-    VF_CASE(1, 1) VF_CASE(2, 1) VF_CASE(4, 1) VF_CASE(8, 1) VF_CASE(16, 1)
-    VF_CASE(32, 1) VF_CASE(32, 2) VF_CASE(32, 4) VF_CASE(32, 8)
+    VF_CASE(1, 2) VF_CASE(1, 4) VF_CASE(2, 4) VF_CASE(4, 4) VF_CASE(8, 4) VF_CASE(16, 4)
+    VF_CASE(32, 4) VF_CASE(32, 8)
 #undef VF_CASE
     return nullptr;
 }
 
+// TEAM lanes per row with ~4 16-byte chunks per lane: fewer shuffles per distance than a full
+// warp per row and several rows' loads in flight per lane.
 static void team_for(int chunks, int *team, int *cpl) {
+    const int want = (chunks + 3) / 4;
     int t = 1;
-    while (t < chunks && t < 32) t <<= 1;
+    while (t < want && t < 32) t <<= 1;
     *team = t;
     *cpl = (chunks + t - 1) / t;
 }

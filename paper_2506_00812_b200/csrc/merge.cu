@@ -1,6 +1,5 @@
 // a5 -- "Merge results and map to global IDs" (Alg. 2; OR P:L523; parallel AND P:L555).
-// Per query: the union of its items' top-k lists (and, for scans split into row tiles, of the
-// tiles' partial lists), de-duplicated by global id (reading #20), best k by (dist, gid), padded.
+// Per query: the union of its items' top-k lists, de-duplicated by global id (reading #20), best k by (dist, gid), padded.
 // Queries whose single item already wrote its row directly are skipped. The lists are short
 // (k entries, a handful of items), so one lane per query runs a k-way merge over the list heads.
 #include "common.cuh"
@@ -46,13 +45,7 @@ __global__ void __launch_bounds__(128) k_merge(SearchArgs a) {
     for (int64_t s = lo; s < hi; s++) {
         const Item it = a.items[s];
         if ((it.meta & 3u) == PATH_NONE) continue;
-        if (it.meta & META_MULTI) {
-            const Segment sg = a.segs[a.item_seg[s]];
-            for (int t = 0; t < sg.n_tiles; t++)
-                merge_into(res, &n, tmp, a.partials + ((size_t)s * a.max_tiles_per_label + t) * k, k);
-        } else {
-            merge_into(res, &n, tmp, a.item_res + (size_t)s * k, k);
-        }
+        merge_into(res, &n, tmp, a.item_res + (size_t)s * k, k);
     }
     for (int t = 0; t < k; t++) {
         a.out_ids[q * k + t] = t < n ? (int32_t)key_id(res[t]) : -1;

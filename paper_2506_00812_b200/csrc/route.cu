@@ -8,112 +8,122 @@
 namespace vf {
 
 // ---------------------------------------------------------------- prepare: pad + hash + route
-__global__ void __launch_bounds__(256) k_prepare(SearchArgs a, const uint8_t *__restrict__ raw,
-                                                 int raw_bytes) {
-    const int lane = threadIdx.x & 31;
-    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (q >= a.n_q) return;
+constexpr int kPrepWarps = 32;   // queries per block (block-aggregated atomics)
+
+__global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const uint8_t *__restrict__ raw,
+                                                             int raw_bytes) {
+    __shared__ int s_ngraph[kPrepWarps];
+    __shared__ int s_gbase;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * kPrepWarps + wid;
+    const bool live = q < a.n_q;
     const DevIndex &ix = a.ix;
+    int32_t chosen[kMaxQueryLabels];
+    uint32_t cpath[kMaxQueryLabels];
+    int nch = 0, ngraph = 0, nraw = 0;
+    int64_t lo = 0;
+    uint32_t pred = 0;
 
-    // -- padded copy of the query row + content hash (reading c.3: FNV-free, order-independent)
-    const uint8_t *src = raw + q * (int64_t)raw_bytes;
-    uint8_t *dst = const_cast<uint8_t *>(a.Qp) + q * (int64_t)ix.row_bytes;
-    const int nwords = (raw_bytes + 3) >> 2;
-    const int dwords = ix.row_bytes >> 2;
-    uint32_t hacc = 0;
-    for (int w = lane; w < dwords; w += 32) {
-        uint32_t word = 0;
-        if (w < nwords) {
-            if ((raw_bytes & 3) == 0) {
-                word = __ldg(reinterpret_cast<const uint32_t *>(src) + w);
-            } else {
-                for (int t = 0; t < 4; t++) {
-                    int p = w * 4 + t;
-                    uint32_t b = p < raw_bytes ? (uint32_t)__ldg(src + p) : 0u;
-                    word |= b << (8 * t);
+    if (live) {
+        // -- padded copy of the query row + content hash (reading c.3)
+        const uint8_t *src = raw + q * (int64_t)raw_bytes;
+        uint8_t *dst = const_cast<uint8_t *>(a.Qp) + q * (int64_t)ix.row_bytes;
+        const int nwords = (raw_bytes + 3) >> 2;
+        const int dwords = ix.row_bytes >> 2;
+        uint32_t hacc = 0;
+        for (int w = lane; w < dwords; w += 32) {
+            uint32_t word = 0;
+            if (w < nwords) {
+                if ((raw_bytes & 3) == 0) {
+                    word = __ldg(reinterpret_cast<const uint32_t *>(src) + w);
+                } else {
+                    for (int t = 0; t < 4; t++) {
+                        int p = w * 4 + t;
+                        uint32_t b = p < raw_bytes ? (uint32_t)__ldg(src + p) : 0u;
+                        word |= b << (8 * t);
+                    }
                 }
+                hacc += fmix32(word + (uint32_t)w * 0x9E3779B9u);
             }
-            hacc += fmix32(word + (uint32_t)w * 0x9E3779B9u);
+            reinterpret_cast<uint32_t *>(dst)[w] = word;
         }
-        reinterpret_cast<uint32_t *>(dst)[w] = word;
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) hacc += __shfl_xor_sync(FULL, hacc, o);
-    const uint32_t qh = fmix32(hacc);
+        for (int o = 16; o > 0; o >>= 1) hacc += __shfl_xor_sync(FULL, hacc, o);
+        const uint32_t qh = fmix32(hacc);
 
-    // -- labels: sort + dedup (reading #22), lane 0 (queries carry a handful of labels)
-    const int64_t lo = a.q_off[q], hi = a.q_off[q + 1];
-    const int nraw = (int)(hi - lo);
-    int32_t *L = a.qlab + lo;   // sorted in place (the device copy of the caller's labels)
-    int nl = 0, n_items = 0;
-    if (lane == 0) {
-        for (int i = 1; i < nraw; i++) {          // insertion sort
-            int32_t v = L[i];
-            int j = i - 1;
-            while (j >= 0 && L[j] > v) { L[j + 1] = L[j]; j--; }
-            L[j + 1] = v;
-        }
-        for (int i = 0; i < nraw; i++)
-            if (nl == 0 || L[i] != L[nl - 1]) L[nl++] = L[i];
-        // routing: size 0 = empty / unknown label (reading #19)
-        auto lsize = [&](int32_t l) -> int32_t {
-            return (l >= 0 && l < ix.n_labels) ? ix.dir[l].size : 0;
-        };
-        auto path_of = [&](int32_t l) -> uint32_t {
-            int32_t s = lsize(l);
-            if (s == 0) return PATH_NONE;
-            return (a.exact || s < ix.T) ? PATH_SCAN : PATH_GRAPH;
-        };
-        // items occupy slots lo + t; unused slots are marked NONE
-        uint32_t pred = 0;
-        int32_t chosen[kMaxQueryLabels];
-        int nch = 0;
-        if (a.op == 0 || a.op == 1) {             // SINGLE / OR: one item per non-empty label
-            if (!(a.op == 0 && nl > 1))
-                for (int t = 0; t < nl; t++) if (lsize(L[t]) > 0) chosen[nch++] = L[t];
-        } else {                                  // AND
-            bool any_empty = nl == 0;
-            for (int t = 0; t < nl; t++) any_empty |= lsize(L[t]) == 0;
-            if (!any_empty) {
-                pred = nl > 1 ? META_PRED : 0;
-                if (a.recall_mode == 0) {         // greedy: l* = argmin(|C_l|, l)
-                    int best = 0;
-                    for (int t = 1; t < nl; t++) if (lsize(L[t]) < lsize(L[best])) best = t;
-                    chosen[nch++] = L[best];
-                } else {                          // parallel: every label
-                    for (int t = 0; t < nl; t++) chosen[nch++] = L[t];
+        lo = a.q_off[q];
+        nraw = (int)(a.q_off[q + 1] - lo);
+        int32_t *L = a.qlab + lo;   // the search's private copy of the labels, sorted in place
+        if (lane == 0) {
+            // -- sort + dedup (reading #22)
+            for (int i = 1; i < nraw; i++) {
+                int32_t v = L[i];
+                int j = i - 1;
+                while (j >= 0 && L[j] > v) { L[j + 1] = L[j]; j--; }
+                L[j + 1] = v;
+            }
+            int nl = 0;
+            for (int i = 0; i < nraw; i++)
+                if (nl == 0 || L[i] != L[nl - 1]) L[nl++] = L[i];
+            auto lsize = [&](int32_t l) -> int32_t {
+                return (l >= 0 && l < ix.n_labels) ? ix.dir[l].size : 0;   // reading #19
+            };
+            if (a.op == 0 || a.op == 1) {             // SINGLE / OR: one item per non-empty label
+                if (!(a.op == 0 && nl > 1))
+                    for (int t = 0; t < nl; t++) if (lsize(L[t]) > 0) chosen[nch++] = L[t];
+            } else {                                  // AND
+                bool any_empty = nl == 0;
+                for (int t = 0; t < nl; t++) any_empty |= lsize(L[t]) == 0;
+                if (!any_empty) {
+                    pred = nl > 1 ? META_PRED : 0;
+                    if (a.recall_mode == 0) {         // greedy: l* = argmin(|C_l|, l)
+                        int best = 0;
+                        for (int t = 1; t < nl; t++) if (lsize(L[t]) < lsize(L[best])) best = t;
+                        chosen[nch++] = L[best];
+                    } else {                          // parallel: every label
+                        for (int t = 0; t < nl; t++) chosen[nch++] = L[t];
+                    }
                 }
             }
+            for (int t = 0; t < nch; t++) {           // routing equation
+                const int32_t s = lsize(chosen[t]);
+                cpath[t] = (a.exact || s < ix.T) ? PATH_SCAN : PATH_GRAPH;
+                ngraph += cpath[t] == PATH_GRAPH;
+            }
+            QueryInfo qi;
+            qi.nl = nl; qi.n_items = nch; qi.qh = qh; qi.pad = 0;
+            a.qinfo[q] = qi;
         }
-        n_items = nch;
+    }
+    if (lane == 0) s_ngraph[wid] = ngraph;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0, items = 0;
+        for (int i = 0; i < kPrepWarps; i++) { const int g = s_ngraph[i]; s_ngraph[i] = tot; tot += g; }
+        s_gbase = tot ? atomicAdd(&a.ctr->n_graph, tot) : 0;
+        (void)items;
+    }
+    __syncthreads();
+    if (live && lane == 0) {
+        int gpos = s_gbase + s_ngraph[wid];
         for (int t = 0; t < nraw; t++) {
             Item it;
             it.qid = (int32_t)q;
             it.rank = 0;
             if (t < nch) {
-                int32_t l = chosen[t];
-                uint32_t path = path_of(l);
+                const int32_t l = chosen[t];
                 it.label = l;
-                it.meta = path | pred | (nch == 1 ? META_DIRECT : 0u);
-                if (path == PATH_SCAN) {
-                    it.rank = atomicAdd(a.ls_count + ix.dir[l].bslot, 1);
-                } else if (path == PATH_GRAPH) {
-                    int pos = atomicAdd(&a.ctr->n_graph, 1);
-                    a.graph_list[pos] = (int32_t)(lo + t);
-                }
+                it.meta = cpath[t] | pred | (nch == 1 ? META_DIRECT : 0u);
+                if (cpath[t] == PATH_SCAN) it.rank = atomicAdd(a.ls_count + ix.dir[l].bslot, 1);
+                else a.graph_list[gpos++] = (int32_t)(lo + t);
             } else {
                 it.label = -1;
                 it.meta = PATH_NONE;
             }
             a.items[lo + t] = it;
         }
-        QueryInfo qi;
-        qi.nl = nl; qi.n_items = n_items; qi.qh = qh; qi.pad = 0;
-        a.qinfo[q] = qi;
-        if (n_items > 0) atomicAdd(&a.ctr->n_items, n_items);
     }
-    n_items = __shfl_sync(FULL, n_items, 0);
-    if (n_items == 0) {                           // empty result row: pad (reading #23)
+    if (live && __shfl_sync(FULL, nch, 0) == 0) {    // empty result row: pad (reading #23)
         for (int t = lane; t < a.k; t += 32) {
             a.out_ids[q * a.k + t] = -1;
             a.out_dists[q * a.k + t] = __uint_as_float(0x7f800000u);
@@ -170,7 +180,7 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
         a.item_seg[s] = seg;
         const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
         if (ntile > 1) {
-            it.meta = (it.meta & ~META_DIRECT) | META_MULTI;
+            it.meta |= META_MULTI;       // finalised in the scan kernel (last tile done)
             a.items[s] = it;
         }
         if (it.rank == 0) a.ls_count[d.bslot] = 0;   // bucket counters stay zero between searches
@@ -179,10 +189,9 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
 
 int launch_prepare(const SearchArgs &a, cudaStream_t s) {
     if (a.n_q == 0) return 0;
-    const int wpb = 8;
-    const int64_t blocks = (a.n_q + wpb - 1) / wpb;
+    const int64_t blocks = (a.n_q + kPrepWarps - 1) / kPrepWarps;
     const int raw_bytes = a.ix.dim * (a.ix.dtype == 0 ? 1 : 4);
-    k_prepare<<<(unsigned)blocks, wpb * 32, 0, s>>>(a, a.Qraw, raw_bytes);
+    k_prepare<<<(unsigned)blocks, kPrepWarps * 32, 0, s>>>(a, a.Qraw, raw_bytes);
     return 1;
 }
 

@@ -1,66 +1,37 @@
 // a2 -- IVF-BFS for low-specificity labels (Alg. 2), redesigned
 // for sm_100a as a label-grouped scan: all queries routed to one LS label in this batch (a
 // "segment", up to QG of them) share ONE pass over the label's rows, so every touched posting
-// list is read from HBM once per batch.
+// list is read from HBM once per batch. HBM-bound at every workload (arithmetic
+// intensity ~ 2 x queries-per-label ops/byte), so the design goal is bytes in flight, not FLOPs.
 //
-// Persistent CTAs, warp-specialised:
-//   warp 0 (producer, one elected lane): claims row tiles with an atomic counter and streams each
-//     tile's rows -- contiguous in the label-grouped X_LS store -- into a ring of shared-memory
-//     stages with 1-D TMA bulk copies (cp.async.bulk, completion counted in bytes on an mbarrier).
-//   warps 1-4 (consumers): one row per thread per stage; exact squared L2 against every query of
-//     the segment held in shared memory (u8: vabsdiff4+dp4a int32; f32: FFMA), then a warp top-k
-//     update (ballot against the k-th key, bitonic sort + rank merge only when a key qualifies).
-//     AND items mask rows that fail the predicate (equivalent to the paper's pre-filter, reading
-//     #21). At a tile's last stage the four warp lists are merged and written.
-// The row-to-thread mapping reads the 16-byte chunks of a row in a lane-rotated order, so the 8
-// lanes of a quarter-warp hit 8 different bank groups (conflict-free for 512-byte rows).
+// Persistent CTAs (one per SM), warp-specialised, 288 threads:
+//   warp 0 (producer): claims row tiles (<= tile_rows rows of one segment) with an atomic
+//     counter. Per tile it first prefetches the segment's query rows and item metadata into one of
+//     two query buffers (mbarrier pair qfull/qempty), then streams the tile's rows into a ring of
+//     shared-memory stages: one 1-D TMA bulk copy (cp.async.bulk + mbarrier complete_tx) of the
+//     contiguous X_LS rows per stage; in exact mode an HS label's rows are gathered from X through
+//     M_HS with one bulk copy per row.
+//   warps 1-8 (consumers): "teams" of TS lanes split each row's 16-byte chunks (lane tl owns chunks
+//     tl, tl+TS, ...), so each lane keeps its query chunks in registers; NV rows per team are
+//     accumulated at once and a butterfly reduces the NV x TS partial sums in (NV-1)+log2(TS/NV)
+//     shuffles, leaving one exact distance per "owner" lane (u8: vabsdiff4+dp4a int32; f32: FFMA,
+//     exact for integer-valued data). Per query and warp a top-k list is updated only when a key
+//     beats the k-th (ballot); AND items mask rows failing the predicate (reading #21). At a tile's
+//     end the 8 warp lists are merged; a segment split over several tiles is finalised by the CTA
+//     that completes its last tile (partial lists in global memory, last-block-done counter).
 #include "common.cuh"
 
 namespace vf {
 
-constexpr int kScanConsumers = 4;
+constexpr int kScanConsumers = 8;
 constexpr int kScanThreads = 32 * (1 + kScanConsumers);
 enum : int { ST_FIRST = 1, ST_LAST = 2, ST_END = 4 };
 
 struct ScanLayout {
-    int nst, rps, qg, k, row_bytes;
-    size_t off_full, off_empty, off_meta, off_stage, off_q, off_lists, off_lcnt, off_scratch,
-        off_qmeta, total;
+    int nst, rps, qg, k, row_bytes, ts, cpl;
+    size_t off_full, off_empty, off_qfull, off_qempty, off_meta, off_tinfo, off_stage, off_qbuf,
+        off_qmeta, off_lists, off_lcnt, off_scratch, off_flag, total;
 };
-
-static ScanLayout scan_layout(int row_bytes, int k, int qg) {
-    ScanLayout L;
-    L.row_bytes = row_bytes;
-    L.k = k;
-    L.qg = qg;
-    L.rps = 32 * kScanConsumers;
-    while (L.rps > 32 && (size_t)L.rps * row_bytes * 2 > 112 * 1024) L.rps -= 32;
-    const size_t stage = (size_t)L.rps * row_bytes;
-    L.nst = (int)((120 * 1024) / stage);
-    if (L.nst < 2) L.nst = 2;
-    if (L.nst > 8) L.nst = 8;
-    size_t o = 0;
-    L.off_full = o; o += 8 * L.nst;
-    L.off_empty = o; o += 8 * L.nst;
-    L.off_meta = o; o += 16 * L.nst;
-    o = (o + 127) & ~(size_t)127;
-    L.off_stage = o; o += stage * L.nst;
-    L.off_q = o; o += (size_t)qg * row_bytes;
-    L.off_lists = o; o += (size_t)kScanConsumers * qg * k * 8;
-    L.off_scratch = o; o += (size_t)kScanConsumers * (32 + 2 * k) * 8;
-    L.off_lcnt = o; o += (size_t)kScanConsumers * qg * 4;
-    L.off_qmeta = o; o += (size_t)qg * 32;
-    L.total = o;
-    return L;
-}
-
-int scan_qg(int row_bytes, int k) {
-    int qg = kScanQG;
-    while (qg > 1 && ((size_t)qg * row_bytes > 32 * 1024 ||
-                      (size_t)kScanConsumers * qg * k * 8 > 40 * 1024))
-        qg >>= 1;
-    return qg;
-}
 
 struct QMeta {          // per query of the current segment
     int64_t p_off;      // offset of the query's sorted labels (predicate)
@@ -69,6 +40,59 @@ struct QMeta {          // per query of the current segment
     int32_t nl;
     int32_t pad[2];
 };
+
+struct TInfo {          // per tile, written by the producer with the query prefetch
+    int64_t base;       // first row of the label in X_LS (or M_HS in exact mode)
+    int32_t tile, seg, label, nq, tile_in_seg, n_tiles, hs, pad;
+};
+
+static void scan_team(int chunks, int *ts, int *cpl) {
+    for (int t = 32; t >= 2; t >>= 1)
+        if (chunks % t == 0 && chunks / t <= 4) { *ts = t; *cpl = chunks / t; return; }
+    *ts = 32;
+    *cpl = (chunks + 31) / 32;
+}
+
+int scan_qg(int row_bytes, int k) {
+    int qg = kScanQG;
+    while (qg > 1 && ((size_t)qg * row_bytes > 16 * 1024 || (size_t)kScanConsumers * qg * k * 8 > 40 * 1024))
+        qg >>= 1;
+    return qg;
+}
+
+static ScanLayout scan_layout(int row_bytes, int k, int qg) {
+    ScanLayout L;
+    L.row_bytes = row_bytes;
+    L.k = k;
+    L.qg = qg;
+    scan_team(row_bytes / 16, &L.ts, &L.cpl);
+    const int nv = L.ts < 8 ? L.ts : 8;
+    const int br = nv * (32 / L.ts);                    // rows per warp batch
+    int rb = 1;
+    while (rb < 4 && (size_t)kScanConsumers * br * (rb * 2) * row_bytes <= 32 * 1024) rb *= 2;
+    L.rps = kScanConsumers * br * rb;
+    const size_t stage = (size_t)L.rps * row_bytes;
+    L.nst = (int)((128 * 1024) / stage);
+    if (L.nst < 2) L.nst = 2;
+    if (L.nst > 8) L.nst = 8;
+    size_t o = 0;
+    L.off_full = o; o += 8 * L.nst;
+    L.off_empty = o; o += 8 * L.nst;
+    L.off_qfull = o; o += 16;
+    L.off_qempty = o; o += 16;
+    L.off_meta = o; o += 16 * L.nst;
+    L.off_tinfo = o; o += 2 * sizeof(TInfo);
+    L.off_flag = o; o += 16;
+    o = (o + 127) & ~(size_t)127;
+    L.off_stage = o; o += stage * L.nst;
+    L.off_qbuf = o; o += 2 * (size_t)qg * row_bytes;
+    L.off_qmeta = o; o += 2 * (size_t)qg * sizeof(QMeta);
+    L.off_lists = o; o += (size_t)kScanConsumers * qg * k * 8;
+    L.off_scratch = o; o += (size_t)kScanConsumers * (32 + 2 * k) * 8;
+    L.off_lcnt = o; o += (size_t)kScanConsumers * qg * 4;
+    L.total = o;
+    return L;
+}
 
 // warp-level top-k update of one query's per-warp list with 32 candidate keys (one per lane)
 __device__ __forceinline__ void warp_topk_update(ull *L, int *cnt_p, ull key, int k, ull *cbuf, ull *tmp,
@@ -88,38 +112,105 @@ __device__ __forceinline__ void warp_topk_update(ull *L, int *cnt_p, ull key, in
     __syncwarp();
 }
 
-template <int DT>
+// Write one item's final list to its destination (direct output row or the item's result slot).
+__device__ __forceinline__ void write_final(const SearchArgs &a, const QMeta &q, const ull *L, int n, int k,
+                                            int lane) {
+    for (int t = lane; t < k; t += 32) {
+        const ull key = t < n ? L[t] : KEY_INF;
+        if (q.meta & META_DIRECT) {
+            a.out_ids[(int64_t)q.qid * k + t] = key == KEY_INF ? -1 : (int32_t)key_id(key);
+            a.out_dists[(int64_t)q.qid * k + t] = key == KEY_INF ? __uint_as_float(0x7f800000u) : key_dist(key);
+        } else {
+            a.item_res[(size_t)q.slot * k + t] = key;
+        }
+    }
+}
+
+// Distances of NQB queries against the NV rows of this lane's team; after the butterfly the owner
+// lane of each row holds that row's distance for every query (see file header).
+template <int DT, int TS, int CPLMAX, int NQB>
+__device__ __forceinline__ void batch_dist(const uint8_t *__restrict__ rows, int row_bytes, int cpl, int tl,
+                                           const uint4 (&q)[4][CPLMAX], typename Acc<DT>::T (&out)[4], int lane) {
+    typedef Acc<DT> A;
+    constexpr int NV = TS < 8 ? TS : 8;
+    typename A::T acc[NQB][NV];
+#pragma unroll
+    for (int g = 0; g < NQB; g++)
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[g][i] = 0;
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        const uint4 *r = reinterpret_cast<const uint4 *>(rows + (size_t)i * row_bytes);
+#pragma unroll
+        for (int j = 0; j < CPLMAX; j++) {
+            if (j < cpl) {
+                const uint4 x = r[tl + j * TS];
+#pragma unroll
+                for (int g = 0; g < NQB; g++) A::add(acc[g][i], q[g][j], x);
+            }
+        }
+    }
+    // butterfly: halve the NV values per lane log2(NV) times, then full-reduce the rest of the team
+#pragma unroll
+    for (int g = 0; g < NQB; g++) {
+#pragma unroll
+        for (int s = 0; (1 << s) < NV; s++) {
+            const int o = TS >> (s + 1);
+            const int half = NV >> (s + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < half; i++) {
+                const typename A::T send = up ? acc[g][i] : acc[g][i + half];
+                const typename A::T keep = up ? acc[g][i + half] : acc[g][i];
+                acc[g][i] = keep + __shfl_xor_sync(FULL, send, o);
+            }
+        }
+#pragma unroll
+        for (int o = TS / (2 * NV); o >= 1; o >>= 1) acc[g][0] += __shfl_xor_sync(FULL, acc[g][0], o);
+        out[g] = acc[g][0];
+    }
+}
+
+template <int DT, int TS, int CPLMAX>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayout SL) {
+    constexpr int NV = TS < 8 ? TS : 8;
+    constexpr int BR = NV * (32 / TS);               // rows per warp batch
+    typedef Acc<DT> A;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + SL.off_full);
     uint64_t *empty = reinterpret_cast<uint64_t *>(smem + SL.off_empty);
+    uint64_t *qfull = reinterpret_cast<uint64_t *>(smem + SL.off_qfull);
+    uint64_t *qempty = reinterpret_cast<uint64_t *>(smem + SL.off_qempty);
     int4 *meta = reinterpret_cast<int4 *>(smem + SL.off_meta);
+    TInfo *tinfo = reinterpret_cast<TInfo *>(smem + SL.off_tinfo);
+    int *flag = reinterpret_cast<int *>(smem + SL.off_flag);
     uint8_t *stages = smem + SL.off_stage;
-    const uint4 *qsm = reinterpret_cast<const uint4 *>(smem + SL.off_q);
+    uint8_t *qbuf = smem + SL.off_qbuf;
+    QMeta *qmeta = reinterpret_cast<QMeta *>(smem + SL.off_qmeta);
     ull *lists = reinterpret_cast<ull *>(smem + SL.off_lists);
     ull *scratch = reinterpret_cast<ull *>(smem + SL.off_scratch);
     int *lcnt = reinterpret_cast<int *>(smem + SL.off_lcnt);
-    QMeta *qm = reinterpret_cast<QMeta *>(smem + SL.off_qmeta);
 
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nst = SL.nst, rps = SL.rps, k = SL.k, row_bytes = ix.row_bytes;
+    const int nst = SL.nst, rps = SL.rps, k = SL.k, qg = SL.qg, row_bytes = ix.row_bytes;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
             mbar_init(full + i, 1);
             mbar_init(empty + i, kScanConsumers);
         }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(qfull + i, 1);
+            mbar_init(qempty + i, 1);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer (warp 0)
-        // LS labels: one bulk copy of the tile's contiguous X_LS rows per stage. In exact mode an
-        // HS label is scanned too; its rows are gathered from X through M_HS, one bulk copy per row
-        // issued by all 32 lanes (no duplicated vectors).
-        uint32_t n = 0;
+        // ------------------------------------------------------------ producer
+        uint32_t n = 0, tc = 0;
         const int ntiles = a.ctr->n_tiles;
         for (;;) {
             int t = 0;
@@ -138,6 +229,40 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
             const Segment sg = a.segs[tl.seg];
             const LabelDir d = ix.dir[sg.label];
             const bool hs = d.size >= ix.T;
+            // -- query prefetch for this tile (double buffer by tile parity)
+            const int tp = tc & 1;
+            if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
+            __syncwarp();
+            const int nq = sg.n_items;
+            QMeta *qm = qmeta + (size_t)tp * qg;
+            for (int g = lane; g < nq; g += 32) {
+                const int s = a.scan_slots[sg.item_base + g];
+                const Item it = a.items[s];
+                QMeta m;
+                m.p_off = a.q_off[it.qid];
+                m.slot = s;
+                m.qid = it.qid;
+                m.meta = it.meta;
+                m.nl = a.qinfo[it.qid].nl;
+                m.pad[0] = m.pad[1] = 0;
+                qm[g] = m;
+            }
+            if (lane == 0) {
+                TInfo ti;
+                ti.base = d.base;
+                ti.tile = t; ti.seg = tl.seg; ti.label = sg.label; ti.nq = nq;
+                ti.tile_in_seg = tl.tile_in_seg; ti.n_tiles = sg.n_tiles; ti.hs = hs; ti.pad = 0;
+                tinfo[tp] = ti;
+            }
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) mbar_arrive_expect_tx(qfull + tp, (uint32_t)nq * row_bytes);
+            __syncwarp();
+            for (int g = lane; g < nq; g += 32)
+                tma_load_1d(qbuf + ((size_t)tp * qg + g) * row_bytes, a.Qp + (int64_t)qm[g].qid * row_bytes,
+                            (uint32_t)row_bytes, qfull + tp);
+            tc++;
+            // -- row stages
             for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += rps) {
                 const int nr = min(rps, tl.row_end - r0);
                 const int slot = n % nst;
@@ -165,117 +290,159 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     }
 
     // ---------------------------------------------------------------- consumers
-    typedef Acc<DT> A;
-    const int cw = warp - 1;                 // consumer warp 0..3
-    const int ct = threadIdx.x - 32;         // consumer thread 0..127
-    const int chunks = ix.chunks;
+    const int cw = warp - 1;
+    const int ct = threadIdx.x - 32;
+    const int tm = lane / TS, tl = lane % TS;
+    const int r_own = tl / (TS / NV);                 // row of the team this lane owns after reduction
+    const bool owner = (tl % (TS / NV)) == 0;
+    const int cpl = SL.cpl;
     ull *cbuf = scratch + (size_t)cw * (32 + 2 * k);
     ull *tmp = cbuf + 32;
     ull *fin2 = tmp + k;
-    int nq = 0, label = 0, tile_in_seg = 0;
-    int64_t lbase = 0;
-    const int32_t *gmap = ix.M_ls;   // local row -> global id (M_LS, or M_HS in exact mode)
     unsigned long long my_rows = 0, my_qrows = 0;
-    uint32_t n = 0;
+    uint32_t n = 0, tc = 0;
+    TInfo ti;
+    ti.nq = 0;
+    const QMeta *qm = qmeta;
+    const uint8_t *qb = qbuf;
+    const int32_t *gmap = ix.M_ls;
+    int tp = 0;
     for (;;) {
         const int slot = n % nst;
         mbar_wait(full + slot, (n / nst) & 1);
         const int4 m = meta[slot];
         if (m.w & ST_END) break;
         if (m.w & ST_FIRST) {
-            named_bar_sync(1, 32 * kScanConsumers);
-            const Tile tl = a.tiles[m.x];
-            const Segment sg = a.segs[tl.seg];
-            nq = sg.n_items;
-            label = sg.label;
-            tile_in_seg = tl.tile_in_seg;
-            lbase = ix.dir[label].base;
-            gmap = ix.dir[label].size >= ix.T ? ix.M_hs : ix.M_ls;
-            if (ct < nq) {
-                const int s = a.scan_slots[sg.item_base + ct];
-                const Item it = a.items[s];
-                QMeta q;
-                q.slot = s; q.qid = it.qid; q.meta = it.meta;
-                q.p_off = a.q_off[it.qid];
-                q.nl = a.qinfo[it.qid].nl;
-                qm[ct] = q;
-            }
-            for (int i = ct; i < nq * kScanConsumers; i += 32 * kScanConsumers) lcnt[i] = 0;
-            named_bar_sync(1, 32 * kScanConsumers);
-            uint4 *qdst = reinterpret_cast<uint4 *>(smem + SL.off_q);
-            for (int e = ct; e < nq * chunks; e += 32 * kScanConsumers) {
-                const int g = e / chunks, c = e - g * chunks;
-                qdst[e] = __ldg(reinterpret_cast<const uint4 *>(a.Qp + (int64_t)qm[g].qid * row_bytes) + c);
-            }
-            named_bar_sync(1, 32 * kScanConsumers);
+            tp = tc & 1;
+            mbar_wait(qfull + tp, (tc >> 1) & 1);
+            ti = tinfo[tp];
+            qm = qmeta + (size_t)tp * qg;
+            qb = qbuf + (size_t)tp * qg * row_bytes;
+            gmap = ti.hs ? ix.M_hs : ix.M_ls;
+            for (int g = lane; g < ti.nq; g += 32) lcnt[cw * qg + g] = 0;
+            if (k <= 32)
+                for (int e = lane; e < ti.nq * k; e += 32) lists[(size_t)cw * qg * k + e] = KEY_INF;
+            __syncwarp();
         }
-        // -- compute: thread ct owns row ct of the stage
-        const int nr = m.z;
-        const bool valid = ct < nr;
-        const uint4 *rowp = reinterpret_cast<const uint4 *>(stages + (size_t)slot * rps * row_bytes +
-                                                            (size_t)ct * row_bytes);
-        const int32_t gid = valid ? __ldg(gmap + lbase + m.y + ct) : -1;
-        const int rot = ct % chunks;
-        for (int g0 = 0; g0 < nq; g0 += 8) {
-            typename A::T acc[8];
+        const int nq = ti.nq, nr = m.z;
+        const uint8_t *stage = stages + (size_t)slot * rps * row_bytes;
+        for (int b0 = cw * BR; b0 < nr; b0 += kScanConsumers * BR) {
+            // rows b0 .. b0+BR of the stage: team tm takes rows b0 + tm*NV + i, i < NV
+            const int trow0 = b0 + tm * NV;
+            const int orow = trow0 + r_own;
+            const bool ovalid = owner && orow < nr;
+            const int32_t gid = ovalid ? __ldg(gmap + ti.base + m.y + orow) : -1;
+            for (int g0 = 0; g0 < nq; g0 += 4) {
+                const int nb = min(4, nq - g0);
+                uint4 q[4][CPLMAX];
 #pragma unroll
-            for (int g = 0; g < 8; g++) acc[g] = 0;
-            if (valid) {
-                int cc = rot;
-                for (int c = 0; c < chunks; c++) {
-                    const uint4 xv = rowp[cc];
+                for (int g = 0; g < 4; g++)
 #pragma unroll
-                    for (int g = 0; g < 8; g++)
-                        if (g0 + g < nq) A::add(acc[g], qsm[(g0 + g) * chunks + cc], xv);
-                    cc = cc + 1 == chunks ? 0 : cc + 1;
+                    for (int j = 0; j < CPLMAX; j++)
+                        q[g][j] = (g < nb && j < cpl)
+                                      ? reinterpret_cast<const uint4 *>(qb + (size_t)(g0 + g) * row_bytes)[tl + j * TS]
+                                      : make_uint4(0, 0, 0, 0);
+                typename A::T dist[4];
+                const uint8_t *rows = stage + (size_t)trow0 * row_bytes;
+                if (nb == 1) batch_dist<DT, TS, CPLMAX, 1>(rows, row_bytes, cpl, tl, q, dist, lane);
+                else if (nb == 2) batch_dist<DT, TS, CPLMAX, 2>(rows, row_bytes, cpl, tl, q, dist, lane);
+                else batch_dist<DT, TS, CPLMAX, 4>(rows, row_bytes, cpl, tl, q, dist, lane);
+                for (int g = 0; g < nb; g++) {
+                    ull key = KEY_INF;
+                    if (ovalid) {
+                        key = make_key(A::to_float(dist[g]), (uint32_t)gid);
+                        const QMeta &qq = qm[g0 + g];
+                        if ((qq.meta & META_PRED) && !verify_pred(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
+                            key = KEY_INF;
+                    }
+                    const int li = cw * qg + g0 + g;
+                    if (k <= 32) {
+                        ull *L = lists + (size_t)li * k;
+                        const ull thr = L[k - 1];
+                        if (__ballot_sync(FULL, key < thr)) {
+                            ull Li = lane < k ? L[lane] : KEY_INF;
+                            Li = warp_insert_topk(Li, key, k, lane);
+                            if (lane < k) L[lane] = Li;
+                            __syncwarp();
+                        }
+                    } else {
+                        warp_topk_update(lists + (size_t)li * k, lcnt + li, key, k, cbuf, tmp, lane);
+                    }
                 }
-            }
-#pragma unroll
-            for (int g = 0; g < 8; g++) {
-                if (g0 + g >= nq) break;
-                ull key = KEY_INF;
-                if (valid) {
-                    key = make_key(A::to_float(acc[g]), (uint32_t)gid);
-                    const QMeta &q = qm[g0 + g];
-                    if ((q.meta & META_PRED) && !verify_pred(ix, gid, a.qlab + q.p_off, q.nl, label))
-                        key = KEY_INF;
-                }
-                const int li = cw * nq + g0 + g;
-                warp_topk_update(lists + (size_t)li * k, lcnt + li, key, k, cbuf, tmp, lane);
             }
         }
         if (ct == 0) { my_rows += nr; my_qrows += (unsigned long long)nr * nq; }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
         if (m.w & ST_LAST) {
-            // -- merge the four warp lists of every query and write the tile's results
+            // -- merge the warp lists of every query; write the tile's result
             named_bar_sync(1, 32 * kScanConsumers);
+            const bool multi = ti.n_tiles > 1;
             for (int g = cw; g < nq; g += kScanConsumers) {
                 ull *A0 = tmp, *B0 = fin2;
-                int na = lcnt[0 * nq + g];
-                for (int i = lane; i < na; i += 32) A0[i] = lists[(size_t)(0 * nq + g) * k + i];
-                __syncwarp();
-                for (int w2 = 1; w2 < kScanConsumers; w2++) {
-                    const int li = w2 * nq + g;
-                    na = warp_merge(A0, na, lists + (size_t)li * k, lcnt[li], B0, k, lane);
-                    ull *t2 = A0; A0 = B0; B0 = t2;
-                }
-                const QMeta &q = qm[g];
-                for (int t = lane; t < k; t += 32) {
-                    const ull key = t < na ? A0[t] : KEY_INF;
-                    if (q.meta & META_MULTI) {
-                        a.partials[((size_t)q.slot * a.max_tiles_per_label + tile_in_seg) * k + t] = key;
-                    } else if (q.meta & META_DIRECT) {
-                        a.out_ids[(int64_t)q.qid * k + t] = key == KEY_INF ? -1 : (int32_t)key_id(key);
-                        a.out_dists[(int64_t)q.qid * k + t] =
-                            key == KEY_INF ? __uint_as_float(0x7f800000u) : key_dist(key);
-                    } else {
-                        a.item_res[(size_t)q.slot * k + t] = key;
+                int na;
+                if (k <= 32) {
+                    ull Li = lane < k ? lists[(size_t)g * k + lane] : KEY_INF;
+                    for (int w2 = 1; w2 < kScanConsumers; w2++) {
+                        const ull c = lane < k ? lists[(size_t)(w2 * qg + g) * k + lane] : KEY_INF;
+                        Li = warp_insert_topk(Li, c, k, lane);
                     }
+                    if (lane < k) A0[lane] = Li;
+                    na = __popc(__ballot_sync(FULL, lane < k && Li != KEY_INF));
+                    __syncwarp();
+                } else {
+                    na = lcnt[g];
+                    for (int i = lane; i < na; i += 32) A0[i] = lists[(size_t)g * k + i];
+                    __syncwarp();
+                    for (int w2 = 1; w2 < kScanConsumers; w2++) {
+                        const int li = w2 * qg + g;
+                        na = warp_merge(A0, na, lists + (size_t)li * k, lcnt[li], B0, k, lane);
+                        ull *t2 = A0; A0 = B0; B0 = t2;
+                    }
+                }
+                if (multi) {
+                    for (int t = lane; t < k; t += 32)
+                        a.partials[((size_t)qm[g].slot * a.max_tiles_per_label + ti.tile_in_seg) * k + t] =
+                            t < na ? A0[t] : KEY_INF;
+                } else {
+                    write_final(a, qm[g], A0, na, k, lane);
                 }
                 __syncwarp();
             }
+            if (multi) {
+                // last-block-done: the CTA completing the segment's last tile merges the partials
+                __threadfence();
+                named_bar_sync(1, 32 * kScanConsumers);
+                if (ct == 0) flag[0] = atomicAdd(&a.segs[ti.seg].pad[0], 1) == ti.n_tiles - 1;
+                named_bar_sync(1, 32 * kScanConsumers);
+                if (flag[0]) {
+                    __threadfence();
+                    for (int g = cw; g < nq; g += kScanConsumers) {
+                        ull *A0 = tmp, *B0 = fin2;
+                        int na = 0;
+                        for (int t2 = 0; t2 < ti.n_tiles; t2++) {
+                            const volatile ull *P =
+                                a.partials + ((size_t)qm[g].slot * a.max_tiles_per_label + t2) * k;
+                            ull *C = cbuf;                    // stage the partial list (k <= 32 per chunk)
+                            for (int c0 = 0; c0 < k; c0 += 32) {
+                                const int cn = min(32, k - c0);
+                                ull v = lane < cn ? P[c0 + lane] : KEY_INF;
+                                C[lane] = v;
+                                __syncwarp();
+                                int nc = __popc(__ballot_sync(FULL, v != KEY_INF));
+                                na = warp_merge(A0, na, C, nc, B0, k, lane);
+                                ull *t3 = A0; A0 = B0; B0 = t3;
+                                __syncwarp();
+                            }
+                        }
+                        write_final(a, qm[g], A0, na, k, lane);
+                        __syncwarp();
+                    }
+                }
+            }
             named_bar_sync(1, 32 * kScanConsumers);
+            if (ct == 0) mbar_arrive(qempty + tp);
+            tc++;
         }
         n++;
     }
@@ -285,22 +452,31 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     }
 }
 
+// ------------------------------------------------------------------ dispatch
+typedef void (*scan_fn)(SearchArgs, ScanLayout);
+
+template <int DT>
+static scan_fn scan_pick(int ts, int cpl) {
+#define VF_S(T_, C_) if (ts == T_ && cpl <= C_) return k_scan<DT, T_, C_>;
+    VF_S(32, 1) VF_S(32, 2) VF_S(32, 4) VF_S(32, 8) VF_S(16, 1) VF_S(16, 2) VF_S(16, 4)
+    VF_S(8, 1) VF_S(8, 2) VF_S(8, 4) VF_S(4, 1) VF_S(4, 2) VF_S(4, 4) VF_S(2, 1) VF_S(2, 2) VF_S(2, 4)
+#undef VF_S
+    return nullptr;
+}
+
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound) {
     if (max_tiles_bound <= 0) return 0;
     const int qg = scan_qg(a.ix.row_bytes, a.k);
     const ScanLayout SL = scan_layout(a.ix.row_bytes, a.k, qg);
+    scan_fn f = a.ix.dtype == 0 ? scan_pick<0>(SL.ts, SL.cpl) : scan_pick<1>(SL.ts, SL.cpl);
+    if (!f) return -1;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     int grid = nsm;
     if (grid > max_tiles_bound) grid = max_tiles_bound;
-    if (a.ix.dtype == 0) {
-        cudaFuncSetAttribute(k_scan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
-        k_scan<0><<<grid, kScanThreads, SL.total, s>>>(a, SL);
-    } else {
-        cudaFuncSetAttribute(k_scan<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
-        k_scan<1><<<grid, kScanThreads, SL.total, s>>>(a, SL);
-    }
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
+    f<<<grid, kScanThreads, SL.total, s>>>(a, SL);
     return 1;
 }
 

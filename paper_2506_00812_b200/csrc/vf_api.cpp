@@ -217,7 +217,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     // -- directory + M_HS / G_HS (compacted, ordered by label) + M_LS
     std::vector<LabelDir> dir(std::max(L, 1));
     std::vector<int32_t> m_hs((size_t)std::max<int64_t>(hs_rows, 1)), m_ls((size_t)std::max<int64_t>(ls_rows, 1));
-    std::vector<int32_t> g_hs((size_t)std::max<int64_t>(hs_rows * R, 1));
+    std::vector<int2> g_hs((size_t)std::max<int64_t>(hs_rows * R, 1));
     int64_t hb = 0, lb = 0;
     int32_t bslot = 0;
     for (int l = 0; l < L; l++) {
@@ -230,7 +230,11 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
         if (S >= T) {
             dir[l].base = hb;
             std::memcpy(&m_hs[hb], pi + a, S * sizeof(int32_t));
-            std::memcpy(&g_hs[hb * R], d->graph_local_ids + d->graph_row_offsets[l] * R, S * R * sizeof(int32_t));
+            const int32_t *src = d->graph_local_ids + d->graph_row_offsets[l] * R;
+            for (int64_t e = 0; e < S * R; e++) {
+                const int32_t c = src[e];
+                g_hs[hb * R + e] = c >= 0 ? make_int2(c, pi[a + c]) : make_int2(-1, -1);
+            }
             hb += S;
         } else {
             dir[l].base = lb;
@@ -242,8 +246,8 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     VF_B(cudaMemcpy(ix->dir.p, dir.data(), dir.size() * sizeof(LabelDir), cudaMemcpyHostToDevice));
     VF_B(ix->M_hs.ensure(m_hs.size() * 4));
     VF_B(cudaMemcpy(ix->M_hs.p, m_hs.data(), m_hs.size() * 4, cudaMemcpyHostToDevice));
-    VF_B(ix->G.ensure(g_hs.size() * 4));
-    VF_B(cudaMemcpy(ix->G.p, g_hs.data(), g_hs.size() * 4, cudaMemcpyHostToDevice));
+    VF_B(ix->G.ensure(g_hs.size() * 8));
+    VF_B(cudaMemcpy(ix->G.p, g_hs.data(), g_hs.size() * 8, cudaMemcpyHostToDevice));
     VF_B(ix->M_ls.ensure(m_ls.size() * 4));
     VF_B(cudaMemcpy(ix->M_ls.p, m_ls.data(), m_ls.size() * 4, cudaMemcpyHostToDevice));
     // -- X_LS: label-contiguous row copies of the LS lists, gathered on the device
@@ -280,7 +284,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     D.n_bslots = bslot;
     D.X = ix->X.as<uint8_t>();
     D.dir = ix->dir.as<LabelDir>();
-    D.G = ix->G.as<int32_t>();
+    D.G = ix->G.as<int2>();
     D.M_hs = ix->M_hs.as<int32_t>();
     D.Xls = ix->Xls.as<uint8_t>();
     D.M_ls = ix->M_ls.as<int32_t>();
@@ -299,7 +303,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     I.row_bytes = row_bytes;
     I.degree_R = R;
     I.bytes_vectors = N * row_bytes;
-    I.bytes_graph = hs_rows * R * 4;
+    I.bytes_graph = hs_rows * R * 8;
     I.bytes_map_hs = hs_rows * 4;
     I.bytes_ls_vectors = ls_rows * row_bytes;
     I.bytes_map_ls = ls_rows * 4;
@@ -389,7 +393,9 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
 
     // -- plan
     const int scan_max = p->exact ? ix->max_label_size : ix->max_ls_size;
-    int tile_rows = 4096;
+    // row tiles: small in the normal path (load balance across SMs; a label split over several
+    // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
+    int tile_rows = p->exact ? 4096 : 512;
     if ((scan_max + 255) / 256 > tile_rows) tile_rows = (scan_max + 255) / 256;
     const int mtpl = std::max(1, (scan_max + tile_rows - 1) / tile_rows);
     const bool multi = mtpl > 1;
@@ -399,10 +405,11 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     const int n_init = p->n_init > 0 ? p->n_init : R * w;
     const int max_iter = p->max_iterations > 0 ? p->max_iterations : 2 * ((p->itopk + w - 1) / w) + 16;
     // visited sets: shared-memory table sized for ~16 warps/SM, exact global overflow table
-    int hs = 256;
+    // ~32 itopk-sized expansions' worth of ids in shared memory, within ~7 KB per warp
+    int hs = 1024;
     {
-        const int64_t budget = 14336 - 16ll * p->itopk - 1024;
-        while ((int64_t)hs * 2 * 4 <= budget && hs < 8192) hs <<= 1;
+        const int64_t budget = 7168 - 16ll * p->itopk - 1024;
+        while (hs < 64 * p->itopk && hs < 8192 && (int64_t)hs * 2 * 4 <= budget) hs <<= 1;
     }
     const int64_t v_bound = (int64_t)n_init + (int64_t)max_iter * w * R + 32;
     const uint64_t gslots = pow2ceil((uint64_t)(2 * v_bound + 64));
@@ -510,13 +517,15 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     launches += launch_prepare(a, s);
     launches += launch_bucket(a, s, n_slots, qg);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
-    launches += launch_scan(a, s, (int)std::min<int64_t>(max_tiles, INT32_MAX));
+    const int sl = launch_scan(a, s, (int)std::min<int64_t>(max_tiles, INT32_MAX));
+    if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
+    launches += sl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));
     const int gl = launch_graph(a, s, (int)std::min<int64_t>(n_slots, INT32_MAX), graph_ctas);
     if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
     launches += gl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));
-    const bool need_merge = p->op == VF_OR || (p->op == VF_AND && p->recall_mode == VF_RECALL_PARALLEL) || multi;
+    const bool need_merge = p->op == VF_OR || (p->op == VF_AND && p->recall_mode == VF_RECALL_PARALLEL);
     if (need_merge) launches += launch_merge(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[5], s));
     VF_CUDA(cudaGetLastError());
@@ -545,7 +554,7 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     Counters c;
     VF_CUDA(cudaMemcpy(&c, sc->ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
     st->n_queries = sc->last.n_q;
-    st->n_items = c.n_items;
+    st->n_items = (int64_t)c.n_graph + c.n_scan_items;
     st->n_graph_items = c.n_graph;
     st->n_scan_items = c.n_scan_items;
     st->n_segments = c.n_segs;

@@ -34,7 +34,8 @@ struct DevIndex {
     int32_t n_bslots;      // non-empty labels (scan-bucket counters)
     const uint8_t *X;      // [n_points][row_bytes]  global vectors (one copy)
     const LabelDir *dir;   // [n_labels]
-    const int32_t *G;      // [hs_rows][R] local ids (G_HS)
+    const int2 *G;         // [hs_rows][R] (local id, global id) edges of G_HS (the
+                           // M_HS indirection of P:L444 folded into the row)
     const int32_t *M_hs;   // [hs_rows] local -> global (M_HS)
     const uint8_t *Xls;    // [ls_rows][row_bytes] label-contiguous LS copies (X_LS)
     const int32_t *M_ls;   // [ls_rows] (M_LS)

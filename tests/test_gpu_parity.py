@@ -247,7 +247,7 @@ def test_byte_accounting(vf, tiny):
     rb = info["row_bytes"]
     assert info["hs_rows"] == hs and info["ls_rows"] == ls
     assert info["bytes_vectors"] == w.cfg.n_points * rb
-    assert info["bytes_graph"] == hs * w.cfg.degree_R * 4
+    assert info["bytes_graph"] == hs * w.cfg.degree_R * 8      # (local, global) edge pairs
     assert info["bytes_ls_vectors"] == ls * rb
     # redundancy bypassing saves exactly the HS vector copies
     assert info["bytes_total"] < info["bytes_total"] + hs * rb
