@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--config", default="sift", choices=["tiny", "sift", "yfcc"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--targets", default="0.90,0.99")
+    ap.add_argument("--widths", default="1,2,4", help="search widths w swept for the operating points")
     ap.add_argument("--cpu-sample", type=int, default=2000)
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--ref-itopk", type=int, default=64)
@@ -226,30 +227,50 @@ def main():
         gt[s:e], gd[s:e] = ti.cpu().numpy(), td.cpu().numpy()
     log(f"ground truth (exact mode): {time.time() - t0:.1f}s")
 
-    # -- itopk sweep -> operating points
+    # -- (search_width, itopk) sweep -> operating points: for each recall target the fastest
+    #    configuration whose mean tie-aware recall@10 reaches it (the paper traces QPS-recall curves
+    #    by sweeping its search parameters)
     targets = [float(x) for x in args.targets.split(",")]
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
+
+    def quick_ms(itopk, w_):
+        ms = []
+        for _ in range(3):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return float(np.median(ms))
+
     sweep = []
-    for itopk in ITOPK_GRID:
-        ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, op=op, stream=stream)
-        torch.cuda.synchronize()
-        r_strict, r_tie = recall_vs(ids.cpu().numpy(), dd.cpu().numpy(), gt, gd, k)
-        sweep.append((itopk, r_strict, r_tie))
-        log(f"itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f}")
-        if r_tie >= max(targets) and itopk >= 32:
-            break
+    for w_ in [int(x) for x in args.widths.split(",")]:
+        for itopk in ITOPK_GRID:
+            if itopk < k:
+                continue
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            torch.cuda.synchronize()
+            r_strict, r_tie = recall_vs(ids.cpu().numpy(), dd.cpu().numpy(), gt, gd, k)
+            qms = quick_ms(itopk, w_)
+            sweep.append((itopk, r_strict, r_tie, w_, qms))
+            log(f"w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
+                f"{n / qms / 1e3:.2f} MQPS")
+            if r_tie >= max(targets):
+                break
     ops = {}
     for tgt in targets:
         ok = [s for s in sweep if s[2] >= tgt]
-        ops[tgt] = ok[0] if ok else None
+        ops[tgt] = min(ok, key=lambda s: s[4]) if ok else None
 
-    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
     ix.set_profiling(True)
     hbm_peak, peak_kind = measured_peaks()
 
-    def timed(itopk):
+    def timed(itopk, w_):
         """W warm-up + exactly K timed steps; per-step CUDA events around vf_search only."""
         for _ in range(args.warmup):
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, op=op, stream=stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         stats = []
@@ -258,7 +279,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, op=op, stream=stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
             ev[i][1].record(stream)
             stats.append(ix.last_stats(stream))   # syncs; between steps, outside the events
         torch.cuda.synchronize()
@@ -271,8 +292,8 @@ def main():
         for tgt, opnt in ops.items():
             if opnt is None:
                 continue
-            itopk = opnt[0]
-            ms, stats = timed(itopk)
+            itopk, w_ = opnt[0], opnt[3]
+            ms, stats = timed(itopk, w_)
             tot = float(np.sum(ms))
             if world > 1:
                 t = torch.tensor([tot], device=dev)
@@ -285,20 +306,20 @@ def main():
     main_tgt = targets[0]
     e2e = None
     if main_tgt in results:
-        itopk = results[main_tgt][0]
+        itopk, w_ = results[main_tgt][0], results[main_tgt][1][3]
         Qh = torch.from_numpy(w.Q).pin_memory()
         qoh = torch.from_numpy(w.q_off).pin_memory()
         qlh = torch.from_numpy(w.q_lab).pin_memory()
         oih = torch.empty((n, k), dtype=torch.int32).pin_memory()
         odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
         for _ in range(args.warmup):
-            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, op=op, stream=stream)
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
-            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, op=op, stream=stream)
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         et = e0.elapsed_time(e1)
@@ -315,15 +336,16 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
         import oracle
-        itopk = results[main_tgt][0]
+        itopk, w_ = results[main_tgt][0], results[main_tgt][1][3]
         o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
         m = min(n, args.cpu_sample)
         threads = os.cpu_count() or 1
         t0 = time.perf_counter()
-        o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], k=k, itopk=itopk, op=op, nthreads=threads)
+        o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], k=k, itopk=itopk, search_width=w_, op=op,
+                 nthreads=threads)
         el = time.perf_counter() - t0
         cpu = {"value": m / el, "unit": "queries/s", "cores": threads, "kind": "oracle",
-               "sample": f"first {m} of the {n} queries, itopk={itopk}, {threads} threads, {el:.1f}s"}
+               "sample": f"first {m} of the {n} queries, itopk={itopk}, w={w_}, {threads} threads, {el:.1f}s"}
 
     if rank != 0:
         if world > 1:
@@ -354,14 +376,15 @@ def main():
         "config": {"workload": f"{args.config} (BASELINE.json configs[{ {'tiny': 0, 'sift': 1, 'yfcc': 2}[args.config]}])",
                    "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
                    "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
-                   "R": R, "itopk": itopk, "recall_target": main_tgt,
+                   "R": R, "itopk": itopk, "search_width": opnt[3], "recall_target": main_tgt,
                    "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
                    "flush": "256 MiB L2 flush before every timed step (outside the step events)",
                    "parallelism": f"replicas{world}" if world > 1 else "single"},
-        "at_recall": {f"{t:.2f}": {"itopk": r[0], "qps": n * world * K / (r[4] / 1000.0),
+        "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "qps": n * world * K / (r[4] / 1000.0),
                                    "ms_per_step": r[4] / K, "recall_strict": r[1][1],
                                    "recall_tie_aware": r[1][2]} for t, r in results.items()},
-        "sweep": [{"itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2]} for s in sweep],
+        "sweep": [{"search_width": s[3], "itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2],
+                   "ms": s[4]} for s in sweep],
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": None, "algorithmic_bytes_per_launch": int(bytes_dom),

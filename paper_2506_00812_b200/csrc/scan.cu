@@ -30,7 +30,7 @@ enum : int { ST_FIRST = 1, ST_LAST = 2, ST_END = 4 };
 struct ScanLayout {
     int nst, rps, qg, k, row_bytes, ts, cpl;
     size_t off_full, off_empty, off_qfull, off_qempty, off_meta, off_tinfo, off_stage, off_qbuf,
-        off_qmeta, off_lists, off_lcnt, off_scratch, off_flag, total;
+        off_qmeta, off_lists, off_lcnt, off_scratch, off_flag, off_sthr, total;
 };
 
 struct QMeta {          // per query of the current segment
@@ -90,6 +90,8 @@ static ScanLayout scan_layout(int row_bytes, int k, int qg) {
     L.off_lists = o; o += (size_t)kScanConsumers * qg * k * 8;
     L.off_scratch = o; o += (size_t)kScanConsumers * (32 + 2 * k) * 8;
     L.off_lcnt = o; o += (size_t)kScanConsumers * qg * 4;
+    o = (o + 7) & ~(size_t)7;
+    L.off_sthr = o; o += 2 * (size_t)qg * 8;
     L.total = o;
     return L;
 }
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     ull *lists = reinterpret_cast<ull *>(smem + SL.off_lists);
     ull *scratch = reinterpret_cast<ull *>(smem + SL.off_scratch);
     int *lcnt = reinterpret_cast<int *>(smem + SL.off_lcnt);
+    ull *sthr = reinterpret_cast<ull *>(smem + SL.off_sthr);   // [2][qg] CTA-wide pruning bound
 
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                 m.qid = it.qid;
                 m.meta = it.meta;
                 m.nl = a.qinfo[it.qid].nl;
+                sthr[(size_t)tp * qg + g] = KEY_INF;
                 m.pad[0] = m.pad[1] = 0;
                 qm[g] = m;
             }
@@ -358,11 +362,17 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                     const int li = cw * qg + g0 + g;
                     if (k <= 32) {
                         ull *L = lists + (size_t)li * k;
-                        const ull thr = L[k - 1];
+                        // prune with min(own k-th, CTA-wide bound): any warp's k-th key bounds the
+                        // merged k-th from above, so keys at or above it can never be in the result
+                        ull *st = sthr + (size_t)tp * qg + g0 + g;
+                        const ull own = L[k - 1], shr = *(volatile ull *)st;
+                        const ull thr = own < shr ? own : shr;
                         if (__ballot_sync(FULL, key < thr)) {
                             ull Li = lane < k ? L[lane] : KEY_INF;
-                            Li = warp_insert_topk(Li, key, k, lane);
+                            Li = warp_insert_topk(Li, key < thr ? key : KEY_INF, k, lane);
                             if (lane < k) L[lane] = Li;
+                            const ull kth = __shfl_sync(FULL, Li, k - 1);
+                            if (lane == 0 && kth < shr) atomicMin(st, kth);
                             __syncwarp();
                         }
                     } else {
