@@ -15,10 +15,12 @@
 //     tl, tl+TS, ...), so each lane keeps its query chunks in registers; NV rows per team are
 //     accumulated at once and a butterfly reduces the NV x TS partial sums in (NV-1)+log2(TS/NV)
 //     shuffles, leaving one exact distance per "owner" lane (u8: vabsdiff4+dp4a int32; f32: FFMA,
-//     exact for integer-valued data). Per query and warp a top-k list is updated only when a key
-//     beats the k-th (ballot); AND items mask rows failing the predicate (reading #21). At a tile's
-//     end the 8 warp lists are merged; a segment split over several tiles is finalised by the CTA
-//     that completes its last tile (partial lists in global memory, last-block-done counter).
+//     exact for integer-valued data), written to a shared distance tile; AND items mark rows that
+//     fail the predicate (equivalent to the paper's pre-filter, reading #21). After one named
+//     barrier per stage the warp owning each query merges the tile into that query's single
+//     register-resident top-k list (ballot against the k-th, insert by shuffle). A segment split
+//     over several tiles is finalised by the CTA that completes its last tile (partial lists in
+//     global memory, last-block-done counter).
 #include "common.cuh"
 
 namespace vf {
@@ -30,8 +32,9 @@ enum : int { ST_FIRST = 1, ST_LAST = 2, ST_END = 4 };
 struct ScanLayout {
     int nst, rps, qg, k, row_bytes, ts, cpl;
     size_t off_full, off_empty, off_qfull, off_qempty, off_meta, off_tinfo, off_stage, off_qbuf,
-        off_qmeta, off_lists, off_lcnt, off_scratch, off_flag, off_sthr, total;
+        off_qmeta, off_lists, off_lcnt, off_scratch, off_flag, off_dist, off_gid, total;
 };
+constexpr uint32_t DIST_EXCL = 0xFFFFFFFFu;   // distance slot of an invalid / filtered row
 
 struct QMeta {          // per query of the current segment
     int64_t p_off;      // offset of the query's sorted labels (predicate)
@@ -53,26 +56,30 @@ static void scan_team(int chunks, int *ts, int *cpl) {
     *cpl = (chunks + 31) / 32;
 }
 
-int scan_qg(int row_bytes, int k) {
-    int qg = kScanQG;
-    while (qg > 1 && ((size_t)qg * row_bytes > 16 * 1024 || (size_t)kScanConsumers * qg * k * 8 > 40 * 1024))
-        qg >>= 1;
-    return qg;
-}
-
-static ScanLayout scan_layout(int row_bytes, int k, int qg) {
+// Shared-memory plan: a ring of row stages, two query buffers, a double-buffered distance tile
+// D[2][qg][rps] (+ the stage rows' global ids) and one top-k list per query of the segment.
+static ScanLayout scan_layout(int row_bytes, int k) {
     ScanLayout L;
     L.row_bytes = row_bytes;
     L.k = k;
-    L.qg = qg;
     scan_team(row_bytes / 16, &L.ts, &L.cpl);
     const int nv = L.ts < 8 ? L.ts : 8;
     const int br = nv * (32 / L.ts);                    // rows per warp batch
     int rb = 1;
-    while (rb < 4 && (size_t)kScanConsumers * br * (rb * 2) * row_bytes <= 32 * 1024) rb *= 2;
+    while (rb < 4 && kScanConsumers * br * rb * 2 <= 256 &&
+           (size_t)kScanConsumers * br * (rb * 2) * row_bytes <= 32 * 1024)
+        rb *= 2;
     L.rps = kScanConsumers * br * rb;
+    int qg = kScanQG;
+    while (qg > 1 && ((size_t)qg * row_bytes > 16 * 1024 || (size_t)qg * k * 8 > 16 * 1024 ||
+                      (size_t)qg * L.rps > 8192))
+        qg >>= 1;
+    L.qg = qg;
     const size_t stage = (size_t)L.rps * row_bytes;
-    L.nst = (int)((128 * 1024) / stage);
+    size_t fixed = 2 * (size_t)qg * row_bytes + 2 * (size_t)qg * sizeof(QMeta) + (size_t)qg * k * 8 +
+                   (size_t)kScanConsumers * (32 + 2 * k) * 8 + (size_t)qg * 4 + 2 * (size_t)qg * L.rps * 4 +
+                   2 * (size_t)L.rps * 4 + 1024;
+    L.nst = (int)((200 * 1024 - fixed) / stage);
     if (L.nst < 2) L.nst = 2;
     if (L.nst > 8) L.nst = 8;
     size_t o = 0;
@@ -87,14 +94,16 @@ static ScanLayout scan_layout(int row_bytes, int k, int qg) {
     L.off_stage = o; o += stage * L.nst;
     L.off_qbuf = o; o += 2 * (size_t)qg * row_bytes;
     L.off_qmeta = o; o += 2 * (size_t)qg * sizeof(QMeta);
-    L.off_lists = o; o += (size_t)kScanConsumers * qg * k * 8;
+    L.off_lists = o; o += (size_t)qg * k * 8;
     L.off_scratch = o; o += (size_t)kScanConsumers * (32 + 2 * k) * 8;
-    L.off_lcnt = o; o += (size_t)kScanConsumers * qg * 4;
-    o = (o + 7) & ~(size_t)7;
-    L.off_sthr = o; o += 2 * (size_t)qg * 8;
+    L.off_dist = o; o += 2 * (size_t)qg * L.rps * 4;
+    L.off_gid = o; o += 2 * (size_t)L.rps * 4;
+    L.off_lcnt = o; o += (size_t)qg * 4;
     L.total = o;
     return L;
 }
+
+int scan_qg(int row_bytes, int k) { return scan_layout(row_bytes, k).qg; }
 
 // warp-level top-k update of one query's per-warp list with 32 candidate keys (one per lane)
 __device__ __forceinline__ void warp_topk_update(ull *L, int *cnt_p, ull key, int k, ull *cbuf, ull *tmp,
@@ -192,7 +201,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     ull *lists = reinterpret_cast<ull *>(smem + SL.off_lists);
     ull *scratch = reinterpret_cast<ull *>(smem + SL.off_scratch);
     int *lcnt = reinterpret_cast<int *>(smem + SL.off_lcnt);
-    ull *sthr = reinterpret_cast<ull *>(smem + SL.off_sthr);   // [2][qg] CTA-wide pruning bound
+    uint32_t *dtile = reinterpret_cast<uint32_t *>(smem + SL.off_dist);   // [2][qg][rps] distance bits
+    int32_t *gtile = reinterpret_cast<int32_t *>(smem + SL.off_gid);      // [2][rps] global ids
 
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(qfull + i, 1);
-            mbar_init(qempty + i, 1);
+            mbar_init(qempty + i, kScanConsumers);
         }
         fence_mbar_init();
     }
@@ -247,7 +257,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                 m.qid = it.qid;
                 m.meta = it.meta;
                 m.nl = a.qinfo[it.qid].nl;
-                sthr[(size_t)tp * qg + g] = KEY_INF;
                 m.pad[0] = m.pad[1] = 0;
                 qm[g] = m;
             }
@@ -294,6 +303,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     }
 
     // ---------------------------------------------------------------- consumers
+    // Per stage: (1) every warp computes the exact distances of its rows for all queries of the
+    // segment into the distance tile D[buf]; (2) one named barrier; (3) the warp owning query g
+    // (g = cw mod 8) streams D[buf][g] into that query's single top-k list. One list per query
+    // means ~k(1 + ln(rows/k)) insertions per tile instead of one re-filling list per warp.
     const int cw = warp - 1;
     const int ct = threadIdx.x - 32;
     const int tm = lane / TS, tl = lane % TS;
@@ -323,19 +336,24 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
             qm = qmeta + (size_t)tp * qg;
             qb = qbuf + (size_t)tp * qg * row_bytes;
             gmap = ti.hs ? ix.M_hs : ix.M_ls;
-            for (int g = lane; g < ti.nq; g += 32) lcnt[cw * qg + g] = 0;
-            if (k <= 32)
-                for (int e = lane; e < ti.nq * k; e += 32) lists[(size_t)cw * qg * k + e] = KEY_INF;
+            for (int g = cw; g < ti.nq; g += kScanConsumers) {          // my queries' lists
+                for (int e = lane; e < k; e += 32) lists[(size_t)g * k + e] = KEY_INF;
+                if (lane == 0) lcnt[g] = 0;
+            }
             __syncwarp();
         }
         const int nq = ti.nq, nr = m.z;
+        const int buf = n & 1;
+        uint32_t *D = dtile + (size_t)buf * qg * rps;
+        int32_t *Gd = gtile + (size_t)buf * rps;
         const uint8_t *stage = stages + (size_t)slot * rps * row_bytes;
+        // (1) distances
         for (int b0 = cw * BR; b0 < nr; b0 += kScanConsumers * BR) {
-            // rows b0 .. b0+BR of the stage: team tm takes rows b0 + tm*NV + i, i < NV
             const int trow0 = b0 + tm * NV;
             const int orow = trow0 + r_own;
             const bool ovalid = owner && orow < nr;
             const int32_t gid = ovalid ? __ldg(gmap + ti.base + m.y + orow) : -1;
+            if (owner && orow < rps) Gd[orow] = gid;
             for (int g0 = 0; g0 < nq; g0 += 4) {
                 const int nb = min(4, nq - g0);
                 uint4 q[4][CPLMAX];
@@ -351,32 +369,16 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                 if (nb == 1) batch_dist<DT, TS, CPLMAX, 1>(rows, row_bytes, cpl, tl, q, dist, lane);
                 else if (nb == 2) batch_dist<DT, TS, CPLMAX, 2>(rows, row_bytes, cpl, tl, q, dist, lane);
                 else batch_dist<DT, TS, CPLMAX, 4>(rows, row_bytes, cpl, tl, q, dist, lane);
-                for (int g = 0; g < nb; g++) {
-                    ull key = KEY_INF;
-                    if (ovalid) {
-                        key = make_key(A::to_float(dist[g]), (uint32_t)gid);
-                        const QMeta &qq = qm[g0 + g];
-                        if ((qq.meta & META_PRED) && !verify_pred(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
-                            key = KEY_INF;
-                    }
-                    const int li = cw * qg + g0 + g;
-                    if (k <= 32) {
-                        ull *L = lists + (size_t)li * k;
-                        // prune with min(own k-th, CTA-wide bound): any warp's k-th key bounds the
-                        // merged k-th from above, so keys at or above it can never be in the result
-                        ull *st = sthr + (size_t)tp * qg + g0 + g;
-                        const ull own = L[k - 1], shr = *(volatile ull *)st;
-                        const ull thr = own < shr ? own : shr;
-                        if (__ballot_sync(FULL, key < thr)) {
-                            ull Li = lane < k ? L[lane] : KEY_INF;
-                            Li = warp_insert_topk(Li, key < thr ? key : KEY_INF, k, lane);
-                            if (lane < k) L[lane] = Li;
-                            const ull kth = __shfl_sync(FULL, Li, k - 1);
-                            if (lane == 0 && kth < shr) atomicMin(st, kth);
-                            __syncwarp();
+                if (owner && orow < rps) {
+                    for (int g = 0; g < nb; g++) {
+                        uint32_t bits = DIST_EXCL;
+                        if (ovalid) {
+                            bits = __float_as_uint(A::to_float(dist[g]));
+                            const QMeta &qq = qm[g0 + g];
+                            if ((qq.meta & META_PRED) && !verify_pred(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
+                                bits = DIST_EXCL;
                         }
-                    } else {
-                        warp_topk_update(lists + (size_t)li * k, lcnt + li, key, k, cbuf, tmp, lane);
+                        D[(size_t)(g0 + g) * rps + orow] = bits;
                     }
                 }
             }
@@ -384,38 +386,43 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
         if (ct == 0) { my_rows += nr; my_qrows += (unsigned long long)nr * nq; }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
+        // (2) the distance tile is complete
+        named_bar_sync(1, 32 * kScanConsumers);
+        // (3) selection: my queries' lists absorb this stage's keys
+        for (int g = cw; g < nq; g += kScanConsumers) {
+            ull *L = lists + (size_t)g * k;
+            const uint32_t *Dg = D + (size_t)g * rps;
+            if (k <= 32) {
+                ull Li = lane < k ? L[lane] : KEY_INF;
+                for (int r0 = 0; r0 < nr; r0 += 32) {
+                    const int r = r0 + lane;
+                    const uint32_t bits = r < nr ? Dg[r] : DIST_EXCL;
+                    const ull key = bits == DIST_EXCL ? KEY_INF : (((ull)bits << 32) | (uint32_t)Gd[r]);
+                    Li = warp_insert_topk(Li, key, k, lane);
+                }
+                if (lane < k) L[lane] = Li;
+            } else {
+                for (int r0 = 0; r0 < nr; r0 += 32) {
+                    const int r = r0 + lane;
+                    const uint32_t bits = r < nr ? Dg[r] : DIST_EXCL;
+                    const ull key = bits == DIST_EXCL ? KEY_INF : (((ull)bits << 32) | (uint32_t)Gd[r]);
+                    warp_topk_update(L, lcnt + g, key, k, cbuf, tmp, lane);
+                }
+            }
+            __syncwarp();
+        }
         if (m.w & ST_LAST) {
-            // -- merge the warp lists of every query; write the tile's result
-            named_bar_sync(1, 32 * kScanConsumers);
             const bool multi = ti.n_tiles > 1;
             for (int g = cw; g < nq; g += kScanConsumers) {
-                ull *A0 = tmp, *B0 = fin2;
-                int na;
-                if (k <= 32) {
-                    ull Li = lane < k ? lists[(size_t)g * k + lane] : KEY_INF;
-                    for (int w2 = 1; w2 < kScanConsumers; w2++) {
-                        const ull c = lane < k ? lists[(size_t)(w2 * qg + g) * k + lane] : KEY_INF;
-                        Li = warp_insert_topk(Li, c, k, lane);
-                    }
-                    if (lane < k) A0[lane] = Li;
-                    na = __popc(__ballot_sync(FULL, lane < k && Li != KEY_INF));
-                    __syncwarp();
-                } else {
-                    na = lcnt[g];
-                    for (int i = lane; i < na; i += 32) A0[i] = lists[(size_t)g * k + i];
-                    __syncwarp();
-                    for (int w2 = 1; w2 < kScanConsumers; w2++) {
-                        const int li = w2 * qg + g;
-                        na = warp_merge(A0, na, lists + (size_t)li * k, lcnt[li], B0, k, lane);
-                        ull *t2 = A0; A0 = B0; B0 = t2;
-                    }
-                }
+                const ull *L = lists + (size_t)g * k;
+                const int na = k <= 32 ? __popc(__ballot_sync(FULL, lane < k && L[lane < k ? lane : 0] != KEY_INF))
+                                       : lcnt[g];
                 if (multi) {
                     for (int t = lane; t < k; t += 32)
                         a.partials[((size_t)qm[g].slot * a.max_tiles_per_label + ti.tile_in_seg) * k + t] =
-                            t < na ? A0[t] : KEY_INF;
+                            t < na ? L[t] : KEY_INF;
                 } else {
-                    write_final(a, qm[g], A0, na, k, lane);
+                    write_final(a, qm[g], L, na, k, lane);
                 }
                 __syncwarp();
             }
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                         for (int t2 = 0; t2 < ti.n_tiles; t2++) {
                             const volatile ull *P =
                                 a.partials + ((size_t)qm[g].slot * a.max_tiles_per_label + t2) * k;
-                            ull *C = cbuf;                    // stage the partial list (k <= 32 per chunk)
+                            ull *C = cbuf;                    // stage the partial list 32 keys at a time
                             for (int c0 = 0; c0 < k; c0 += 32) {
                                 const int cn = min(32, k - c0);
                                 ull v = lane < cn ? P[c0 + lane] : KEY_INF;
@@ -450,8 +457,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                     }
                 }
             }
-            named_bar_sync(1, 32 * kScanConsumers);
-            if (ct == 0) mbar_arrive(qempty + tp);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(qempty + tp);   // this warp is done with the tile's queries
             tc++;
         }
         n++;
@@ -476,8 +483,7 @@ static scan_fn scan_pick(int ts, int cpl) {
 
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound) {
     if (max_tiles_bound <= 0) return 0;
-    const int qg = scan_qg(a.ix.row_bytes, a.k);
-    const ScanLayout SL = scan_layout(a.ix.row_bytes, a.k, qg);
+    const ScanLayout SL = scan_layout(a.ix.row_bytes, a.k);
     scan_fn f = a.ix.dtype == 0 ? scan_pick<0>(SL.ts, SL.cpl) : scan_pick<1>(SL.ts, SL.cpl);
     if (!f) return -1;
     int dev = 0, nsm = 148;
