@@ -362,7 +362,9 @@ def main():
     s0 = stats[-1]
     rb = s0["row_bytes"]
     R = c.degree_R
-    g_bytes = s0["graph_V"] * (rb + 4) + s0["graph_E"] * R * 4
+    # per graph item V vector rows + E adjacency rows of R (local, global) int32 pairs;
+    # per scan tile row: the X_LS row + its global id
+    g_bytes = s0["graph_V"] * rb + s0["graph_E"] * R * 8
     g_ms = float(np.mean([s["ms_graph"] for s in stats]))
     s_bytes = s0["scan_rows"] * (rb + 4)
     s_ms = float(np.mean([s["ms_scan"] for s in stats]))

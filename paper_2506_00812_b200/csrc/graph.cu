@@ -173,6 +173,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
                 floc[ci] = c;
             }
             __syncwarp();
+            if (nc > RP * GROUP) {
+                // more rows than one load group: put every row's 128-byte lines in flight to L2 now,
+                // so the later groups do not each pay a full DRAM round trip
+                const int lines = (row_bytes + 127) >> 7;
+                for (int e = lane; e < nc * lines; e += 32) {
+                    const int r = e / lines, l = e - r * lines;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(ix.X + (int64_t)fgid[r] * row_bytes + l * 128));
+                }
+            }
             for (int p0 = 0; p0 < nc; p0 += RP * GROUP) {
                 uint4 xv[GROUP][MAXCPL];
 #pragma unroll

@@ -159,10 +159,17 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
             a.segs[seg0 + g] = sg;
             for (int t = 0; t < ntile; t++) {
                 Tile tl;
+                tl.base = d.base;
                 tl.seg = seg0 + g;
                 tl.row_begin = t * a.tile_rows;
                 tl.row_end = min(d.size, (t + 1) * a.tile_rows);
                 tl.tile_in_seg = t;
+                tl.label = it.label;
+                tl.nq = sg.n_items;
+                tl.item_base = sg.item_base;
+                tl.n_tiles = ntile;
+                tl.hs = d.size >= a.ix.T;
+                tl.pad = 0;
                 a.tiles[tb + g * ntile + t] = tl;
             }
         }
@@ -183,6 +190,14 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
             it.meta |= META_MULTI;       // finalised in the scan kernel (last tile done)
             a.items[s] = it;
         }
+        ScanQuery sq;
+        sq.p_off = a.q_off[it.qid];
+        sq.slot = (int32_t)s;
+        sq.qid = it.qid;
+        sq.meta = it.meta;
+        sq.nl = a.qinfo[it.qid].nl;
+        sq.pad[0] = sq.pad[1] = 0;
+        a.scan_q[a.ls_itembase[d.bslot] + it.rank] = sq;
         if (it.rank == 0) a.ls_count[d.bslot] = 0;   // bucket counters stay zero between searches
     }
 }
@@ -213,8 +228,9 @@ __global__ void k_gather_rows(const uint8_t *__restrict__ X, int row_bytes, cons
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = e / words;
         const int c = (int)(e - r * words);
+        const int32_t id = ids[r];                    // -1: alignment padding row -> zeros
         reinterpret_cast<uint4 *>(out + r * row_bytes)[c] =
-            __ldg(reinterpret_cast<const uint4 *>(X + (int64_t)ids[r] * row_bytes) + c);
+            id < 0 ? make_uint4(0, 0, 0, 0) : __ldg(reinterpret_cast<const uint4 *>(X + (int64_t)id * row_bytes) + c);
     }
 }
 

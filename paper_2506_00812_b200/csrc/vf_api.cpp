@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -65,7 +66,7 @@ struct DevBuf {
 };
 
 struct Scratch {
-    DevBuf raw, Qp, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, segs, tiles, item_seg,
+    DevBuf raw, Qp, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
         item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
     size_t gtab_slots = 0, gtab_warps = 0;
     cudaEvent_t ev[8];
@@ -151,7 +152,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
 
     // -- validate posting lists (ascending global ids) and graphs
     if (po[0] != 0) return fail(VF_ERR_INVALID_ARG, "posting_offsets[0] must be 0");
-    int64_t hs_rows = 0, ls_rows = 0, n_hs = 0, n_ls = 0;
+    int64_t hs_rows = 0, ls_rows = 0, ls_rows_pad = 0, n_hs = 0, n_ls = 0;
     int32_t max_ls = 0, max_any = 0;
     for (int l = 0; l < L; l++) {
         const int64_t a = po[l], b = po[l + 1];
@@ -180,6 +181,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
             if (rows != 0 && rows != S)
                 return fail(VF_ERR_INVALID_ARG, "graph rows of label " + std::to_string(l) + " must be 0 or |C_l|");
             ls_rows += S;
+            ls_rows_pad += (S + 3) & ~3ll;        // label bases 4-row aligned (16-byte id slices)
             n_ls++;
             max_ls = std::max<int32_t>(max_ls, (int32_t)S);
         }
@@ -216,7 +218,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     }
     // -- directory + M_HS / G_HS (compacted, ordered by label) + M_LS
     std::vector<LabelDir> dir(std::max(L, 1));
-    std::vector<int32_t> m_hs((size_t)std::max<int64_t>(hs_rows, 1)), m_ls((size_t)std::max<int64_t>(ls_rows, 1));
+    std::vector<int32_t> m_hs((size_t)std::max<int64_t>(hs_rows, 1)), m_ls((size_t)ls_rows_pad + 4, -1);   // + slack: the last id slice is read 16 B-rounded
     std::vector<int2> g_hs((size_t)std::max<int64_t>(hs_rows * R, 1));
     int64_t hb = 0, lb = 0;
     int32_t bslot = 0;
@@ -239,7 +241,7 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
         } else {
             dir[l].base = lb;
             std::memcpy(&m_ls[lb], pi + a, S * sizeof(int32_t));
-            lb += S;
+            lb += (S + 3) & ~3ll;
         }
     }
     VF_B(ix->dir.ensure(dir.size() * sizeof(LabelDir)));
@@ -251,8 +253,8 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     VF_B(ix->M_ls.ensure(m_ls.size() * 4));
     VF_B(cudaMemcpy(ix->M_ls.p, m_ls.data(), m_ls.size() * 4, cudaMemcpyHostToDevice));
     // -- X_LS: label-contiguous row copies of the LS lists, gathered on the device
-    VF_B(ix->Xls.ensure((size_t)std::max<int64_t>(ls_rows, 1) * row_bytes));
-    launch_gather_rows(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), ls_rows, ix->Xls.as<uint8_t>(), s);
+    VF_B(ix->Xls.ensure((size_t)std::max<int64_t>(ls_rows_pad, 1) * row_bytes));
+    launch_gather_rows(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), ls_rows_pad, ix->Xls.as<uint8_t>(), s);
     VF_B(cudaGetLastError());
     // -- predicate table: point -> sorted labels, transposed from the posting lists
     std::vector<int64_t> poff((size_t)N + 1, 0);
@@ -305,8 +307,8 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     I.bytes_vectors = N * row_bytes;
     I.bytes_graph = hs_rows * R * 8;
     I.bytes_map_hs = hs_rows * 4;
-    I.bytes_ls_vectors = ls_rows * row_bytes;
-    I.bytes_map_ls = ls_rows * 4;
+    I.bytes_ls_vectors = ls_rows_pad * row_bytes;
+    I.bytes_map_ls = (ls_rows_pad + 4) * 4;
     I.bytes_predicate = (N + 1) * 8 + n_entries * 4;
     I.bytes_directory = (int64_t)L * sizeof(LabelDir);
     I.bytes_total = I.bytes_vectors + I.bytes_graph + I.bytes_map_hs + I.bytes_ls_vectors + I.bytes_map_ls +
@@ -396,7 +398,11 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     // row tiles: small in the normal path (load balance across SMs; a label split over several
     // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
     int tile_rows = p->exact ? 4096 : 512;
-    if ((scan_max + 255) / 256 > tile_rows) tile_rows = (scan_max + 255) / 256;
+    if (!p->exact) {
+        static const int env_tile = [] { const char *e = getenv("VF_TILE_ROWS"); return e ? atoi(e) : 0; }();
+        if (env_tile >= 64) tile_rows = env_tile & ~63;   // experiment knob (scripts/ab.py)
+    }
+    if ((scan_max + 255) / 256 > tile_rows) tile_rows = (((scan_max + 255) / 256) + 63) & ~63;  // x64 rows
     const int mtpl = std::max(1, (scan_max + tile_rows - 1) / tile_rows);
     const bool multi = mtpl > 1;
     const int qg = scan_qg(D.row_bytes, k);
@@ -449,6 +455,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     VF_CUDA(sc->item_ctr.ensure((size_t)slots * 12));
     VF_CUDA(sc->graph_list.ensure((size_t)slots * 4));
     VF_CUDA(sc->scan_slots.ensure((size_t)slots * 4));
+    VF_CUDA(sc->scan_q.ensure((size_t)slots * sizeof(ScanQuery)));
     VF_CUDA(sc->segs.ensure((size_t)slots * sizeof(Segment)));
     VF_CUDA(sc->tiles.ensure((size_t)max_tiles * sizeof(Tile)));
     VF_CUDA(sc->item_seg.ensure((size_t)slots * 4));
@@ -503,6 +510,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     a.ls_itembase = sc->ls_itembase.as<int32_t>();
     a.graph_list = sc->graph_list.as<int32_t>();
     a.scan_slots = sc->scan_slots.as<int32_t>();
+    a.scan_q = sc->scan_q.as<ScanQuery>();
     a.segs = sc->segs.as<Segment>();
     a.tiles = sc->tiles.as<Tile>();
     a.item_seg = sc->item_seg.as<int32_t>();

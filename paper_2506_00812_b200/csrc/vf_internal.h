@@ -69,11 +69,29 @@ struct Segment {
     int32_t pad[3];
 };
 
+// A row tile of a segment: everything the scan producer needs in one 48-byte record, so claiming a
+// tile costs one dependent load (written by k_segments).
 struct Tile {
+    int64_t base;        // first row of the label in X_LS (or in M_HS for an HS label, exact mode)
     int32_t seg;
-    int32_t row_begin;   // rows relative to the label's first LS row
+    int32_t row_begin;   // rows relative to the label's first row
     int32_t row_end;
     int32_t tile_in_seg;
+    int32_t label;
+    int32_t nq;          // queries of the segment
+    int32_t item_base;   // first entry of the segment in scan_slots / scan_q
+    int32_t n_tiles;
+    int32_t hs;          // 1: HS label scanned in exact mode (rows gathered through M_HS)
+    int32_t pad;
+};
+
+// Per scan item, in scan_slots order: what the scan needs about its query (written by k_scatter).
+struct ScanQuery {
+    int64_t p_off;       // offset of the query's sorted labels (the AND predicate)
+    int32_t slot, qid;
+    uint32_t meta;
+    int32_t nl;
+    int32_t pad[2];
 };
 
 // Device counters, zeroed at the start of every search.
@@ -105,6 +123,7 @@ struct SearchArgs {
     int32_t *ls_itembase;     // [n_bslots] first scan_slots entry of the label
     int32_t *graph_list;      // [slots]
     int32_t *scan_slots;      // [slots]
+    ScanQuery *scan_q;        // [slots] per scan item, scan_slots order
     Segment *segs;            // [slots]
     Tile *tiles;              // [max_tiles]
     int32_t *item_seg;        // [slots] segment of a scan item (multi-tile merge)

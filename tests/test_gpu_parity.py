@@ -248,6 +248,8 @@ def test_byte_accounting(vf, tiny):
     assert info["hs_rows"] == hs and info["ls_rows"] == ls
     assert info["bytes_vectors"] == w.cfg.n_points * rb
     assert info["bytes_graph"] == hs * w.cfg.degree_R * 8      # (local, global) edge pairs
-    assert info["bytes_ls_vectors"] == ls * rb
+    ls_sizes = sizes[(sizes > 0) & (sizes < w.cfg.threshold_T)]
+    ls_pad = int(((ls_sizes + 3) // 4 * 4).sum())                 # 4-row aligned label bases
+    assert info["bytes_ls_vectors"] == ls_pad * rb
     # redundancy bypassing saves exactly the HS vector copies
     assert info["bytes_total"] < info["bytes_total"] + hs * rb
