@@ -115,6 +115,23 @@ typedef struct {
 vf_status vf_build_index(const vf_build_desc *desc, vf_index **out);
 
 /*
+ * Label sharding on ONE device (SURVEY §8(e) "virtual shards"): builds n_shards label shards of the
+ * index (the same LPT ownership as a world_size = n_shards NCCL group) on desc->device and runs
+ * the sharded protocol -- route, ship items to their owners, execute, return, merge -- with an
+ * in-process transport. vf_search on it splits the batch into n_shards contiguous chunks (one per
+ * origin shard) and returns results identical to vf_build_index. Host query / result buffers
+ * only. desc->world_size / rank / nccl_unique_id are ignored. 1 <= n_shards <= 16.
+ */
+vf_status vf_build_index_virtual_shards(const vf_build_desc *desc, int32_t n_shards, vf_index **out);
+
+/*
+ * The label -> rank ownership used by label sharding: greedy LPT over the posting sizes (labels by
+ * size descending, ties by id; each to the least-loaded rank, ties to the lower rank). Pure host
+ * function, deterministic, identical on every rank. sizes [n_labels] host, owner [n_labels] host out.
+ */
+vf_status vf_partition_labels(int32_t n_labels, const int64_t *sizes, int32_t world, int32_t *owner);
+
+/*
  * Search a batch (Alg. 2). queries [n_queries][dim] (host or device, dtype of the index);
  * query labels as CSR: qlabel_offsets [n_queries+1] int64, qlabels int32 (host or device; label
  * ids outside [0, n_labels) are "unknown": empty posting list, reading #19). Outputs out_ids

@@ -22,7 +22,8 @@ VF_RECALL_GREEDY, VF_RECALL_PARALLEL = 0, 1
 OPS = {"single": VF_SINGLE, "or": VF_OR, "and": VF_AND}
 MODES = {"greedy": VF_RECALL_GREEDY, "parallel": VF_RECALL_PARALLEL}
 EXPORTED = ("vf_build_index", "vf_search", "vf_free", "vf_last_error", "vf_get_index_info",
-            "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items")
+            "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items", "vf_build_index_virtual_shards",
+            "vf_partition_labels")
 
 
 class VfError(RuntimeError):
@@ -96,6 +97,10 @@ def lib():
         L.vf_get_last_stats.argtypes = [p, p, C.POINTER(SearchStats)]
         L.vf_get_last_items.restype = C.c_int
         L.vf_get_last_items.argtypes = [p, p, i64, p, C.POINTER(i64)]
+        L.vf_build_index_virtual_shards.restype = C.c_int
+        L.vf_build_index_virtual_shards.argtypes = [C.POINTER(BuildDesc), i32, C.POINTER(p)]
+        L.vf_partition_labels.restype = C.c_int
+        L.vf_partition_labels.argtypes = [i32, p, i32, p]
         _lib = L
     return _lib
 
@@ -135,7 +140,7 @@ class Index:
     """Device-resident label-centric index: vf_build_index / vf_search / vf_free."""
 
     def __init__(self, X, post_off, post_ids, threshold_T, degree_R=16, graph_off=None,
-                 graph_ids=None, device=0, world_size=1, rank=0, nccl_unique_id=None):
+                 graph_ids=None, device=0, world_size=1, rank=0, nccl_unique_id=None, virtual_shards=0):
         X = np.ascontiguousarray(X)
         self._keep = [X, np.ascontiguousarray(post_off, np.int64), np.ascontiguousarray(post_ids, np.int32)]
         self.dtype = _dtype_code(X)
@@ -159,7 +164,10 @@ class Index:
             self._uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
             d.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         h = C.c_void_p()
-        _check(lib().vf_build_index(C.byref(d), C.byref(h)))
+        if virtual_shards:
+            _check(lib().vf_build_index_virtual_shards(C.byref(d), int(virtual_shards), C.byref(h)))
+        else:
+            _check(lib().vf_build_index(C.byref(d), C.byref(h)))
         self._h = h
         self._keep = None   # the library copied everything
 
@@ -219,3 +227,21 @@ class Index:
         rec = np.empty((max(n.value, 1), 6), np.int32)
         _check(lib().vf_get_last_items(self._h, _stream_ptr(stream), n.value, _ptr(rec), C.byref(n)))
         return rec[:n.value]
+
+
+def partition_labels(sizes, world):
+    """vf_partition_labels: label -> rank ownership (greedy LPT over |C_l|)."""
+    sizes = np.ascontiguousarray(sizes, np.int64)
+    owner = np.empty(max(1, sizes.size), np.int32)
+    _check(lib().vf_partition_labels(sizes.size, _ptr(sizes), int(world), _ptr(owner)))
+    return owner[:sizes.size]
+
+
+def nccl_unique_id():
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it and broadcasts it with torch.distributed)."""
+    import ctypes.util
+    h = C.CDLL("libnccl.so.2")
+    buf = C.create_string_buffer(128)
+    if h.ncclGetUniqueId(buf) != 0:
+        raise VfError(VF_ERR_NCCL, "ncclGetUniqueId failed")
+    return bytes(buf.raw)

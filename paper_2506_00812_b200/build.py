@@ -12,8 +12,8 @@ OUT = os.path.join(HERE, "libvecflow.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["route.cu", "scan.cu", "graph.cu", "merge.cu"]
-CPP = ["vf_api.cpp"]
-HEADERS = ["vf_internal.h", "common.cuh"]
+CPP = ["vf_api.cpp", "shard.cpp"]
+HEADERS = ["vf_internal.h", "common.cuh", "host_internal.h"]
 
 
 def _sources():
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         objs.append(obj)
     tmp = OUT + ".tmp"
-    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs
+    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

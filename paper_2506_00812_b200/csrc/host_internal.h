@@ -1,0 +1,134 @@
+// Host-side internals shared by vf_api.cpp (index build, single-index search) and shard.cpp (label
+// sharding, §8(e)). Not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "vf.h"
+#include "vf_internal.h"
+
+namespace vf {
+
+vf_status fail(vf_status s, const std::string &m);
+
+#define VF_CUDA(x)                                                                               \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) {                                                                 \
+            vf_status st_ = e_ == cudaErrorMemoryAllocation ? VF_ERR_OUT_OF_MEMORY : VF_ERR_CUDA; \
+            return ::vf::fail(st_, std::string(#x) + ": " + cudaGetErrorString(e_));            \
+        }                                                                                        \
+    } while (0)
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    // grow to at least `bytes` (contents not preserved)
+    cudaError_t ensure(size_t bytes, bool *fresh = nullptr) {
+        if (fresh) *fresh = false;
+        if (bytes <= n && p) return cudaSuccess;
+        release();
+        const size_t want = bytes < 256 ? 256 : bytes;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return e;
+        }
+        n = want;
+        if (fresh) *fresh = true;
+        return cudaSuccess;
+    }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// Per-stream (and per role) scratch of a search.
+struct Scratch {
+    DevBuf raw, Qp, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
+        item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
+    // label sharding: item records out / in, returned results, slots of the sent items
+    DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
+    size_t gtab_slots = 0, gtab_warps = 0;
+    cudaEvent_t ev[8];
+    bool ev_ok = false;
+    bool profiled = false;
+    SearchArgs last{};
+    int64_t last_slots = 0;
+    int last_launches = 0;
+    bool has_last = false;
+    ~Scratch() {
+        if (ev_ok)
+            for (auto &e : ev) cudaEventDestroy(e);
+    }
+};
+
+struct Transport;
+
+struct vf_index_impl;
+}  // namespace vf
+
+struct vf_index {
+    vf::DevIndex dev{};
+    int device = 0;
+    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev;
+    vf_index_info info{};
+    int32_t max_ls_size = 0, max_label_size = 0;
+    std::mutex mu;
+    std::unordered_map<uint64_t, vf::Scratch *> scratch;   // (stream, role) -> scratch
+    bool profiling = false;
+    // label sharding (§8(e))
+    int world = 1, rank = 0;
+    std::vector<int32_t> owner;                 // [n_labels] owning rank (host copy)
+    vf::Transport *transport = nullptr;         // NCCL (one rank per process) or loopback
+    std::vector<vf_index *> vshards;            // virtual shards on one device (loopback transport)
+    ~vf_index();
+};
+
+namespace vf {
+
+Scratch *get_scratch(vf_index *ix, cudaStream_t s, int role);
+bool is_device_ptr(const void *p);
+
+// Plan of one search pass over a batch on one index (shard).
+struct Plan {
+    SearchArgs a{};
+    int64_t n_slots = 0;
+    int qg = 0;
+    int64_t max_tiles = 0;
+    int graph_ctas = 0;
+    bool multi = false;
+};
+
+// Size every scratch buffer for a batch of n queries / n_slots item slots and fill the SearchArgs
+// (queries, labels and outputs are bound by the caller).
+vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, const vf_search_params *p,
+                      cudaStream_t s, Plan *out);
+// route (k_prepare) or unpack received items, then bucket, scan and graph for the local items.
+vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
+                    int rec_bytes, int *launches);
+
+// Label sharding entry points (shard.cpp).
+vf_status shard_partition(int32_t n_labels, const int64_t *sizes, int32_t world, int32_t *owner);
+vf_status nccl_transport_create(const void *unique_id, int world, int rank, Transport **out);
+vf_status loopback_transport_create(Transport **out);
+void transport_destroy(Transport *t);
+vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void *> &queries,
+                         std::vector<int64_t> &nq, std::vector<const int64_t *> &qoff,
+                         std::vector<const int32_t *> &qlab, const vf_search_params *p,
+                         std::vector<int32_t *> &out_ids, std::vector<float *> &out_dists, Transport *tr,
+                         cudaStream_t s);
+
+}  // namespace vf

@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
             for (int t = 0; t < nch; t++) {           // routing equation
                 const int32_t s = lsize(chosen[t]);
                 cpath[t] = (a.exact || s < ix.T) ? PATH_SCAN : PATH_GRAPH;
+                // label sharding: an item whose label lives on another rank is shipped there
+                if (ix.owner && ix.owner[chosen[t]] != ix.rank) cpath[t] |= META_REMOTE;
                 ngraph += cpath[t] == PATH_GRAPH;
             }
             QueryInfo qi;
@@ -113,8 +115,10 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
             if (t < nch) {
                 const int32_t l = chosen[t];
                 it.label = l;
-                it.meta = cpath[t] | pred | (nch == 1 ? META_DIRECT : 0u);
-                if (cpath[t] == PATH_SCAN) it.rank = atomicAdd(a.ls_count + ix.dir[l].bslot, 1);
+                const bool remote = (cpath[t] & META_REMOTE) != 0;
+                it.meta = cpath[t] | pred | (nch == 1 && !remote ? META_DIRECT : 0u);
+                if (remote) atomicAdd(&a.ctr->remote[ix.owner[l]], 1);
+                else if (cpath[t] == PATH_SCAN) it.rank = atomicAdd(a.ls_count + ix.dir[l].bslot, 1);
                 else a.graph_list[gpos++] = (int32_t)(lo + t);
             } else {
                 it.label = -1;
@@ -138,7 +142,7 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
          s += (int64_t)gridDim.x * blockDim.x) {
         const Item it = a.items[s];
-        if ((it.meta & 3u) != PATH_SCAN || it.rank != 0) continue;
+        if ((it.meta & (3u | META_REMOTE)) != PATH_SCAN || it.rank != 0) continue;
         const LabelDir d = a.ix.dir[it.label];
         const int count = a.ls_count[d.bslot];
         const int nseg = (count + qg - 1) / qg;
@@ -180,7 +184,7 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots;
          s += (int64_t)gridDim.x * blockDim.x) {
         Item it = a.items[s];
-        if ((it.meta & 3u) != PATH_SCAN) continue;
+        if ((it.meta & (3u | META_REMOTE)) != PATH_SCAN) continue;
         const LabelDir d = a.ix.dir[it.label];
         const int seg = a.ls_segbase[d.bslot] + it.rank / qg;
         a.scan_slots[a.ls_itembase[d.bslot] + it.rank] = (int32_t)s;
@@ -255,6 +259,103 @@ void launch_pad_rows(const uint8_t *src, int src_bytes, int64_t n, int row_bytes
                      cudaStream_t s) {
     if (n == 0) return;
     k_pad_rows<<<148 * 8, 256, 0, s>>>(src, src_bytes, n, row_bytes, dst);
+}
+
+// ---------------------------------------------------------------- label sharding (§8(e))
+// Origin rank: pack every remote item into the send buffer region of its owner.
+__global__ void k_pack_remote(SearchArgs a, int64_t n_slots, uint8_t *__restrict__ send,
+                              const int64_t *__restrict__ dst_off, int32_t *__restrict__ sent_slots, int rec_bytes) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp per slot
+    if (s >= n_slots) return;
+    const Item it = a.items[s];
+    if (!(it.meta & META_REMOTE)) return;
+    const int dst = a.ix.owner[it.label];
+    int pos = 0;
+    if (lane == 0) pos = atomicAdd(&a.ctr->remote_pos[dst], 1);
+    pos = __shfl_sync(FULL, pos, 0);
+    const int64_t idx = dst_off[dst] + pos;
+    uint8_t *rec = send + idx * (int64_t)rec_bytes;
+    ItemRecord *h = reinterpret_cast<ItemRecord *>(rec);
+    const QueryInfo qi = a.qinfo[it.qid];
+    const int32_t *L = a.qlab + a.q_off[it.qid];
+    if (lane == 0) {
+        h->origin_slot = (int32_t)s;
+        h->label = it.label;
+        h->nl = qi.nl;
+        h->pred = it.meta & META_PRED;
+        h->qh = qi.qh;
+        h->pad[0] = h->pad[1] = h->pad[2] = 0;
+        sent_slots[idx] = (int32_t)s;
+    }
+    if (lane < kRecLabels) h->labels[lane] = lane < qi.nl ? L[lane] : -1;
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.Qp + (int64_t)it.qid * a.ix.row_bytes);
+    uint4 *dst_row = reinterpret_cast<uint4 *>(rec + sizeof(ItemRecord));
+    for (int c = lane; c < a.ix.chunks; c += 32) dst_row[c] = src[c];
+}
+
+// Owner rank: received records become a batch of single-item queries (query i = record i, item
+// slot i, labels at qlab[i * kRecLabels]) whose results are written directly to out_ids/out_dists.
+__global__ void k_unpack_items(SearchArgs a, const uint8_t *__restrict__ recv, int64_t n, int rec_bytes) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const uint8_t *rec = recv + i * (int64_t)rec_bytes;
+    const ItemRecord *h = reinterpret_cast<const ItemRecord *>(rec);
+    const uint4 *src = reinterpret_cast<const uint4 *>(rec + sizeof(ItemRecord));
+    uint4 *dst = reinterpret_cast<uint4 *>(const_cast<uint8_t *>(a.Qp) + i * (int64_t)a.ix.row_bytes);
+    for (int c = lane; c < a.ix.chunks; c += 32) dst[c] = src[c];
+    if (lane < kRecLabels) a.qlab[i * kRecLabels + lane] = h->labels[lane];
+    if (lane == 0) {
+        int64_t *qoff = const_cast<int64_t *>(a.q_off);
+        qoff[i] = i * kRecLabels;
+        if (i == n - 1) qoff[n] = n * kRecLabels;
+        const int32_t l = h->label;
+        const LabelDir d = a.ix.dir[l];
+        QueryInfo qi;
+        qi.nl = h->nl; qi.n_items = 1; qi.qh = h->qh; qi.pad = 0;
+        a.qinfo[i] = qi;
+        const uint32_t path = (a.exact || d.size < a.ix.T) ? PATH_SCAN : PATH_GRAPH;
+        Item it;
+        it.qid = (int32_t)i;
+        it.label = l;
+        it.rank = 0;
+        it.meta = path | h->pred | META_DIRECT;
+        if (path == PATH_SCAN) it.rank = atomicAdd(a.ls_count + d.bslot, 1);
+        else a.graph_list[atomicAdd(&a.ctr->n_graph, 1)] = (int32_t)i;
+        a.items[i] = it;
+    }
+}
+
+// Origin rank: results returned by the owners (in send order) become the remote items' keys.
+__global__ void k_scatter_results(SearchArgs a, const int32_t *__restrict__ ids, const float *__restrict__ dists,
+                                  const int32_t *__restrict__ sent_slots, int64_t n) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * a.k) return;
+    const int64_t j = e / a.k;
+    const int t = (int)(e - j * a.k);
+    const int32_t id = ids[e];
+    a.item_res[(size_t)sent_slots[j] * a.k + t] = id < 0 ? KEY_INF : make_key(dists[e], (uint32_t)id);
+}
+
+int launch_pack_remote(const SearchArgs &a, cudaStream_t s, int64_t n_slots, uint8_t *send, const int64_t *dst_off,
+                       int32_t *sent_slots, int rec_bytes) {
+    if (n_slots == 0) return 0;
+    k_pack_remote<<<(unsigned)((n_slots * 32 + 255) / 256), 256, 0, s>>>(a, n_slots, send, dst_off, sent_slots, rec_bytes);
+    return 1;
+}
+
+int launch_unpack_items(const SearchArgs &a, cudaStream_t s, const uint8_t *recv, int64_t n, int rec_bytes) {
+    if (n == 0) return 0;
+    k_unpack_items<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(a, recv, n, rec_bytes);
+    return 1;
+}
+
+int launch_scatter_results(const SearchArgs &a, cudaStream_t s, const int32_t *ids, const float *dists,
+                           const int32_t *sent_slots, int64_t n) {
+    if (n == 0) return 0;
+    k_scatter_results<<<(unsigned)((n * a.k + 255) / 256), 256, 0, s>>>(a, ids, dists, sent_slots, n);
+    return 1;
 }
 
 }  // namespace vf

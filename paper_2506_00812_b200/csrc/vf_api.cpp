@@ -1,103 +1,26 @@
 // C-ABI of libvecflow (include/vf.h): validation, index build (Alg. 1) into the HBM
 // layout of DESIGN.md §5, and the per-batch orchestration of the search path (Alg. 2): copies,
-// route/bucket (a1), scan (a2), graph (a3), merge (a5). Host code only plans and launches;
-// every step of the search runs in the CUDA kernels of this directory.
-#include "vf.h"
-
+// route/bucket (a1), scan (a2), graph (a3), merge (a5). Host code only plans and launches; every
+// step of the search runs in the CUDA kernels of this directory. Label sharding (§8(e)) is in
+// shard.cpp.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <mutex>
-#include <string>
-#include <unordered_map>
-#include <vector>
 
-#include "vf_internal.h"
+#include "host_internal.h"
 
 namespace vf {
 int scan_qg(int row_bytes, int k);
-}
-
-using namespace vf;
 
 static thread_local std::string g_err;
 
-static vf_status fail(vf_status s, const std::string &m) {
+vf_status fail(vf_status s, const std::string &m) {
     g_err = m;
     return s;
 }
 
-#define VF_CUDA(x)                                                                              \
-    do {                                                                                        \
-        cudaError_t e_ = (x);                                                                   \
-        if (e_ != cudaSuccess) {                                                                \
-            vf_status st_ = e_ == cudaErrorMemoryAllocation ? VF_ERR_OUT_OF_MEMORY : VF_ERR_CUDA;\
-            return fail(st_, std::string(#x) + ": " + cudaGetErrorString(e_));                  \
-        }                                                                                       \
-    } while (0)
-
-// ------------------------------------------------------------------ device buffers
-struct DevBuf {
-    void *p = nullptr;
-    size_t n = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf &) = delete;
-    DevBuf &operator=(const DevBuf &) = delete;
-    ~DevBuf() { release(); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    // grow to at least `bytes` (contents not preserved); returns true if reallocated
-    cudaError_t ensure(size_t bytes, bool *fresh = nullptr) {
-        if (fresh) *fresh = false;
-        if (bytes <= n && p) return cudaSuccess;
-        release();
-        size_t want = bytes < 256 ? 256 : bytes;
-        cudaError_t e = cudaMalloc(&p, want);
-        if (e != cudaSuccess) { p = nullptr; return e; }
-        n = want;
-        if (fresh) *fresh = true;
-        return cudaSuccess;
-    }
-    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
-};
-
-struct Scratch {
-    DevBuf raw, Qp, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
-        item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
-    size_t gtab_slots = 0, gtab_warps = 0;
-    cudaEvent_t ev[8];
-    bool ev_ok = false;
-    bool profiled = false;
-    SearchArgs last{};
-    int64_t last_slots = 0;
-    int last_launches = 0;
-    bool has_last = false;
-    ~Scratch() {
-        if (ev_ok)
-            for (auto &e : ev) cudaEventDestroy(e);
-    }
-};
-
-struct vf_index {
-    DevIndex dev{};
-    int device = 0;
-    DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab;
-    vf_index_info info{};
-    int32_t max_ls_size = 0, max_label_size = 0;
-    std::mutex mu;
-    std::unordered_map<cudaStream_t, Scratch *> scratch;
-    bool profiling = false;
-    ~vf_index() {
-        for (auto &kv : scratch) delete kv.second;
-    }
-};
-
-// ------------------------------------------------------------------ helpers
-static bool is_device_ptr(const void *p) {
+bool is_device_ptr(const void *p) {
     if (!p) return false;
     cudaPointerAttributes at;
     cudaError_t e = cudaPointerGetAttributes(&at, p);
@@ -116,7 +39,27 @@ static uint64_t pow2ceil(uint64_t x) {
     return p;
 }
 
-extern "C" const char *vf_last_error(void) { return g_err.c_str(); }
+Scratch *get_scratch(vf_index *ix, cudaStream_t s, int role) {
+    std::lock_guard<std::mutex> g(ix->mu);
+    const uint64_t key = (uint64_t)(uintptr_t)s * 4 + (uint64_t)role;
+    auto it = ix->scratch.find(key);
+    if (it != ix->scratch.end()) return it->second;
+    Scratch *sc = new Scratch();
+    ix->scratch[key] = sc;
+    return sc;
+}
+
+}  // namespace vf
+
+using namespace vf;
+
+vf_index::~vf_index() {
+    for (auto &kv : scratch) delete kv.second;
+    for (vf_index *s : vshards) delete s;
+    if (transport) transport_destroy(transport);
+}
+
+extern "C" const char *vf_last_error(void) { return vf::g_err.c_str(); }
 
 extern "C" void vf_free(vf_index *index) {
     if (!index) return;
@@ -125,9 +68,7 @@ extern "C" void vf_free(vf_index *index) {
 }
 
 // ------------------------------------------------------------------ build (Alg. 1)
-extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
-    if (!out) return fail(VF_ERR_INVALID_ARG, "out is NULL");
-    *out = nullptr;
+static vf_status validate_desc(const vf_build_desc *d) {
     if (!d) return fail(VF_ERR_INVALID_ARG, "desc is NULL");
     if (d->dtype != VF_U8 && d->dtype != VF_F32) return fail(VF_ERR_INVALID_ARG, "dtype must be VF_U8 or VF_F32");
     if (d->dim < 1 || (int64_t)d->dim * elem_size(d->dtype) > 4096)
@@ -139,21 +80,13 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
         return fail(VF_ERR_INVALID_ARG, "posting lists are NULL");
     if (d->threshold_T < 1) return fail(VF_ERR_INVALID_ARG, "threshold_T must be >= 1");
     if (d->degree_R < 1 || d->degree_R > 64) return fail(VF_ERR_INVALID_ARG, "degree_R must be in [1, 64]");
-    if (d->world_size != 1 && d->world_size != 0)
-        return fail(VF_ERR_INVALID_ARG, "world_size > 1: use the sharded build (vf_shard.cpp)");
-
     const int64_t N = d->n_points;
     const int L = d->n_labels, R = d->degree_R, T = d->threshold_T;
-    const int es = elem_size(d->dtype);
-    const int raw_bytes = d->dim * es;
-    const int row_bytes = (raw_bytes + 15) & ~15;
     const int64_t *po = d->posting_offsets;
     const int32_t *pi = d->posting_ids;
-
-    // -- validate posting lists (ascending global ids) and graphs
     if (po[0] != 0) return fail(VF_ERR_INVALID_ARG, "posting_offsets[0] must be 0");
-    int64_t hs_rows = 0, ls_rows = 0, ls_rows_pad = 0, n_hs = 0, n_ls = 0;
-    int32_t max_ls = 0, max_any = 0;
+    if (d->graph_row_offsets && d->graph_row_offsets[0] != 0)
+        return fail(VF_ERR_INVALID_ARG, "graph_row_offsets[0] must be 0");
     for (int l = 0; l < L; l++) {
         const int64_t a = po[l], b = po[l + 1];
         if (b < a) return fail(VF_ERR_INVALID_ARG, "posting_offsets not non-decreasing at label " + std::to_string(l));
@@ -166,7 +99,6 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
         }
         const int64_t S = b - a;
         if (S == 0) continue;
-        max_any = std::max<int32_t>(max_any, (int32_t)S);
         const int64_t rows = d->graph_row_offsets ? d->graph_row_offsets[l + 1] - d->graph_row_offsets[l] : 0;
         if (S >= T) {
             if (rows != S)
@@ -175,24 +107,53 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
             for (int64_t e = 0; e < S * R; e++)
                 if (g[e] < -1 || g[e] >= S)
                     return fail(VF_ERR_INVALID_ARG, "graph entry outside [-1, |C_l|) in label " + std::to_string(l));
+        } else if (rows != 0 && rows != S) {
+            return fail(VF_ERR_INVALID_ARG, "graph rows of label " + std::to_string(l) + " must be 0 or |C_l|");
+        }
+    }
+    return VF_OK;
+}
+
+// One rank's index: X and the predicate table replicated, graphs / LS rows only of the labels
+// this rank owns (all labels when owner is empty). The directory keeps |C_l| of every label so
+// routing decisions (path, greedy l*) are the same on every rank.
+static vf_status build_one(const vf_build_desc *d, int world, int rank, const std::vector<int32_t> &owner,
+                           vf_index **out) {
+    const int64_t N = d->n_points;
+    const int L = d->n_labels, R = d->degree_R, T = d->threshold_T;
+    const int raw_bytes = d->dim * elem_size(d->dtype);
+    const int row_bytes = (raw_bytes + 15) & ~15;
+    const int64_t *po = d->posting_offsets;
+    const int32_t *pi = d->posting_ids;
+    auto mine = [&](int l) { return owner.empty() || owner[l] == rank; };
+
+    int64_t hs_rows = 0, ls_rows = 0, ls_rows_pad = 0, n_hs = 0, n_ls = 0;
+    int32_t max_ls = 0, max_any = 0;
+    for (int l = 0; l < L; l++) {
+        const int64_t S = po[l + 1] - po[l];
+        if (S == 0 || !mine(l)) continue;
+        max_any = std::max<int32_t>(max_any, (int32_t)S);
+        if (S >= T) {
             hs_rows += S;
             n_hs++;
         } else {
-            if (rows != 0 && rows != S)
-                return fail(VF_ERR_INVALID_ARG, "graph rows of label " + std::to_string(l) + " must be 0 or |C_l|");
             ls_rows += S;
             ls_rows_pad += (S + 3) & ~3ll;        // label bases 4-row aligned (16-byte id slices)
             n_ls++;
             max_ls = std::max<int32_t>(max_ls, (int32_t)S);
         }
     }
-    if (d->graph_row_offsets && d->graph_row_offsets[0] != 0)
-        return fail(VF_ERR_INVALID_ARG, "graph_row_offsets[0] must be 0");
 
     VF_CUDA(cudaSetDevice(d->device));
     vf_index *ix = new vf_index();
     ix->device = d->device;
-    auto bail = [&](vf_status s) { delete ix; return s; };
+    ix->world = world;
+    ix->rank = rank;
+    ix->owner = owner;
+    auto bail = [&](vf_status st) {
+        delete ix;
+        return st;
+    };
 #define VF_B(x)                                                                                  \
     do {                                                                                         \
         cudaError_t e_ = (x);                                                                    \
@@ -216,18 +177,19 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
             VF_B(cudaDeviceSynchronize());
         }
     }
-    // -- directory + M_HS / G_HS (compacted, ordered by label) + M_LS
+    // -- directory + G_HS (fat rows, compacted by label) + M_HS + M_LS
     std::vector<LabelDir> dir(std::max(L, 1));
-    std::vector<int32_t> m_hs((size_t)std::max<int64_t>(hs_rows, 1)), m_ls((size_t)ls_rows_pad + 4, -1);   // + slack: the last id slice is read 16 B-rounded
+    std::vector<int32_t> m_hs((size_t)std::max<int64_t>(hs_rows, 1));
+    std::vector<int32_t> m_ls((size_t)ls_rows_pad + 4, -1);   // + slack: the last id slice is read 16 B-rounded
     std::vector<int2> g_hs((size_t)std::max<int64_t>(hs_rows * R, 1));
     int64_t hb = 0, lb = 0;
     int32_t bslot = 0;
     for (int l = 0; l < L; l++) {
         const int64_t a = po[l], S = po[l + 1] - po[l];
-        dir[l].size = (int32_t)S;
+        dir[l].size = (int32_t)S;          // every label's size: routing is identical on all ranks
         dir[l].bslot = -1;
-        dir[l].base = 0;
-        if (S == 0) continue;
+        dir[l].base = -1;
+        if (S == 0 || !mine(l)) continue;
         dir[l].bslot = bslot++;
         if (S >= T) {
             dir[l].base = hb;
@@ -272,6 +234,10 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     VF_B(cudaMemcpy(ix->pt_off.p, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice));
     VF_B(ix->pt_lab.ensure(plab.size() * 4));
     VF_B(cudaMemcpy(ix->pt_lab.p, plab.data(), plab.size() * 4, cudaMemcpyHostToDevice));
+    if (!owner.empty()) {
+        VF_B(ix->owner_dev.ensure(owner.size() * 4));
+        VF_B(cudaMemcpy(ix->owner_dev.p, owner.data(), owner.size() * 4, cudaMemcpyHostToDevice));
+    }
     VF_B(cudaDeviceSynchronize());
 
     DevIndex &D = ix->dev;
@@ -292,6 +258,9 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     D.M_ls = ix->M_ls.as<int32_t>();
     D.pt_off = ix->pt_off.as<int64_t>();
     D.pt_lab = ix->pt_lab.as<int32_t>();
+    D.owner = owner.empty() ? nullptr : ix->owner_dev.as<int32_t>();
+    D.rank = rank;
+    D.world = world;
     ix->max_ls_size = max_ls;
     ix->max_label_size = max_any;
 
@@ -310,15 +279,93 @@ extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
     I.bytes_ls_vectors = ls_rows_pad * row_bytes;
     I.bytes_map_ls = (ls_rows_pad + 4) * 4;
     I.bytes_predicate = (N + 1) * 8 + n_entries * 4;
-    I.bytes_directory = (int64_t)L * sizeof(LabelDir);
+    I.bytes_directory = (int64_t)L * sizeof(LabelDir) + (owner.empty() ? 0 : (int64_t)L * 4);
     I.bytes_total = I.bytes_vectors + I.bytes_graph + I.bytes_map_hs + I.bytes_ls_vectors + I.bytes_map_ls +
                     I.bytes_predicate + I.bytes_directory;
-    I.world_size = 1;
-    I.rank = 0;
+    I.world_size = world;
+    I.rank = rank;
     I.owned_labels = n_hs + n_ls;
     *out = ix;
     return VF_OK;
 #undef VF_B
+}
+
+static std::vector<int64_t> label_sizes(const vf_build_desc *d) {
+    std::vector<int64_t> sz(d->n_labels);
+    for (int l = 0; l < d->n_labels; l++) sz[l] = d->posting_offsets[l + 1] - d->posting_offsets[l];
+    return sz;
+}
+
+extern "C" vf_status vf_build_index(const vf_build_desc *d, vf_index **out) {
+    if (!out) return fail(VF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    vf_status st = validate_desc(d);
+    if (st != VF_OK) return st;
+    const int world = d->world_size < 1 ? 1 : d->world_size;
+    if (world > kMaxWorld) return fail(VF_ERR_INVALID_ARG, "world_size must be <= 16");
+    if (world == 1) return build_one(d, 1, 0, {}, out);
+    if (d->rank < 0 || d->rank >= world) return fail(VF_ERR_INVALID_ARG, "rank out of range");
+    if (!d->nccl_unique_id) return fail(VF_ERR_INVALID_ARG, "world_size > 1 needs nccl_unique_id");
+    std::vector<int64_t> sz = label_sizes(d);
+    std::vector<int32_t> owner(std::max(d->n_labels, 1));
+    shard_partition(d->n_labels, sz.data(), world, owner.data());
+    owner.resize(d->n_labels);
+    vf_index *ix = nullptr;
+    st = build_one(d, world, d->rank, owner, &ix);
+    if (st != VF_OK) return st;
+    st = nccl_transport_create(d->nccl_unique_id, world, d->rank, &ix->transport);
+    if (st != VF_OK) {
+        delete ix;
+        return st;
+    }
+    *out = ix;
+    return VF_OK;
+}
+
+extern "C" vf_status vf_build_index_virtual_shards(const vf_build_desc *d, int32_t n_shards, vf_index **out) {
+    if (!out) return fail(VF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    vf_status st = validate_desc(d);
+    if (st != VF_OK) return st;
+    if (n_shards < 1 || n_shards > kMaxWorld) return fail(VF_ERR_INVALID_ARG, "n_shards must be in [1, 16]");
+    std::vector<int64_t> sz = label_sizes(d);
+    std::vector<int32_t> owner(std::max(d->n_labels, 1));
+    shard_partition(d->n_labels, sz.data(), n_shards, owner.data());
+    owner.resize(d->n_labels);
+    vf_index *parent = new vf_index();
+    parent->device = d->device;
+    parent->world = n_shards;
+    parent->owner = owner;
+    for (int r = 0; r < n_shards; r++) {
+        vf_index *sh = nullptr;
+        st = build_one(d, n_shards, r, owner, &sh);
+        if (st != VF_OK) {
+            delete parent;
+            return st;
+        }
+        parent->vshards.push_back(sh);
+    }
+    st = loopback_transport_create(&parent->transport);
+    if (st != VF_OK) {
+        delete parent;
+        return st;
+    }
+    parent->info = parent->vshards[0]->info;
+    parent->info.owned_labels = 0;
+    parent->info.bytes_total = 0;
+    for (vf_index *sh : parent->vshards) {
+        parent->info.owned_labels += sh->info.owned_labels;
+        parent->info.bytes_total += sh->info.bytes_total;
+    }
+    parent->dev = parent->vshards[0]->dev;
+    *out = parent;
+    return VF_OK;
+}
+
+extern "C" vf_status vf_partition_labels(int32_t n_labels, const int64_t *sizes, int32_t world, int32_t *owner) {
+    if (n_labels < 0 || (n_labels > 0 && (!sizes || !owner))) return fail(VF_ERR_INVALID_ARG, "NULL argument");
+    if (world < 1 || world > kMaxWorld) return fail(VF_ERR_INVALID_ARG, "world must be in [1, 16]");
+    return shard_partition(n_labels, sizes, world, owner);
 }
 
 extern "C" vf_status vf_get_index_info(const vf_index *index, vf_index_info *info) {
@@ -330,70 +377,18 @@ extern "C" vf_status vf_get_index_info(const vf_index *index, vf_index_info *inf
 extern "C" vf_status vf_set_profiling(vf_index *index, int32_t enable) {
     if (!index) return fail(VF_ERR_INVALID_ARG, "NULL index");
     index->profiling = enable != 0;
+    for (vf_index *s : index->vshards) s->profiling = enable != 0;
     return VF_OK;
 }
 
 // ------------------------------------------------------------------ search (Alg. 2)
-static Scratch *get_scratch(vf_index *ix, cudaStream_t s) {
-    std::lock_guard<std::mutex> g(ix->mu);
-    auto it = ix->scratch.find(s);
-    if (it != ix->scratch.end()) return it->second;
-    Scratch *sc = new Scratch();
-    ix->scratch[s] = sc;
-    return sc;
-}
+namespace vf {
 
-extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, const int64_t *qoff,
-                               const int32_t *qlab, const vf_search_params *p, int32_t *out_ids,
-                               float *out_dists, void *cuda_stream) {
-    if (!ix) return fail(VF_ERR_INVALID_ARG, "index is NULL");
-    if (!p) return fail(VF_ERR_INVALID_ARG, "params is NULL");
-    if (n < 0) return fail(VF_ERR_INVALID_ARG, "n_queries < 0");
-    if (p->k < 1 || p->k > kMaxK) return fail(VF_ERR_INVALID_ARG, "k must be in [1, 256]");
-    if (p->itopk < p->k || p->itopk > kMaxItopk) return fail(VF_ERR_INVALID_ARG, "itopk must be in [k, 1024]");
-    const int R = ix->dev.R;
-    const int w = p->search_width < 1 ? 1 : p->search_width;
-    if (w * R > 64) return fail(VF_ERR_INVALID_ARG, "search_width * R must be <= 64");
-    if (p->op < 0 || p->op > 2) return fail(VF_ERR_INVALID_ARG, "op must be VF_SINGLE, VF_OR or VF_AND");
-    if (p->recall_mode < 0 || p->recall_mode > 1) return fail(VF_ERR_INVALID_ARG, "bad recall_mode");
-    if (n > 0 && (!queries || !qoff || !out_ids || !out_dists))
-        return fail(VF_ERR_INVALID_ARG, "NULL queries / offsets / outputs");
-    if (n == 0) return VF_OK;
-    VF_CUDA(cudaSetDevice(ix->device));
-    cudaStream_t s = (cudaStream_t)cuda_stream;
-    Scratch *sc = get_scratch(ix, s);
+vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, const vf_search_params *p,
+                      cudaStream_t s, Plan *out) {
     const DevIndex &D = ix->dev;
-    const int k = p->k;
-
-    const bool q_dev = is_device_ptr(queries);
-    const bool off_dev = is_device_ptr(qoff);
-    const bool lab_dev = is_device_ptr(qlab);
-    const bool out_dev = is_device_ptr(out_ids);
-    if (out_dev != is_device_ptr(out_dists))
-        return fail(VF_ERR_INVALID_ARG, "out_ids and out_dists must both be host or both be device");
-
-    int64_t n_slots = 0;
-    if (!off_dev) {
-        if (qoff[0] != 0) return fail(VF_ERR_INVALID_ARG, "qlabel_offsets[0] must be 0");
-        n_slots = qoff[n];
-        for (int64_t i = 0; i < n; i++) {
-            const int64_t c = qoff[i + 1] - qoff[i];
-            if (c < 0 || c > kMaxQueryLabels)
-                return fail(VF_ERR_INVALID_ARG, "query " + std::to_string(i) + " has a bad label count (max 64)");
-            if (p->op == VF_SINGLE && c > 1 && !lab_dev) {
-                for (int64_t e = qoff[i] + 1; e < qoff[i + 1]; e++)
-                    if (qlab[e] != qlab[qoff[i]])
-                        return fail(VF_ERR_INVALID_ARG, "VF_SINGLE query " + std::to_string(i) + " has more than one label");
-            }
-        }
-    } else {
-        VF_CUDA(cudaMemcpyAsync(&n_slots, qoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        VF_CUDA(cudaStreamSynchronize(s));
-    }
-    if (n_slots > 0 && !qlab) return fail(VF_ERR_INVALID_ARG, "qlabels is NULL");
-    if (n_slots >= (1ll << 31)) return fail(VF_ERR_INVALID_ARG, "too many query labels");
-
-    // -- plan
+    const int R = D.R, k = p->k;
+    const int w = p->search_width < 1 ? 1 : p->search_width;
     const int scan_max = p->exact ? ix->max_label_size : ix->max_ls_size;
     // row tiles: small in the normal path (load balance across SMs; a label split over several
     // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
@@ -404,14 +399,16 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     }
     if ((scan_max + 255) / 256 > tile_rows) tile_rows = (((scan_max + 255) / 256) + 63) & ~63;  // x64 rows
     const int mtpl = std::max(1, (scan_max + tile_rows - 1) / tile_rows);
-    const bool multi = mtpl > 1;
-    const int qg = scan_qg(D.row_bytes, k);
+    Plan &pl = *out;
+    pl = Plan();
+    pl.n_slots = n_slots;
+    pl.multi = mtpl > 1;
+    pl.qg = scan_qg(D.row_bytes, k);
     const int64_t slots = std::max<int64_t>(n_slots, 1);
-    const int64_t max_tiles = slots * mtpl;
+    pl.max_tiles = slots * mtpl;
     const int n_init = p->n_init > 0 ? p->n_init : R * w;
     const int max_iter = p->max_iterations > 0 ? p->max_iterations : 2 * ((p->itopk + w - 1) / w) + 16;
-    // visited sets: shared-memory table sized for ~16 warps/SM, exact global overflow table
-    // ~32 itopk-sized expansions' worth of ids in shared memory, within ~7 KB per warp
+    // visited sets: a shared-memory table within ~7 KB per warp, exact global overflow table
     int hs = 1024;
     {
         const int64_t budget = 7168 - 16ll * p->itopk - 1024;
@@ -420,7 +417,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     const int64_t v_bound = (int64_t)n_init + (int64_t)max_iter * w * R + 32;
     const uint64_t gslots = pow2ceil((uint64_t)(2 * v_bound + 64));
 
-    SearchArgs a{};
+    SearchArgs &a = pl.a;
     a.ix = D;
     a.n_q = n;
     a.k = k;
@@ -434,33 +431,28 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     a.exact = p->exact ? 1 : 0;
     a.tile_rows = tile_rows;
     a.max_tiles_per_label = mtpl;
-    a.max_tiles = (int32_t)std::min<int64_t>(max_tiles, INT32_MAX);
+    a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     a.hash_slots = hs;
     a.gtab_slots = (int64_t)gslots;
+    pl.graph_ctas = graph_max_ctas(a);
+    if (pl.graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
+    const size_t nwarp = (size_t)pl.graph_ctas * kWarpsPerGraphCta;
 
-    const int graph_ctas = graph_max_ctas(a);
-    if (graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
-    const size_t nwarp = (size_t)graph_ctas * kWarpsPerGraphCta;
-    a.n_warp_slots = (int32_t)nwarp;
-
-    // -- scratch
-    const int raw_bytes = D.dim * elem_size(D.dtype);
     bool fresh = false;
-    if (!q_dev) VF_CUDA(sc->raw.ensure((size_t)n * raw_bytes));
-    VF_CUDA(sc->Qp.ensure((size_t)n * D.row_bytes));
-    if (!off_dev) VF_CUDA(sc->qoff.ensure((size_t)(n + 1) * 8));
+    VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
+    VF_CUDA(sc->qoff.ensure((size_t)(n + 1) * 8));
     VF_CUDA(sc->qlab.ensure((size_t)slots * 4));
-    VF_CUDA(sc->qinfo.ensure((size_t)n * sizeof(QueryInfo)));
+    VF_CUDA(sc->qinfo.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(QueryInfo)));
     VF_CUDA(sc->items.ensure((size_t)slots * sizeof(Item)));
     VF_CUDA(sc->item_ctr.ensure((size_t)slots * 12));
     VF_CUDA(sc->graph_list.ensure((size_t)slots * 4));
     VF_CUDA(sc->scan_slots.ensure((size_t)slots * 4));
     VF_CUDA(sc->scan_q.ensure((size_t)slots * sizeof(ScanQuery)));
     VF_CUDA(sc->segs.ensure((size_t)slots * sizeof(Segment)));
-    VF_CUDA(sc->tiles.ensure((size_t)max_tiles * sizeof(Tile)));
+    VF_CUDA(sc->tiles.ensure((size_t)pl.max_tiles * sizeof(Tile)));
     VF_CUDA(sc->item_seg.ensure((size_t)slots * 4));
     VF_CUDA(sc->item_res.ensure((size_t)slots * k * 8));
-    if (multi) VF_CUDA(sc->partials.ensure((size_t)slots * mtpl * k * 8));
+    if (pl.multi) VF_CUDA(sc->partials.ensure((size_t)slots * mtpl * k * 8));
     VF_CUDA(sc->ctr.ensure(sizeof(Counters)));
     const size_t nls = (size_t)std::max(D.n_bslots, 1);
     VF_CUDA(sc->ls_count.ensure(nls * 4, &fresh));
@@ -475,32 +467,14 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
         sc->gtab_slots = gs;
         sc->gtab_warps = gw;
     }
-    // the kernels index the tables with the allocated geometry
-    a.gtab_slots = (int64_t)sc->gtab_slots;
+    a.gtab_slots = (int64_t)sc->gtab_slots;   // the kernels index the tables with the allocated geometry
     a.n_warp_slots = (int32_t)sc->gtab_warps;
-    if (!out_dev) {
-        VF_CUDA(sc->out_ids.ensure((size_t)n * k * 4));
-        VF_CUDA(sc->out_dists.ensure((size_t)n * k * 4));
-    }
     if (!sc->ev_ok) {
         for (auto &e : sc->ev) VF_CUDA(cudaEventCreate(&e));
         sc->ev_ok = true;
     }
-    const bool prof = ix->profiling;
-    if (prof) VF_CUDA(cudaEventRecord(sc->ev[0], s));
-
-    // -- inputs to the device
-    if (!q_dev) VF_CUDA(cudaMemcpyAsync(sc->raw.p, queries, (size_t)n * raw_bytes, cudaMemcpyHostToDevice, s));
-    if (!off_dev) VF_CUDA(cudaMemcpyAsync(sc->qoff.p, qoff, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
-    if (n_slots > 0)
-        VF_CUDA(cudaMemcpyAsync(sc->qlab.p, qlab, (size_t)n_slots * 4,
-                                lab_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    VF_CUDA(cudaMemsetAsync(sc->ctr.p, 0, sizeof(Counters), s));
-    if (prof) VF_CUDA(cudaEventRecord(sc->ev[1], s));
-
-    a.Qraw = q_dev ? reinterpret_cast<const uint8_t *>(queries) : sc->raw.as<uint8_t>();
     a.Qp = sc->Qp.as<uint8_t>();
-    a.q_off = off_dev ? qoff : sc->qoff.as<int64_t>();
+    a.q_off = sc->qoff.as<int64_t>();
     a.qlab = sc->qlab.as<int32_t>();
     a.qinfo = sc->qinfo.as<QueryInfo>();
     a.items = sc->items.as<Item>();
@@ -515,24 +489,159 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     a.tiles = sc->tiles.as<Tile>();
     a.item_seg = sc->item_seg.as<int32_t>();
     a.item_res = sc->item_res.as<unsigned long long>();
-    a.partials = multi ? sc->partials.as<unsigned long long>() : nullptr;
+    a.partials = pl.multi ? sc->partials.as<unsigned long long>() : nullptr;
     a.ctr = sc->ctr.as<Counters>();
+    a.gtab = sc->gtab.as<unsigned long long>();
+    return VF_OK;
+}
+
+vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
+                    int rec_bytes, int *launches) {
+    SearchArgs &a = pl.a;
+    const bool prof = ix->profiling;
+    VF_CUDA(cudaMemsetAsync(sc->ctr.p, 0, sizeof(Counters), s));
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[1], s));
+    int nl = 0;
+    if (recv) nl += launch_unpack_items(a, s, recv, n_recv, rec_bytes);
+    else nl += launch_prepare(a, s);
+    nl += launch_bucket(a, s, pl.n_slots, pl.qg);
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
+    const int sl = launch_scan(a, s, (int)std::min<int64_t>(pl.max_tiles, INT32_MAX));
+    if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
+    nl += sl;
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));
+    const int gl = launch_graph(a, s, (int)std::min<int64_t>(pl.n_slots, INT32_MAX), pl.graph_ctas);
+    if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
+    nl += gl;
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));
+    VF_CUDA(cudaGetLastError());
+    *launches += nl;
+    return VF_OK;
+}
+
+static vf_status check_params(vf_index *ix, const vf_search_params *p) {
+    if (!p) return fail(VF_ERR_INVALID_ARG, "params is NULL");
+    if (p->k < 1 || p->k > kMaxK) return fail(VF_ERR_INVALID_ARG, "k must be in [1, 256]");
+    if (p->itopk < p->k || p->itopk > kMaxItopk) return fail(VF_ERR_INVALID_ARG, "itopk must be in [k, 1024]");
+    const int w = p->search_width < 1 ? 1 : p->search_width;
+    if (w * ix->dev.R > 64) return fail(VF_ERR_INVALID_ARG, "search_width * R must be <= 64");
+    if (p->op < 0 || p->op > 2) return fail(VF_ERR_INVALID_ARG, "op must be VF_SINGLE, VF_OR or VF_AND");
+    if (p->recall_mode < 0 || p->recall_mode > 1) return fail(VF_ERR_INVALID_ARG, "bad recall_mode");
+    return VF_OK;
+}
+
+}  // namespace vf
+
+extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, const int64_t *qoff,
+                               const int32_t *qlab, const vf_search_params *p, int32_t *out_ids,
+                               float *out_dists, void *cuda_stream) {
+    if (!ix) return fail(VF_ERR_INVALID_ARG, "index is NULL");
+    vf_status st = check_params(ix, p);
+    if (st != VF_OK) return st;
+    if (n < 0) return fail(VF_ERR_INVALID_ARG, "n_queries < 0");
+    if (n > 0 && (!queries || !qoff || !out_ids || !out_dists))
+        return fail(VF_ERR_INVALID_ARG, "NULL queries / offsets / outputs");
+    VF_CUDA(cudaSetDevice(ix->device));
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const int64_t n_max_labels = ix->world > 1 ? kRecLabels : kMaxQueryLabels;
+
+    const bool off_dev = is_device_ptr(qoff);
+    const bool lab_dev = is_device_ptr(qlab);
+    if (n > 0 && !off_dev) {
+        if (qoff[0] != 0) return fail(VF_ERR_INVALID_ARG, "qlabel_offsets[0] must be 0");
+        for (int64_t i = 0; i < n; i++) {
+            const int64_t c = qoff[i + 1] - qoff[i];
+            if (c < 0 || c > n_max_labels)
+                return fail(VF_ERR_INVALID_ARG, "query " + std::to_string(i) + " has a bad label count (max " +
+                                                    std::to_string(n_max_labels) + ")");
+            if (p->op == VF_SINGLE && c > 1 && !lab_dev) {
+                for (int64_t e = qoff[i] + 1; e < qoff[i + 1]; e++)
+                    if (qlab[e] != qlab[qoff[i]])
+                        return fail(VF_ERR_INVALID_ARG, "VF_SINGLE query " + std::to_string(i) + " has more than one label");
+            }
+        }
+    }
+    // -- label-sharded index: virtual shards on this device (loopback) or one rank of an NCCL group
+    if (ix->world > 1) {
+        std::vector<vf_index *> shards;
+        std::vector<const void *> qs;
+        std::vector<int64_t> nq;
+        std::vector<const int64_t *> qo;
+        std::vector<const int32_t *> ql;
+        std::vector<int32_t *> oi;
+        std::vector<float *> od;
+        if (!ix->vshards.empty()) {
+            // the caller's batch is split into contiguous chunks, one per virtual origin rank
+            if (n > 0 && (off_dev || lab_dev || is_device_ptr(queries) || is_device_ptr(out_ids)))
+                return fail(VF_ERR_INVALID_ARG, "virtual shards take host query / result buffers");
+            const int W = (int)ix->vshards.size();
+            const size_t qbytes = (size_t)ix->dev.dim * elem_size(ix->dev.dtype);
+            for (int r = 0; r < W; r++) {
+                const int64_t lo = n * r / W, hi = n * (r + 1) / W;
+                shards.push_back(ix->vshards[r]);
+                qs.push_back(static_cast<const uint8_t *>(queries) + lo * qbytes);
+                nq.push_back(hi - lo);
+                qo.push_back(qoff + lo);
+                ql.push_back(qlab);
+                oi.push_back(out_ids + lo * p->k);
+                od.push_back(out_dists + lo * p->k);
+            }
+        } else {
+            shards.push_back(ix);
+            qs.push_back(queries);
+            nq.push_back(n);
+            qo.push_back(qoff);
+            ql.push_back(qlab);
+            oi.push_back(out_ids);
+            od.push_back(out_dists);
+        }
+        return sharded_search(shards, qs, nq, qo, ql, p, oi, od, ix->transport, s);
+    }
+    if (n == 0) return VF_OK;
+
+    Scratch *sc = get_scratch(ix, s, 0);
+    const DevIndex &D = ix->dev;
+    const int k = p->k;
+    const bool q_dev = is_device_ptr(queries);
+    const bool out_dev = is_device_ptr(out_ids);
+    if (out_dev != is_device_ptr(out_dists))
+        return fail(VF_ERR_INVALID_ARG, "out_ids and out_dists must both be host or both be device");
+    int64_t n_slots = 0;
+    if (!off_dev) {
+        n_slots = qoff[n];
+    } else {
+        VF_CUDA(cudaMemcpyAsync(&n_slots, qoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        VF_CUDA(cudaStreamSynchronize(s));
+    }
+    if (n_slots > 0 && !qlab) return fail(VF_ERR_INVALID_ARG, "qlabels is NULL");
+    if (n_slots >= (1ll << 31)) return fail(VF_ERR_INVALID_ARG, "too many query labels");
+
+    Plan pl;
+    st = plan_search(ix, sc, n, n_slots, p, s, &pl);
+    if (st != VF_OK) return st;
+    SearchArgs &a = pl.a;
+    const int raw_bytes = D.dim * elem_size(D.dtype);
+    if (!q_dev) VF_CUDA(sc->raw.ensure((size_t)n * raw_bytes));
+    if (!out_dev) {
+        VF_CUDA(sc->out_ids.ensure((size_t)n * k * 4));
+        VF_CUDA(sc->out_dists.ensure((size_t)n * k * 4));
+    }
+    const bool prof = ix->profiling;
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[0], s));
+    // -- inputs to the device
+    if (!q_dev) VF_CUDA(cudaMemcpyAsync(sc->raw.p, queries, (size_t)n * raw_bytes, cudaMemcpyHostToDevice, s));
+    if (off_dev) a.q_off = qoff;
+    else VF_CUDA(cudaMemcpyAsync(sc->qoff.p, qoff, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+    if (n_slots > 0)
+        VF_CUDA(cudaMemcpyAsync(sc->qlab.p, qlab, (size_t)n_slots * 4,
+                                lab_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    a.Qraw = q_dev ? reinterpret_cast<const uint8_t *>(queries) : sc->raw.as<uint8_t>();
     a.out_ids = out_dev ? out_ids : sc->out_ids.as<int32_t>();
     a.out_dists = out_dev ? out_dists : sc->out_dists.as<float>();
-    a.gtab = sc->gtab.as<unsigned long long>();
 
     int launches = 0;
-    launches += launch_prepare(a, s);
-    launches += launch_bucket(a, s, n_slots, qg);
-    if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
-    const int sl = launch_scan(a, s, (int)std::min<int64_t>(max_tiles, INT32_MAX));
-    if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
-    launches += sl;
-    if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));
-    const int gl = launch_graph(a, s, (int)std::min<int64_t>(n_slots, INT32_MAX), graph_ctas);
-    if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
-    launches += gl;
-    if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));
+    st = run_local(ix, sc, pl, s, nullptr, 0, 0, &launches);
+    if (st != VF_OK) return st;
     const bool need_merge = p->op == VF_OR || (p->op == VF_AND && p->recall_mode == VF_RECALL_PARALLEL);
     if (need_merge) launches += launch_merge(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[5], s));
@@ -553,9 +662,10 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
 
 extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_search_stats *st) {
     if (!ix || !st) return fail(VF_ERR_INVALID_ARG, "NULL argument");
+    if (!ix->vshards.empty()) ix = ix->vshards[0];
     VF_CUDA(cudaSetDevice(ix->device));
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    Scratch *sc = get_scratch(ix, s);
+    Scratch *sc = get_scratch(ix, s, 0);
     std::memset(st, 0, sizeof(*st));
     if (!sc->has_last) return fail(VF_ERR_INVALID_ARG, "no search on this stream yet");
     VF_CUDA(cudaStreamSynchronize(s));
@@ -593,9 +703,10 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
 extern "C" vf_status vf_get_last_items(vf_index *ix, void *cuda_stream, int64_t max_items, int32_t *rec,
                                        int64_t *n_items) {
     if (!ix || !n_items) return fail(VF_ERR_INVALID_ARG, "NULL argument");
+    if (!ix->vshards.empty()) return fail(VF_ERR_INVALID_ARG, "per-item records are kept per shard");
     VF_CUDA(cudaSetDevice(ix->device));
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    Scratch *sc = get_scratch(ix, s);
+    Scratch *sc = get_scratch(ix, s, 0);
     if (!sc->has_last) return fail(VF_ERR_INVALID_ARG, "no search on this stream yet");
     VF_CUDA(cudaStreamSynchronize(s));
     const int64_t ns = sc->last_slots;
@@ -614,7 +725,7 @@ extern "C" vf_status vf_get_last_items(vf_index *ix, void *cuda_stream, int64_t 
             r[0] = items[i].qid;
             r[1] = items[i].label;
             r[2] = (int32_t)path;
-            const bool g = path == PATH_GRAPH;
+            const bool g = path == PATH_GRAPH && !(items[i].meta & META_REMOTE);
             r[3] = g ? ctr[i * 3 + 0] : 0;
             r[4] = g ? ctr[i * 3 + 1] : 0;
             r[5] = g ? ctr[i * 3 + 2] : 0;

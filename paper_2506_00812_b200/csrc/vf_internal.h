@@ -41,6 +41,8 @@ struct DevIndex {
     const int32_t *M_ls;   // [ls_rows] (M_LS)
     const int64_t *pt_off; // [n_points+1] predicate table offsets
     const int32_t *pt_lab; // sorted labels per point
+    const int32_t *owner;  // [n_labels] owning rank of each label (label sharding, §8(e)); NULL = all local
+    int32_t rank, world;
 };
 
 // Work item (a1): one (query, label) search (Alg. 2 L418 / L428 "(q, l)").
@@ -50,7 +52,20 @@ struct Item {
     int32_t rank;      // scan items: position within the label bucket
     uint32_t meta;     // bits 0-1 path, bit 2 has_pred, bit 3 direct, bit 4 multi_tile
 };
-constexpr uint32_t META_PRED = 4u, META_DIRECT = 8u, META_MULTI = 16u;
+constexpr uint32_t META_PRED = 4u, META_DIRECT = 8u, META_MULTI = 16u, META_REMOTE = 32u;
+constexpr int kMaxWorld = 16;        // ranks of a label-sharded index
+constexpr int kRecLabels = 16;       // query labels carried by an exchanged item record
+
+// An item shipped to the rank owning its label (label sharding): header + the padded query row.
+struct ItemRecord {
+    int32_t origin_slot;  // the item's slot on the origin rank (results come back in send order)
+    int32_t label;        // the item's label, owned by the receiver
+    int32_t nl;           // sorted, deduplicated query labels that follow (the AND predicate)
+    uint32_t pred;        // META_PRED if the item carries an AND predicate
+    uint32_t qh;          // the query's content hash (entry sampler, reading #34)
+    int32_t pad[3];
+    int32_t labels[kRecLabels];
+};
 
 struct QueryInfo {
     int32_t nl;        // deduplicated label count
@@ -106,6 +121,8 @@ struct Counters {
     int32_t pad;
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
+    int32_t remote[kMaxWorld];      // items of this batch owned by each rank (sharded index)
+    int32_t remote_pos[kMaxWorld];  // packing cursors
 };
 
 struct SearchArgs {
@@ -150,6 +167,12 @@ int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg);
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // a2
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
+// label sharding (§8(e)): pack remote items, unpack received ones, scatter returned results
+int launch_pack_remote(const SearchArgs &a, cudaStream_t s, int64_t n_slots, uint8_t *send, const int64_t *dst_off,
+                       int32_t *sent_slots, int rec_bytes);
+int launch_unpack_items(const SearchArgs &a, cudaStream_t s, const uint8_t *recv, int64_t n, int rec_bytes);
+int launch_scatter_results(const SearchArgs &a, cudaStream_t s, const int32_t *ids, const float *dists,
+                           const int32_t *sent_slots, int64_t n);
 int launch_finish_keys(const SearchArgs &a, cudaStream_t s);
 int graph_smem_bytes(const SearchArgs &a);
 int graph_max_ctas(const SearchArgs &a);

@@ -253,3 +253,25 @@ def test_byte_accounting(vf, tiny):
     assert info["bytes_ls_vectors"] == ls_pad * rb
     # redundancy bypassing saves exactly the HS vector copies
     assert info["bytes_total"] < info["bytes_total"] + hs * rb
+
+
+@pytest.mark.parametrize("shards", [2, 3, 4])
+@pytest.mark.parametrize("op,mode", [("single", "greedy"), ("and", "greedy"), ("and", "parallel"), ("or", "greedy")])
+def test_virtual_shards_bit_identical(vf, tiny, shards, op, mode):
+    """Label sharding (§8(e)) on one device: route -> ship items to owners -> execute -> return ->
+    merge gives exactly the unsharded results (items are independent, the sampler keys on content)."""
+    from workload import gen
+    w, go, gi = tiny
+    qoff, qlab = (w.q_off, w.q_lab) if op == "single" else \
+        gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=len(w.Q), mode="and2" if op == "and" else "or2")
+    one = vf.Index(w.X, w.post_off, w.post_ids, w.cfg.threshold_T, w.cfg.degree_R, go, gi)
+    many = vf.Index(w.X, w.post_off, w.post_ids, w.cfg.threshold_T, w.cfg.degree_R, go, gi, virtual_shards=shards)
+    for itopk in (16, 64):
+        a, ad = one.search(w.Q, qoff, qlab, k=10, itopk=itopk, op=op, recall_mode=mode)
+        b, bd = many.search(w.Q, qoff, qlab, k=10, itopk=itopk, op=op, recall_mode=mode)
+        assert (a == b).all() and (ad == bd).all()
+    a, ad = one.search(w.Q, qoff, qlab, k=10, op=op, recall_mode=mode, exact=True)
+    b, bd = many.search(w.Q, qoff, qlab, k=10, op=op, recall_mode=mode, exact=True)
+    assert (a == b).all() and (ad == bd).all()
+    info = many.info()
+    assert info["owned_labels"] == one.info()["owned_labels"]      # every label owned exactly once
