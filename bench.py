@@ -11,8 +11,10 @@ single-label queries, k = 10) unless --config says otherwise; see DESIGN.md §3 
 Ground truth comes from vf_search in exact mode (T = infinity; parity-tested bit-exact against the
 CPU oracle in tests/). The operating point for a recall target is the smallest itopk of the grid
 whose mean recall@10 reaches it. L2 is flushed (256 MiB write) before every timed step, outside
-the step's CUDA events. Under torchrun (N > 1) every rank holds the index and runs its own batch
-(weak scaling); rank 0 prints the line with value = all ranks' queries / max-over-ranks time.
+the step's CUDA events. Under torchrun (N > 1) the index is label-sharded across the ranks (LPT
+over |C_l|; X and the predicate table replicated; items exchanged with NCCL inside vf_search) and
+every rank brings its own batch (weak scaling); rank 0 prints the line with value = all ranks'
+queries / max-over-ranks time.
 The CPU oracle is used ONLY for the cpu_baseline leg and for --impl reference.
 """
 from __future__ import annotations
@@ -40,10 +42,10 @@ def log(*a):
 
 
 # ----------------------------------------------------------------------------- workload
-def make_inputs(config: str, device):
+def make_inputs(config: str, device, query_stream: int = 0):
     from workload import gen, graphs
     t0 = time.time()
-    w = gen.make_workload(config)
+    w = gen.make_workload(config, query_stream=query_stream)
     c = w.cfg
     log(f"workload {config}: N={c.n_points} D={c.dim} L={c.n_labels} Q={c.n_queries} "
         f"dtype={c.dtype} ({time.time() - t0:.1f}s)")
@@ -196,10 +198,18 @@ def main():
         if world > 1:
             dist.barrier()
 
-    w, go, gi = make_inputs(args.config, dev)
+    w, go, gi = make_inputs(args.config, dev, query_stream=rank)
     c = w.cfg
     t0 = time.time()
-    ix = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi, device=local)
+    if world > 1:
+        # label sharding (§8(e)): one rank per GPU, labels partitioned by LPT over |C_l|, items
+        # exchanged with NCCL over NVLink inside vf_search
+        uid = torch.tensor(list(vf.nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
+        dist.broadcast(uid, 0)
+        ix = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi, device=local,
+                      world_size=world, rank=rank, nccl_unique_id=bytes(uid.cpu().tolist()))
+    else:
+        ix = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi, device=local)
     info = ix.info()
     log(f"vf_build_index: {info['bytes_total'] / 2**30:.2f} GiB on device ({time.time() - t0:.1f}s)")
     op = "and" if c.query_mode in ("and2", "mix_and") else ("or" if c.query_mode == "or2" else "single")
@@ -254,6 +264,10 @@ def main():
             torch.cuda.synchronize()
             r_strict, r_tie = recall_vs(ids.cpu().numpy(), dd.cpu().numpy(), gt, gd, k)
             qms = quick_ms(itopk, w_)
+            if world > 1:   # every rank takes the same decisions (the searches are collective)
+                t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
+                dist.all_reduce(t)
+                r_strict, r_tie, qms = (float(x) / world for x in t.tolist())
             sweep.append((itopk, r_strict, r_tie, w_, qms))
             log(f"w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
                 f"{n / qms / 1e3:.2f} MQPS")
@@ -381,7 +395,8 @@ def main():
                    "R": R, "itopk": itopk, "search_width": opnt[3], "recall_target": main_tgt,
                    "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
                    "flush": "256 MiB L2 flush before every timed step (outside the step events)",
-                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+                   "parallelism": f"label-shard{world}" if world > 1 else "single",
+                   "queries": "per rank (weak scaling)" if world > 1 else "batch"},
         "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "qps": n * world * K / (r[4] / 1000.0),
                                    "ms_per_step": r[4] / K, "recall_strict": r[1][1],
                                    "recall_tie_aware": r[1][2]} for t, r in results.items()},

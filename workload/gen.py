@@ -217,7 +217,9 @@ class Workload:
 
 
 def make_workload(name: str, n_queries: int | None = None, query_mode: str | None = None,
-                  **overrides) -> Workload:
+                  query_stream: int = 0, **overrides) -> Workload:
+    """query_stream > 0 draws an independent query batch (seeds + 7 * query_stream), e.g. one per
+    rank of a weak-scaling run; the index data do not change."""
     cfg = config(name, **overrides)
     if n_queries is not None:
         cfg.n_queries = n_queries
@@ -225,6 +227,6 @@ def make_workload(name: str, n_queries: int | None = None, query_mode: str | Non
         cfg.query_mode = query_mode
     X = gen_vectors(cfg)
     off, ids = gen_postings(cfg)
-    Q = gen_query_vectors(cfg)
-    qoff, qlab = gen_query_labels(cfg, off, ids)
+    Q = gen_query_vectors(cfg, seed=SEED_QVECTORS + 7 * query_stream)
+    qoff, qlab = gen_query_labels(cfg, off, ids, seed=SEED_QLABELS + 7 * query_stream)
     return Workload(cfg, X, off, ids, Q, qoff, qlab)
