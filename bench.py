@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--targets", default="0.90,0.99")
     ap.add_argument("--widths", default="1,2,4", help="search widths w swept for the operating points")
+    ap.add_argument("--gt-sample", type=int, default=-1,
+                    help="queries whose exact ground truth is computed for recall (-1: all; yfcc: 5000)")
     ap.add_argument("--cpu-sample", type=int, default=2000)
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--ref-itopk", type=int, default=64)
@@ -178,6 +180,8 @@ def main():
     ap.add_argument("--dump-stats", default=None)
     args = ap.parse_args()
 
+    if args.gt_sample < 0:
+        args.gt_sample = 5000 if args.config == "yfcc" else 0
     if args.impl == "reference":
         run_reference(args, args.config)
         return
@@ -224,18 +228,20 @@ def main():
 
     # -- ground truth: exact mode (T = inf), in query chunks
     t0 = time.time()
-    gt = np.empty((n, k), np.int32)
-    gd = np.empty((n, k), np.float32)
+    # recall sample: the first m queries of the batch (all of them unless --gt-sample says fewer)
+    m_gt = n if args.gt_sample <= 0 else min(n, args.gt_sample)
+    gt = np.empty((m_gt, k), np.int32)
+    gd = np.empty((m_gt, k), np.float32)
     step = 2000
-    for s in range(0, n, step):
-        e = min(n, s + step)
+    for s in range(0, m_gt, step):
+        e = min(m_gt, s + step)
         Qs, qos, qls = Q[s:e], qo[s:e + 1] - qo[s], ql[int(w.q_off[s]):int(w.q_off[e])]
         ti = torch.empty((e - s, k), dtype=torch.int32, device=dev)
         td = torch.empty((e - s, k), dtype=torch.float32, device=dev)
         ix.search_into(Qs, qos.contiguous(), qls.contiguous(), ti, td, k=k, op=op, exact=True, stream=stream)
         torch.cuda.synchronize()
         gt[s:e], gd[s:e] = ti.cpu().numpy(), td.cpu().numpy()
-    log(f"ground truth (exact mode): {time.time() - t0:.1f}s")
+    log(f"ground truth (exact mode) for {m_gt} queries: {time.time() - t0:.1f}s")
 
     # -- (search_width, itopk) sweep -> operating points: for each recall target the fastest
     #    configuration whose mean tie-aware recall@10 reaches it (the paper traces QPS-recall curves
@@ -262,7 +268,7 @@ def main():
                 continue
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
             torch.cuda.synchronize()
-            r_strict, r_tie = recall_vs(ids.cpu().numpy(), dd.cpu().numpy(), gt, gd, k)
+            r_strict, r_tie = recall_vs(ids[:m_gt].cpu().numpy(), dd[:m_gt].cpu().numpy(), gt, gd, k)
             qms = quick_ms(itopk, w_)
             if world > 1:   # every rank takes the same decisions (the searches are collective)
                 t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
@@ -394,6 +400,7 @@ def main():
                    "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
                    "R": R, "itopk": itopk, "search_width": opnt[3], "recall_target": main_tgt,
                    "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
+                   "recall_sample": f"first {m_gt} queries (exact-mode ground truth)",
                    "flush": "256 MiB L2 flush before every timed step (outside the step events)",
                    "parallelism": f"label-shard{world}" if world > 1 else "single",
                    "queries": "per rank (weak scaling)" if world > 1 else "batch"},

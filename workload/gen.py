@@ -11,13 +11,14 @@ Shapes follow the paper's workloads (§5.1) and BASELINE.jso
                  labels of a base point that has at least two, so |AND set| >= 1.
 
 Everything is drawn from numpy PCG64 streams with fixed seeds (vectors 1001, labels 1002, query
-vectors 1003, query labels 1004) in fixed-size chunks, so a (config, variant) pair always
-yields bit-identical arrays. No distance, routing, search or merge arithmetic lives here.
+vectors 1003, query labels 1004); vectors in 2^18-row chunks, chunk i from SeedSequence(seed)
+spawn i (float32 draws), so a (config, variant) pair always yields bit-identical arrays. No distance, routing, search or merge arithmetic lives here.
 """
 from __future__ import annotations
 
 import dataclasses
 import math
+import os
 
 import numpy as np
 
@@ -77,49 +78,58 @@ def config(name: str, **overrides) -> Config:
 
 
 # ----------------------------------------------------------------------------- vectors
-def _clr_float(rng: np.random.Generator, n: int, dim: int, m: VectorModel,
-               A: np.ndarray, centers: np.ndarray) -> np.ndarray:
-    """n points of the CLR model before rounding: 128 + A z + sigma_n * eps."""
-    out = np.empty((n, dim), dtype=np.float64)
-    for s in range(0, n, _CHUNK):
-        e = min(n, s + _CHUNK)
-        c = rng.integers(0, m.clusters, size=e - s)
-        z = centers[c] + rng.standard_normal((e - s, m.rank))
-        eps = rng.standard_normal((e - s, dim))
-        out[s:e] = 128.0 + z @ A.T + m.sigma_n * eps
-    return out
+def _clr_chunk(seq: np.random.SeedSequence, n: int, dim: int, m: VectorModel, A: np.ndarray,
+               centers: np.ndarray, dtype: str) -> np.ndarray:
+    """n points of the CLR model, 128 + A z + sigma_n * eps, finished to the storage dtype."""
+    rng = np.random.Generator(np.random.PCG64(seq))
+    c = rng.integers(0, m.clusters, size=n)
+    z = centers[c] + rng.standard_normal((n, m.rank), dtype=np.float32)
+    x = z @ A.T
+    x += rng.standard_normal((n, dim), dtype=np.float32) * np.float32(m.sigma_n)
+    x += np.float32(128.0)
+    if dtype == "f32float":
+        return x / np.float32(255.0)
+    np.rint(x, out=x)
+    np.clip(x, 0, 255, out=x)
+    if dtype == "u8":
+        return x.astype(np.uint8)
+    if dtype == "f32int":
+        return x
+    raise ValueError(dtype)
 
 
 def _model_params(dim: int, m: VectorModel):
     rng = np.random.Generator(np.random.PCG64(SEED_VECTORS + 7919))
     scale = m.sigma_x / math.sqrt(m.rank * (1.0 + m.center_scale ** 2))
-    A = rng.standard_normal((dim, m.rank)) * scale
-    centers = rng.standard_normal((m.clusters, m.rank)) * m.center_scale
+    A = (rng.standard_normal((dim, m.rank)) * scale).astype(np.float32)
+    centers = (rng.standard_normal((m.clusters, m.rank)) * m.center_scale).astype(np.float32)
     return A, centers
 
 
-def _finish(xf: np.ndarray, dtype: str) -> np.ndarray:
-    if dtype == "f32float":
-        return (xf / 255.0).astype(np.float32)
-    xi = np.clip(np.rint(xf), 0, 255)
-    if dtype == "u8":
-        return xi.astype(np.uint8)
-    if dtype == "f32int":
-        return xi.astype(np.float32)
-    raise ValueError(dtype)
+def _clr(cfg: Config, n: int, seed: int) -> np.ndarray:
+    """Chunk i of 2^18 rows draws from its own stream SeedSequence(seed).spawn()[i], so the result
+    does not depend on how many threads generate it."""
+    from concurrent.futures import ThreadPoolExecutor
+    A, centers = _model_params(cfg.dim, cfg.model)
+    n_chunks = (n + _CHUNK - 1) // _CHUNK
+    seqs = np.random.SeedSequence(seed).spawn(max(n_chunks, 1))
+    out = np.empty((n, cfg.dim), dtype=np.uint8 if cfg.dtype == "u8" else np.float32)
+
+    def work(i):
+        s0, e0 = i * _CHUNK, min(n, (i + 1) * _CHUNK)
+        out[s0:e0] = _clr_chunk(seqs[i], e0 - s0, cfg.dim, cfg.model, A, centers, cfg.dtype)
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(work, range(n_chunks)))
+    return out
 
 
 def gen_vectors(cfg: Config, seed: int = SEED_VECTORS) -> np.ndarray:
-    A, centers = _model_params(cfg.dim, cfg.model)
-    rng = np.random.Generator(np.random.PCG64(seed))
-    return _finish(_clr_float(rng, cfg.n_points, cfg.dim, cfg.model, A, centers), cfg.dtype)
+    return _clr(cfg, cfg.n_points, seed)
 
 
 def gen_query_vectors(cfg: Config, n: int | None = None, seed: int = SEED_QVECTORS) -> np.ndarray:
-    A, centers = _model_params(cfg.dim, cfg.model)
-    rng = np.random.Generator(np.random.PCG64(seed))
-    return _finish(_clr_float(rng, cfg.n_queries if n is None else n, cfg.dim, cfg.model,
-                              A, centers), cfg.dtype)
+    return _clr(cfg, cfg.n_queries if n is None else n, seed)
 
 
 # ----------------------------------------------------------------------------- labels

@@ -39,10 +39,20 @@ def _knn_numpy(Xl: np.ndarray, K: int) -> np.ndarray:
     return out
 
 
+def _gpu_rows(Xl: np.ndarray, device):
+    """Label rows on the GPU. Integer-valued data in [0, 255] use bf16 operands (exact values; the
+    products accumulate exactly in fp32 on the tensor cores); other data stay fp32."""
+    import torch
+    X = torch.from_numpy(np.ascontiguousarray(Xl)).to(device).float()
+    integral = Xl.dtype == np.uint8 or bool(torch.all(X == torch.round(X)) and X.min() >= 0 and X.max() <= 255)
+    return X, (X.to(torch.bfloat16) if integral else X)
+
+
 def _knn_torch(Xl: np.ndarray, K: int, device) -> np.ndarray:
+    """Exact K nearest neighbours of every row among the other rows (chunked GEMM + top-k)."""
     import torch
     S = Xl.shape[0]
-    X = torch.from_numpy(np.ascontiguousarray(Xl, dtype=np.float32)).to(device)
+    X, Xm = _gpu_rows(Xl, device)
     nrm = (X * X).sum(1)
     kk = min(K, S - 1)
     out = np.full((S, K), -1, np.int64)
@@ -52,11 +62,58 @@ def _knn_torch(Xl: np.ndarray, K: int, device) -> np.ndarray:
     res = []
     for s in range(0, S, step):
         e = min(S, s + step)
-        d = nrm[s:e, None] + nrm[None, :] - 2.0 * (X[s:e] @ X.T)
+        d = nrm[s:e, None] + nrm[None, :] - 2.0 * (Xm[s:e] @ Xm.T).float()
         d[torch.arange(e - s, device=device), torch.arange(s, e, device=device)] = float("inf")
         _, idx = torch.topk(d, kk, dim=1, largest=False, sorted=True)
         res.append(idx.cpu())
     out[:, :kk] = torch.cat(res).numpy()
+    return out
+
+
+def _knn_torch_ivf(Xl: np.ndarray, K: int, device, bucket=2048, probes=4, iters=4, seed=0) -> np.ndarray:
+    """Approximate K-NN for large labels: k-means into ~S/bucket cells (seeded, `iters` Lloyd
+    steps), then the rows of each cell are matched exactly against the points of the cell's
+    `probes` nearest cells (cell-level probing)."""
+    import torch
+    S = Xl.shape[0]
+    X, Xm = _gpu_rows(Xl, device)
+    nrm = (X * X).sum(1)
+    B = max(2, S // bucket)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    C = X[torch.randperm(S, generator=g)[:B].to(device)].clone()
+    step = 1 << 16
+    for _ in range(iters + 1):
+        cn = (C * C).sum(1)
+        assign = torch.empty(S, dtype=torch.int64, device=device)
+        for s0 in range(0, S, step):
+            e0 = min(S, s0 + step)
+            d = cn[None, :] - 2.0 * (X[s0:e0] @ C.T)
+            assign[s0:e0] = torch.argmin(d, dim=1)
+        cnt = torch.bincount(assign, minlength=B).float()
+        newc = torch.zeros_like(C).index_add_(0, assign, X)
+        keep = cnt > 0
+        C[keep] = newc[keep] / cnt[keep, None]
+    cn = (C * C).sum(1)
+    dc = cn[:, None] + cn[None, :] - 2.0 * (C @ C.T)
+    probe = torch.topk(dc, min(probes, B), dim=1, largest=False).indices.cpu().numpy()   # incl. itself
+    order = torch.argsort(assign).cpu().numpy()
+    starts = np.searchsorted(assign.cpu().numpy()[order], np.arange(B + 1))
+    members = [order[starts[b]:starts[b + 1]] for b in range(B)]
+    out = np.full((S, K), -1, np.int64)
+    for b in range(B):
+        rows = members[b]
+        if rows.size == 0:
+            continue
+        cand = np.concatenate([members[c] for c in probe[b]])
+        rt = torch.from_numpy(rows).to(device)
+        ct = torch.from_numpy(cand).to(device)
+        d = nrm[rt, None] + nrm[None, ct] - 2.0 * (Xm[rt] @ Xm[ct].T).float()
+        d[ct[None, :] == rt[:, None]] = float("inf")
+        kk = min(K, cand.size - 1)
+        if kk <= 0:
+            continue
+        _, idx = torch.topk(d, kk, dim=1, largest=False, sorted=True)
+        out[rows, :kk] = ct[idx].cpu().numpy()
     return out
 
 
@@ -96,12 +153,51 @@ def assemble_rows(knn: np.ndarray, R: int) -> np.ndarray:
     return rows
 
 
+EXACT_MAX = 500_000   # labels above this size get the approximate (IVF-probe) kNN lists
+
+
+def assemble_rows_torch(knn: np.ndarray, R: int, device) -> np.ndarray:
+    """assemble_rows on the GPU (same rule, same output) for large labels."""
+    import torch
+    S = knn.shape[0]
+    h = R // 2
+    kt = torch.from_numpy(knn).to(device)
+    fwd, rest = kt[:, :h], kt[:, h:R]
+    u = torch.arange(S, device=device).repeat_interleave(h)
+    rank = torch.arange(h, device=device).repeat(S)
+    v = fwd.reshape(-1)
+    ok = v >= 0
+    u, v, rank = u[ok], v[ok], rank[ok]
+    key = (v * h + rank) * S + u                       # lexsort by (v, rank, u)
+    order = torch.argsort(key)
+    u, v = u[order], v[order]
+    start = torch.searchsorted(v, torch.arange(S, device=device))
+    pos = torch.arange(v.numel(), device=device) - start[v]
+    keep = pos < h
+    rev = torch.full((S, h), -1, dtype=torch.int64, device=device)
+    rev[v[keep], pos[keep]] = u[keep]
+    cand = torch.cat([fwd, rev, rest], dim=1)
+    valid = cand >= 0
+    for c in range(1, cand.shape[1]):
+        valid[:, c] &= ~(cand[:, :c] == cand[:, c:c + 1]).any(dim=1)
+    rk = torch.cumsum(valid.to(torch.int64), dim=1) - 1
+    sel = valid & (rk < R)
+    rows = torch.full((S, R), -1, dtype=torch.int64, device=device)
+    ri, ci = torch.nonzero(sel, as_tuple=True)
+    rows[ri, rk[ri, ci]] = cand[ri, ci]
+    return rows.to(torch.int32).cpu().numpy()
+
+
 def build_label_graph(Xl: np.ndarray, R: int, device=None) -> np.ndarray:
     S = Xl.shape[0]
-    if device is not None and S > 4096:
+    if device is not None and S > EXACT_MAX:
+        knn = _knn_torch_ivf(Xl, R, device)
+    elif device is not None and S > 4096:
         knn = _knn_torch(Xl, R, device)
     else:
         knn = _knn_numpy(Xl, R)
+    if device is not None and S > 4096:
+        return assemble_rows_torch(knn, R, device)
     return assemble_rows(knn, R)
 
 
