@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--targets", default="0.90,0.99")
     ap.add_argument("--widths", default="1,2,4", help="search widths w swept for the operating points")
+    ap.add_argument("--and-scan", default=None,
+                    help="f3 selectivity-aware AND routing thresholds swept (0 = the paper's method)")
     ap.add_argument("--gt-sample", type=int, default=-1,
                     help="queries whose exact ground truth is computed for recall (-1: all; yfcc: 5000)")
     ap.add_argument("--cpu-sample", type=int, default=2000)
@@ -180,6 +182,8 @@ def main():
     ap.add_argument("--dump-stats", default=None)
     args = ap.parse_args()
 
+    if args.and_scan is None:
+        args.and_scan = "0,2000,50000" if args.config == "yfcc" else "0"
     if args.gt_sample < 0:
         args.gt_sample = 5000 if args.config == "yfcc" else 0
     if args.impl == "reference":
@@ -249,33 +253,36 @@ def main():
     targets = [float(x) for x in args.targets.split(",")]
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
 
-    def quick_ms(itopk, w_):
+    def quick_ms(itopk, w_, as_=0):
         ms = []
         for _ in range(3):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
+                           and_scan_threshold=as_, stream=stream)
             e1.record(stream)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
         return float(np.median(ms))
 
     sweep = []
-    for w_ in [int(x) for x in args.widths.split(",")]:
+    and_scans = [int(x) for x in args.and_scan.split(",")] if op == "and" else [0]
+    for as_, w_ in [(a_, b_) for a_ in and_scans for b_ in (int(x) for x in args.widths.split(","))]:
         for itopk in ITOPK_GRID:
             if itopk < k:
                 continue
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
+                           and_scan_threshold=as_, stream=stream)
             torch.cuda.synchronize()
             r_strict, r_tie = recall_vs(ids[:m_gt].cpu().numpy(), dd[:m_gt].cpu().numpy(), gt, gd, k)
-            qms = quick_ms(itopk, w_)
+            qms = quick_ms(itopk, w_, as_)
             if world > 1:   # every rank takes the same decisions (the searches are collective)
                 t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
                 dist.all_reduce(t)
                 r_strict, r_tie, qms = (float(x) / world for x in t.tolist())
-            sweep.append((itopk, r_strict, r_tie, w_, qms))
-            log(f"w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
+            sweep.append((itopk, r_strict, r_tie, w_, qms, as_))
+            log(f"and_scan={as_} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
                 f"{n / qms / 1e3:.2f} MQPS")
             if r_tie >= max(targets):
                 break
@@ -287,10 +294,11 @@ def main():
     ix.set_profiling(True)
     hbm_peak, peak_kind = measured_peaks()
 
-    def timed(itopk, w_):
+    def timed(itopk, w_, as_):
         """W warm-up + exactly K timed steps; per-step CUDA events around vf_search only."""
         for _ in range(args.warmup):
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
+                           and_scan_threshold=as_, stream=stream)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         stats = []
@@ -299,7 +307,8 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
+                           and_scan_threshold=as_, stream=stream)
             ev[i][1].record(stream)
             stats.append(ix.last_stats(stream))   # syncs; between steps, outside the events
         torch.cuda.synchronize()
@@ -312,8 +321,8 @@ def main():
         for tgt, opnt in ops.items():
             if opnt is None:
                 continue
-            itopk, w_ = opnt[0], opnt[3]
-            ms, stats = timed(itopk, w_)
+            itopk, w_, as_ = opnt[0], opnt[3], opnt[5]
+            ms, stats = timed(itopk, w_, as_)
             tot = float(np.sum(ms))
             if world > 1:
                 t = torch.tensor([tot], device=dev)
@@ -326,20 +335,22 @@ def main():
     main_tgt = targets[0]
     e2e = None
     if main_tgt in results:
-        itopk, w_ = results[main_tgt][0], results[main_tgt][1][3]
+        itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
         Qh = torch.from_numpy(w.Q).pin_memory()
         qoh = torch.from_numpy(w.q_off).pin_memory()
         qlh = torch.from_numpy(w.q_lab).pin_memory()
         oih = torch.empty((n, k), dtype=torch.int32).pin_memory()
         odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
         for _ in range(args.warmup):
-            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
+                           and_scan_threshold=as_, stream=stream)
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
-            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op, stream=stream)
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
+                           and_scan_threshold=as_, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         et = e0.elapsed_time(e1)
@@ -356,13 +367,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
         import oracle
-        itopk, w_ = results[main_tgt][0], results[main_tgt][1][3]
+        itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
         o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
         m = min(n, args.cpu_sample)
         threads = os.cpu_count() or 1
         t0 = time.perf_counter()
         o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], k=k, itopk=itopk, search_width=w_, op=op,
-                 nthreads=threads)
+                 nthreads=threads, and_scan_threshold=as_)
         el = time.perf_counter() - t0
         cpu = {"value": m / el, "unit": "queries/s", "cores": threads, "kind": "oracle",
                "sample": f"first {m} of the {n} queries, itopk={itopk}, w={w_}, {threads} threads, {el:.1f}s"}
@@ -398,16 +409,17 @@ def main():
         "config": {"workload": f"{args.config} (BASELINE.json configs[{ {'tiny': 0, 'sift': 1, 'yfcc': 2}[args.config]}])",
                    "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
                    "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
-                   "R": R, "itopk": itopk, "search_width": opnt[3], "recall_target": main_tgt,
+                   "R": R, "itopk": itopk, "search_width": opnt[3], "and_scan_threshold": opnt[5],
+                   "recall_target": main_tgt,
                    "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
                    "recall_sample": f"first {m_gt} queries (exact-mode ground truth)",
                    "flush": "256 MiB L2 flush before every timed step (outside the step events)",
                    "parallelism": f"label-shard{world}" if world > 1 else "single",
                    "queries": "per rank (weak scaling)" if world > 1 else "batch"},
-        "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "qps": n * world * K / (r[4] / 1000.0),
+        "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "and_scan_threshold": r[1][5], "qps": n * world * K / (r[4] / 1000.0),
                                    "ms_per_step": r[4] / K, "recall_strict": r[1][1],
                                    "recall_tie_aware": r[1][2]} for t, r in results.items()},
-        "sweep": [{"search_width": s[3], "itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2],
+        "sweep": [{"and_scan_threshold": s[5], "search_width": s[3], "itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2],
                    "ms": s[4]} for s in sweep],
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,

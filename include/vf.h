@@ -109,6 +109,13 @@ typedef struct {
     int32_t op;
     int32_t recall_mode;
     int32_t exact;
+    /* Selectivity-aware AND routing (BEYOND the paper, 0 = off = the paper's
+     * method). For a GREEDY AND item whose list l* is HS, the expected AND-set size under label
+     * independence, est = |C_l*| * prod_{o != l*} (|C_o| / n_points) (fp64, other labels in
+     * ascending id order, left to right), is computed; est < and_scan_threshold routes the item to
+     * the exact scan of C_l* with the predicate instead of the inline-filtered graph search, whose
+     * traversal collapses when few points pass the filter. */
+    int32_t and_scan_threshold;
 } vf_search_params;
 
 /* Build the index on the device (copies everything; see vf_build_desc). */

@@ -275,12 +275,16 @@ static void exact_one(const or_index *ix, const void *q, const int32_t *lq_in, i
  *                      reading #18); none if some label is empty/unknown
  *   AND parallel    -> one item per label, predicate L_q\{l}; none if some label empty
  * Item record: {qid, label, path, pred_start, pred_len}; predicate labels are written to pred_buf.
- * Returns the number of items, or -1 on an invalid query (SINGLE with > 1 label). */
+ * Returns the number of items, or -1 on an invalid query (SINGLE with > 1 label).
+ * and_scan_threshold > 0 enables the selectivity-aware AND routing of SURVEY §8(f) f3 (NOT in
+ * the paper; include/vf.h): a greedy item with HS l* goes to SCAN when the expected AND-set size
+ * est = |C_l*| * prod over the other labels (ascending) of |C_o| / N, evaluated left to right in
+ * fp64, is below the threshold. */
 typedef struct { int32_t qid, label, path; int64_t pred_start; int32_t pred_len; } item_t;
 
 static int64_t route_query(const or_index *ix, int32_t qid, const int32_t *lq_in, int nl, int op,
-                           int recall_mode, int exact, item_t *items, int32_t *pred_buf,
-                           int64_t *pred_pos)
+                           int recall_mode, int exact, int32_t and_scan_threshold, item_t *items,
+                           int32_t *pred_buf, int64_t *pred_pos)
 {
     int32_t lq[4096];
     if (nl > 4096) return -1;
@@ -306,6 +310,12 @@ static int64_t route_query(const or_index *ix, int32_t qid, const int32_t *lq_in
         for (int t = 1; t < nl; t++)
             if (label_size(ix, lq[t]) < label_size(ix, lq[best])) best = t;  /* ties -> lower id */
         items[0].qid = qid; items[0].label = lq[best]; items[0].path = PATH_OF(lq[best]);
+        if (and_scan_threshold > 0 && nl > 1 && items[0].path == OR_PATH_GRAPH) {
+            double est = (double)label_size(ix, lq[best]);
+            for (int t = 0; t < nl; t++)
+                if (t != best) est = est * (double)label_size(ix, lq[t]) / (double)ix->n_points;
+            if (est < (double)and_scan_threshold) items[0].path = OR_PATH_SCAN;
+        }
         items[0].pred_start = *pred_pos; items[0].pred_len = nl - 1;
         for (int t = 0; t < nl; t++) if (t != best) pred_buf[(*pred_pos)++] = lq[t];
         return 1;
@@ -322,14 +332,15 @@ static int64_t route_query(const or_index *ix, int32_t qid, const int32_t *lq_in
 
 /* Python-facing router: out_items[n_max][5] = {qid, label, path, pred_start, pred_len}. */
 int64_t or_route(const or_index *ix, int64_t n_q, const int64_t *q_off, const int32_t *q_lab, int op,
-                 int recall_mode, int exact, int32_t *out_items, int64_t n_max, int32_t *pred_buf)
+                 int recall_mode, int exact, int32_t and_scan_threshold, int32_t *out_items, int64_t n_max,
+                 int32_t *pred_buf)
 {
     int64_t n = 0, pp = 0;
     item_t *tmp = (item_t *)malloc(sizeof(item_t) * 4096);
     for (int64_t i = 0; i < n_q; i++) {
         int nl = (int)(q_off[i + 1] - q_off[i]);
-        int64_t m = route_query(ix, (int32_t)i, q_lab + q_off[i], nl, op, recall_mode, exact, tmp,
-                                pred_buf, &pp);
+        int64_t m = route_query(ix, (int32_t)i, q_lab + q_off[i], nl, op, recall_mode, exact,
+                                and_scan_threshold, tmp, pred_buf, &pp);
         if (m < 0) { free(tmp); return -1; }
         for (int64_t t = 0; t < m; t++) {
             if (n >= n_max) { free(tmp); return -2; }
@@ -477,6 +488,7 @@ typedef struct {
     const or_index *ix;
     int64_t n_q; const void *Q; const int64_t *q_off; const int32_t *q_lab;
     int op, recall_mode, exact;
+    int32_t and_scan_threshold;
     beam_params bp;
     int32_t forced_entry;
     int32_t *out_ids; double *out_dists;
@@ -502,7 +514,8 @@ static void search_one(job_t *jb, int64_t i)
     item_t *items = (item_t *)malloc(sizeof(item_t) * (size_t)(nl > 0 ? nl : 1));
     int32_t *pred = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nl * nl + 1));
     int64_t pp = 0;
-    int64_t m = route_query(ix, (int32_t)i, lq, nl, jb->op, jb->recall_mode, jb->exact, items, pred, &pp);
+    int64_t m = route_query(ix, (int32_t)i, lq, nl, jb->op, jb->recall_mode, jb->exact,
+                            jb->and_scan_threshold, items, pred, &pp);
     if (m < 0) { jb->err = 1; m = 0; }
     uint32_t qh = or_query_hash(ix->dtype, ix->dim, q);
     entry_t *all = (entry_t *)malloc(sizeof(entry_t) * (size_t)(m * k + 1));
@@ -561,12 +574,13 @@ int or_search(const or_index *ix, int64_t n_q, const void *Q, const int64_t *q_o
               int op, int recall_mode, int exact, int32_t k, int32_t itopk, int32_t search_width,
               int32_t n_init, int32_t max_iterations, uint32_t seed, int32_t forced_entry,
               int32_t *out_ids, double *out_dists, int64_t *item_ctr, int32_t max_items_per_q,
-              int nthreads)
+              int nthreads, int32_t and_scan_threshold)
 {
     job_t jb;
     memset(&jb, 0, sizeof(jb));
     jb.ix = ix; jb.n_q = n_q; jb.Q = Q; jb.q_off = q_off; jb.q_lab = q_lab;
     jb.op = op; jb.recall_mode = recall_mode; jb.exact = exact;
+    jb.and_scan_threshold = and_scan_threshold;
     jb.bp.k = k; jb.bp.itopk = itopk < k ? k : itopk;
     jb.bp.search_width = search_width < 1 ? 1 : (search_width > 64 ? 64 : search_width);
     jb.bp.n_init = n_init > 0 ? n_init : ix->R * jb.bp.search_width;

@@ -85,9 +85,18 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
                     }
                 }
             }
+            // selectivity-aware AND routing (f3, beyond the paper; include/vf.h): expected AND-set
+            // size of the greedy item under label independence, fp64, labels in ascending order
+            bool and_scan = false;
+            if (a.and_scan_thr > 0 && a.op == 2 && a.recall_mode == 0 && nch == 1 && nl > 1) {
+                double est = (double)lsize(chosen[0]);
+                for (int t = 0; t < nl; t++)
+                    if (L[t] != chosen[0]) est = __ddiv_rn(__dmul_rn(est, (double)lsize(L[t])), (double)ix.n_points);
+                and_scan = est < (double)a.and_scan_thr;
+            }
             for (int t = 0; t < nch; t++) {           // routing equation
                 const int32_t s = lsize(chosen[t]);
-                cpath[t] = (a.exact || s < ix.T) ? PATH_SCAN : PATH_GRAPH;
+                cpath[t] = (a.exact || s < ix.T || and_scan) ? PATH_SCAN : PATH_GRAPH;
                 // label sharding: an item whose label lives on another rank is shipped there
                 if (ix.owner && ix.owner[chosen[t]] != ix.rank) cpath[t] |= META_REMOTE;
                 ngraph += cpath[t] == PATH_GRAPH;
@@ -285,7 +294,8 @@ __global__ void k_pack_remote(SearchArgs a, int64_t n_slots, uint8_t *__restrict
         h->nl = qi.nl;
         h->pred = it.meta & META_PRED;
         h->qh = qi.qh;
-        h->pad[0] = h->pad[1] = h->pad[2] = 0;
+        h->pad[0] = (int32_t)(it.meta & 3u);     // the origin's routing decision (path)
+        h->pad[1] = h->pad[2] = 0;
         sent_slots[idx] = (int32_t)s;
     }
     if (lane < kRecLabels) h->labels[lane] = lane < qi.nl ? L[lane] : -1;
@@ -315,7 +325,7 @@ __global__ void k_unpack_items(SearchArgs a, const uint8_t *__restrict__ recv, i
         QueryInfo qi;
         qi.nl = h->nl; qi.n_items = 1; qi.qh = h->qh; qi.pad = 0;
         a.qinfo[i] = qi;
-        const uint32_t path = (a.exact || d.size < a.ix.T) ? PATH_SCAN : PATH_GRAPH;
+        const uint32_t path = (uint32_t)h->pad[0];   // as routed by the origin (a1)
         Item it;
         it.qid = (int32_t)i;
         it.label = l;

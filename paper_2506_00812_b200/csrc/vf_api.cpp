@@ -389,7 +389,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     const DevIndex &D = ix->dev;
     const int R = D.R, k = p->k;
     const int w = p->search_width < 1 ? 1 : p->search_width;
-    const int scan_max = p->exact ? ix->max_label_size : ix->max_ls_size;
+    // labels the scan may stream: LS lists, or every list in exact mode / with f3 AND routing
+    const int scan_max = (p->exact || p->and_scan_threshold > 0) ? ix->max_label_size : ix->max_ls_size;
     // row tiles: small in the normal path (load balance across SMs; a label split over several
     // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
     int tile_rows = p->exact ? 4096 : 512;
@@ -429,6 +430,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.op = p->op;
     a.recall_mode = p->recall_mode;
     a.exact = p->exact ? 1 : 0;
+    a.and_scan_thr = p->and_scan_threshold;
     a.tile_rows = tile_rows;
     a.max_tiles_per_label = mtpl;
     a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);

