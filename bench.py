@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--targets", default="0.90,0.99")
     ap.add_argument("--widths", default="1,2,4", help="search widths w swept for the operating points")
+    ap.add_argument("--lat-calls", type=int, default=1000, help="timed calls per small-batch latency point")
     ap.add_argument("--and-scan", default=None,
                     help="f3 selectivity-aware AND routing thresholds swept (0 = the paper's method)")
     ap.add_argument("--gt-sample", type=int, default=-1,
@@ -363,6 +364,41 @@ def main():
         e2e = {"value": n * world * args.steps / (et / 1000.0), "unit": "queries/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # -- small-batch latency (BASELINE.json configs[3]): batch 1 / 10 / 100 at the 0.90 operating
+    #    point; end to end through the C-ABI with pinned host buffers (H2D, launches, D2H inside) and
+    #    with device-resident buffers; wall clock per blocking call, p50 / p99 over many calls
+    latency = None
+    if main_tgt in results and world == 1:
+        itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
+        latency = {}
+        for bsz in (1, 10, 100):
+            Qh = torch.from_numpy(w.Q[:bsz].copy()).pin_memory()
+            qoh = torch.from_numpy(w.q_off[:bsz + 1].copy()).pin_memory()
+            qlh = torch.from_numpy(w.q_lab[:w.q_off[bsz]].copy()).pin_memory()
+            oih = torch.empty((bsz, k), dtype=torch.int32).pin_memory()
+            odh = torch.empty((bsz, k), dtype=torch.float32).pin_memory()
+            Qd, qod, qld = Qh.to(dev), qoh.to(dev), qlh.to(dev)
+            oid = torch.empty((bsz, k), dtype=torch.int32, device=dev)
+            odd = torch.empty((bsz, k), dtype=torch.float32, device=dev)
+            res = {}
+            for mode in ("host", "device"):
+                ts = []
+                for it_ in range(args.lat_calls + 50):
+                    t0 = time.perf_counter()
+                    if mode == "host":
+                        ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
+                                       and_scan_threshold=as_, stream=stream)
+                    else:
+                        ix.search_into(Qd, qod, qld, oid, odd, k=k, itopk=itopk, search_width=w_, op=op,
+                                       and_scan_threshold=as_, stream=stream)
+                        stream.synchronize()
+                    if it_ >= 50:
+                        ts.append(time.perf_counter() - t0)
+                res[mode] = {"p50_ms": 1e3 * float(np.percentile(ts, 50)),
+                             "p99_ms": 1e3 * float(np.percentile(ts, 99))}
+            latency[f"batch{bsz}"] = res
+        log(f"latency: {latency}")
+
     # -- CPU baseline: the oracle on this host's cores, bounded sample, rank 0 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
@@ -430,6 +466,7 @@ def main():
         "work": {kk: s0[kk] for kk in ("n_items", "n_scan_items", "n_graph_items", "n_segments",
                                        "scan_rows", "graph_V", "graph_E", "graph_iterations", "graph_V_max")},
         "gpu_launches": int(s0["kernel_launches"] * K),
+        "latency": latency,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clocks,

@@ -328,13 +328,22 @@ int graph_max_ctas(const SearchArgs &a) {
     graph_fn f = graph_kernel(a);
     if (!f) return 0;
     const int smem = graph_smem_bytes(a);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 32 * kWarpsPerGraphCta, smem);
-    int dev = 0, nsm = 148;
+    // occupancy queries cost microseconds: cache per (kernel, device, smem) -- small-batch latency
+    struct Key { graph_fn f; int dev, smem, ctas; };
+    static thread_local Key cache[16];
+    static thread_local int ncache = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
+    for (int i = 0; i < ncache; i++)
+        if (cache[i].f == f && cache[i].dev == dev && cache[i].smem == smem) return cache[i].ctas;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 0, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 32 * kWarpsPerGraphCta, smem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return per_sm * nsm;
+    const int ctas = per_sm * nsm;
+    cache[ncache % 16] = Key{f, dev, smem, ctas};
+    ncache++;
+    return ctas;
 }
 
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas) {

@@ -486,12 +486,22 @@ int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound) {
     const ScanLayout SL = scan_layout(a.ix.row_bytes, a.k);
     scan_fn f = a.ix.dtype == 0 ? scan_pick<0>(SL.ts, SL.cpl) : scan_pick<1>(SL.ts, SL.cpl);
     if (!f) return -1;
-    int dev = 0, nsm = 148;
+    // per-(kernel, device) setup cached: attribute calls cost microseconds per small batch
+    struct Key { scan_fn f; int dev, smem, nsm; };
+    static thread_local Key cache[16];
+    static thread_local int ncache = 0;
+    int dev = 0, nsm = -1;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    for (int i = 0; i < ncache && i < 16; i++)
+        if (cache[i].f == f && cache[i].dev == dev && cache[i].smem == (int)SL.total) nsm = cache[i].nsm;
+    if (nsm < 0) {
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
+        cache[ncache % 16] = Key{f, dev, (int)SL.total, nsm};
+        ncache++;
+    }
     int grid = nsm;
     if (grid > max_tiles_bound) grid = max_tiles_bound;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
     f<<<grid, kScanThreads, SL.total, s>>>(a, SL);
     return 1;
 }
