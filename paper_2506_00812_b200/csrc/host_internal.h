@@ -83,7 +83,10 @@ struct vf_index_impl;
 struct vf_index {
     vf::DevIndex dev{};
     int device = 0;
-    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev;
+    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev, xn, xn_ls;
+    alignas(64) unsigned char tm_ls[128];       // CUtensorMap of X_LS (tensor-core scan)
+    alignas(64) unsigned char tm_x[128];        // CUtensorMap of X rows (HS gathers)
+    bool scan_tc = false;                       // tensor-core scan available for this index
     vf_index_info info{};
     int32_t max_ls_size = 0, max_label_size = 0;
     std::mutex mu;
@@ -107,6 +110,7 @@ struct Plan {
     SearchArgs a{};
     int64_t n_slots = 0;
     int qg = 0;
+    bool tc = false;          // tensor-core scan (scan_tc.cu)
     int64_t max_tiles = 0;
     int graph_ctas = 0;
     bool multi = false;

@@ -1,0 +1,681 @@
+// a2 on the 5th-generation tensor cores -- the label-grouped exact scan (Alg. 2;
+// P:L466-L469) as a tcgen05 contraction for u8 vectors.
+//
+// Same work decomposition as k_scan (scan.cu): persistent CTAs claim row tiles of one segment
+// (an LS label with up to QG of this batch's queries). What changes is where the distances come
+// from. For u8, ||x - q||^2 = ||x||^2 + ||q||^2 - 2 q.x with every term an exact int32 (D*255^2 <
+// 2^24), so the query-group x row-tile dot products are one tcgen05.mma.kind::i8 per 32-byte K
+// step (M = 128 rows, N = the segment's queries padded to 16), accumulated exactly in TMEM.
+//
+// 320 threads, warp-specialised:
+//   warp 0  producer: claims tiles, prefetches the segment's query rows + metadata (double buffer
+//           by tile parity), and per 128-row stage issues 2-D TMA tensor loads of the rows in the
+//           128/64/32-byte-swizzled K-major layout the MMA reads (LS: one box per K chunk of the
+//           label-contiguous X_LS; HS rows in exact / f3 mode: TMA tile::gather4 of 4 rows per chunk from
+//           X through M_HS), plus the rows' global ids and precomputed norms.
+//   warp 1  MMA: owns the TMEM allocation (2 accumulator buffers); per tile it converts the query
+//           rows into the swizzled B operand, per stage one elected lane issues the K-step MMAs
+//           and commits them to the accumulator's mbarrier.
+//   warps 2-9 epilogue + selection: a warp reads its TMEM lane quarter (32 rows) for half of the
+//           query columns, forms exact distances, drops every (row, query) pair whose key is not
+//           below the query's current k-th key (a stale threshold only lets more through) or that
+//           fails the AND predicate, and publishes survivors as per-query 128-bit masks; after one
+//           named barrier the warp owning each query inserts only the surviving rows into that
+//           query's register-resident top-k list. Multi-tile segments are finished as in k_scan.
+#include <cuda.h>
+#include "common.cuh"
+
+namespace vf {
+
+namespace {
+
+constexpr int kTcThreads = 320;
+constexpr int kTcEpi = 8;             // epilogue warps
+constexpr int kTcRows = 128;          // rows per stage = MMA M
+enum : int { TS_FIRST = 1, TS_LAST = 2, TS_END = 4 };
+
+struct TcQMeta {
+    int64_t p_off;
+    int32_t slot, qid;
+    uint32_t meta;
+    int32_t nl;
+    int32_t pad[2];
+};
+
+struct TcTInfo {
+    int64_t base;
+    int32_t tile, seg, label, nq, tile_in_seg, n_tiles, hs, pad;
+};
+
+}  // namespace
+
+struct TcLayout {
+    int nst, qg, k, row_bytes, cw, nch, kpad, nmax, tmem_cols;
+    size_t off_bar, off_misc, off_meta, off_tinfo, off_rows, off_sid, off_snorm, off_qbuf, off_bsm, off_qmeta,
+        off_qn, off_thr, off_lists, off_lcnt, off_scratch, off_dist, off_gid, off_mask, total;
+};
+
+static TcLayout tc_layout(int row_bytes, int k) {
+    TcLayout L{};
+    L.row_bytes = row_bytes;
+    L.k = k;
+    L.cw = row_bytes % 128 == 0 ? 128 : row_bytes % 64 == 0 ? 64 : 32;
+    L.kpad = (row_bytes + L.cw - 1) / L.cw * L.cw;
+    L.nch = L.kpad / L.cw;
+    int qg = kScanQG;
+    while (qg > 16 && ((size_t)qg * k * 8 > 16 * 1024 || (size_t)qg * row_bytes > 16 * 1024)) qg >>= 1;
+    L.qg = qg;
+    L.nmax = (qg + 15) / 16 * 16;
+    int cols = 32;
+    while (cols < 2 * L.nmax) cols <<= 1;
+    L.tmem_cols = cols;
+    const size_t stage = (size_t)kTcRows * L.kpad;
+    size_t fixed = 2048 + 2 * (size_t)qg * row_bytes + 2 * (size_t)L.nch * L.nmax * L.cw + 2 * (size_t)qg * 32 +
+                   2 * (size_t)qg * 4 + (size_t)qg * 8 + (size_t)qg * k * 8 + (size_t)qg * 4 +
+                   (size_t)kTcEpi * (32 + 2 * k) * 8 + 2 * (size_t)qg * kTcRows * 4 + 2 * kTcRows * 4 +
+                   2 * (size_t)qg * 16 + 4096;
+    const size_t budget = 225 * 1024;
+    int nst = (int)((budget - fixed) / (stage + 2 * kTcRows * 4));
+    if (nst > 6) nst = 6;
+    L.nst = nst;
+    size_t o = 0;
+    auto take = [&](size_t bytes, size_t align) {
+        o = (o + align - 1) / align * align;
+        const size_t r = o;
+        o += bytes;
+        return r;
+    };
+    L.off_bar = take(8 * (2 * (size_t)nst + 8), 8);
+    L.off_misc = take(16, 16);
+    L.off_meta = take(16 * (size_t)nst, 16);
+    L.off_tinfo = take(2 * sizeof(TcTInfo), 16);
+    L.off_rows = take(stage * nst, 1024);
+    L.off_bsm = take(2 * (size_t)L.nch * L.nmax * L.cw, 1024);
+    L.off_sid = take((size_t)nst * kTcRows * 4, 16);
+    L.off_snorm = take((size_t)nst * kTcRows * 4, 16);
+    L.off_qbuf = take(2 * (size_t)qg * row_bytes, 16);
+    L.off_qmeta = take(2 * (size_t)qg * sizeof(TcQMeta), 16);
+    L.off_qn = take(2 * (size_t)qg * 4, 16);
+    L.off_thr = take((size_t)qg * 8, 16);
+    L.off_lists = take((size_t)qg * k * 8, 16);
+    L.off_lcnt = take((size_t)qg * 4, 16);
+    L.off_scratch = take((size_t)kTcEpi * (32 + 2 * k) * 8, 16);
+    L.off_dist = take(2 * (size_t)qg * kTcRows * 4, 16);
+    L.off_gid = take(2 * (size_t)kTcRows * 4, 16);
+    L.off_mask = take(2 * (size_t)qg * 16, 16);
+    L.total = o + 1024;     // slack for aligning the dynamic window to 1024 bytes
+    return L;
+}
+
+int scan_tc_qg(int row_bytes, int k) { return tc_layout(row_bytes, k).qg; }
+
+// ---------------------------------------------------------------- tcgen05 / TMA helpers
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)) : "memory");
+}
+// 4 rows (global row ids r[0..3]) x one box width, landing as 4 consecutive swizzled rows
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, int x, const int32_t (&r)[4],
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, K-major, swizzle span `cw` bytes: 8-row core groups `8*cw`
+// bytes apart (SBO); LBO is unused for swizzled K-major operands (encoded 1); version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, int cw) {
+    const uint64_t layout = cw == 128 ? 2 : cw == 64 ? 4 : 6;
+    return (uint64_t)((addr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)((8 * cw) >> 4) << 32) |
+           ((uint64_t)1 << 46) | (layout << 61);
+}
+
+// Instruction descriptor, kind::i8: u8 x u8 -> s32, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t idesc_u8(int n) {
+    return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+        ::"r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Byte offset of 16-byte unit `u` of row `r` inside one swizzled K chunk (rows `cw` bytes apart):
+// the hardware XORs address bits [4, 4+log2(cw/16)) with bits [7, ...) (Swizzle<b,4,3>).
+__device__ __forceinline__ uint32_t swz(int r, int u, int cw) {
+    const uint32_t o = (uint32_t)r * cw + (uint32_t)u * 16;
+    const uint32_t m = (uint32_t)(cw / 16 - 1);
+    return o ^ (((o >> 7) & m) << 4);
+}
+
+__device__ __forceinline__ void write_final_tc(const SearchArgs &a, const TcQMeta &q, const ull *L, int n, int k,
+                                               int lane) {
+    for (int t = lane; t < k; t += 32) {
+        const ull key = t < n ? L[t] : KEY_INF;
+        if (q.meta & META_DIRECT) {
+            a.out_ids[(int64_t)q.qid * k + t] = key == KEY_INF ? -1 : (int32_t)key_id(key);
+            a.out_dists[(int64_t)q.qid * k + t] = key == KEY_INF ? __uint_as_float(0x7f800000u) : key_dist(key);
+        } else {
+            a.item_res[(size_t)q.slot * k + t] = key;
+        }
+    }
+}
+
+__device__ __forceinline__ void topk_update_tc(ull *L, int *cnt_p, ull key, int k, ull *cbuf, ull *tmp, int lane) {
+    const int cnt = *cnt_p;
+    const ull thr = cnt < k ? KEY_INF : L[k - 1];
+    const bool take = key < thr;
+    const unsigned m = __ballot_sync(FULL, take);
+    if (m == 0) return;
+    const ull s = warp_sort32(take ? key : KEY_INF, lane);
+    cbuf[lane] = s;
+    __syncwarp();
+    const int nn = warp_merge(L, cnt, cbuf, __popc(m), tmp, k, lane);
+    for (int i = lane; i < nn; i += 32) L[i] = tmp[i];
+    __syncwarp();
+    if (lane == 0) *cnt_p = nn;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_scan_tc(SearchArgs a, TcLayout SL, const __grid_constant__ CUtensorMap tm_ls,
+              const __grid_constant__ CUtensorMap tm_x) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    const int nst = SL.nst, qg = SL.qg, k = SL.k, row_bytes = SL.row_bytes, cw = SL.cw, nch = SL.nch;
+    const int kpad = SL.kpad, nmax = SL.nmax;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + SL.off_bar);
+    uint64_t *full = bars, *empty = bars + nst;
+    uint64_t *qfull = bars + 2 * nst, *qempty = qfull + 2, *accfull = qfull + 4, *accempty = qfull + 6;
+    uint32_t *misc = reinterpret_cast<uint32_t *>(smem + SL.off_misc);   // [0] TMEM base, [1] flag
+    int4 *meta = reinterpret_cast<int4 *>(smem + SL.off_meta);
+    TcTInfo *tinfo = reinterpret_cast<TcTInfo *>(smem + SL.off_tinfo);
+    uint8_t *rows = smem + SL.off_rows;
+    uint8_t *bsm = smem + SL.off_bsm;
+    int32_t *sid = reinterpret_cast<int32_t *>(smem + SL.off_sid);
+    uint32_t *snorm = reinterpret_cast<uint32_t *>(smem + SL.off_snorm);
+    uint8_t *qbuf = smem + SL.off_qbuf;
+    TcQMeta *qmeta = reinterpret_cast<TcQMeta *>(smem + SL.off_qmeta);
+    uint32_t *qn = reinterpret_cast<uint32_t *>(smem + SL.off_qn);
+    ull *thr = reinterpret_cast<ull *>(smem + SL.off_thr);
+    ull *lists = reinterpret_cast<ull *>(smem + SL.off_lists);
+    int *lcnt = reinterpret_cast<int *>(smem + SL.off_lcnt);
+    ull *scratch = reinterpret_cast<ull *>(smem + SL.off_scratch);
+    uint32_t *dtile = reinterpret_cast<uint32_t *>(smem + SL.off_dist);
+    int32_t *gtile = reinterpret_cast<int32_t *>(smem + SL.off_gid);
+    uint32_t *mask = reinterpret_cast<uint32_t *>(smem + SL.off_mask);
+
+    const DevIndex &ix = a.ix;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t stage_bytes = (size_t)kTcRows * kpad;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; i++) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, kTcEpi);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(qfull + i, 1);
+            mbar_init(qempty + i, kTcEpi);
+            mbar_init(accfull + i, 1);
+            mbar_init(accempty + i, kTcEpi);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(misc)),
+                     "r"(SL.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = misc[0];
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        uint32_t n = 0, tc = 0;
+        const int ntiles = a.ctr->n_tiles;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
+            t = __shfl_sync(FULL, t, 0);
+            if (t >= ntiles) {
+                if (lane == 0) {
+                    const int slot = n % nst;
+                    mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
+                    meta[slot] = make_int4(-1, 0, 0, TS_END);
+                    mbar_arrive(full + slot);
+                }
+                break;
+            }
+            const Tile tl = a.tiles[t];
+            const bool hs = tl.hs != 0;
+            const int tp = tc & 1;
+            if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
+            __syncwarp();
+            const int nq = tl.nq;
+            TcQMeta *qm = qmeta + (size_t)tp * qg;
+            for (int g = lane; g < nq; g += 32) {
+                const ScanQuery sq = a.scan_q[tl.item_base + g];
+                TcQMeta m;
+                m.p_off = sq.p_off;
+                m.slot = sq.slot;
+                m.qid = sq.qid;
+                m.meta = sq.meta;
+                m.nl = sq.nl;
+                m.pad[0] = m.pad[1] = 0;
+                qm[g] = m;
+            }
+            if (lane == 0) {
+                TcTInfo ti;
+                ti.base = tl.base;
+                ti.tile = t; ti.seg = tl.seg; ti.label = tl.label; ti.nq = nq;
+                ti.tile_in_seg = tl.tile_in_seg; ti.n_tiles = tl.n_tiles; ti.hs = hs; ti.pad = 0;
+                tinfo[tp] = ti;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(qfull + tp, (uint32_t)nq * row_bytes);
+            __syncwarp();
+            for (int g = lane; g < nq; g += 32)
+                tma_load_1d(qbuf + ((size_t)tp * qg + g) * row_bytes, a.Qp + (int64_t)qm[g].qid * row_bytes,
+                            (uint32_t)row_bytes, qfull + tp);
+            tc++;
+            for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kTcRows) {
+                const int nr = min(kTcRows, tl.row_end - r0);
+                const int slot = n % nst;
+                uint8_t *dst = rows + (size_t)slot * stage_bytes;
+                int32_t *dsid = sid + (size_t)slot * kTcRows;
+                uint32_t *dnorm = snorm + (size_t)slot * kTcRows;
+                const int flags = (r0 == tl.row_begin ? TS_FIRST : 0) | (r0 + nr >= tl.row_end ? TS_LAST : 0);
+                if (!hs) {
+                    if (lane == 0) {
+                        mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
+                        meta[slot] = make_int4(t, r0, nr, flags);
+                        const uint32_t idb = (uint32_t)((nr * 4 + 15) & ~15);
+                        mbar_arrive_expect_tx(full + slot, (uint32_t)stage_bytes + 2 * idb);
+                        const int64_t row0 = tl.base + r0;
+                        for (int c = 0; c < nch; c++)
+                            tma_load_2d(dst + (size_t)c * kTcRows * cw, &tm_ls, c * cw, (int)row0, full + slot);
+                        tma_load_1d(dsid, ix.M_ls + row0, idb, full + slot);
+                        tma_load_1d(dnorm, ix.xn_ls + row0, idb, full + slot);
+                    }
+                    __syncwarp();
+                } else {
+                    // HS label (exact mode / f3): gather rows of X through M_HS, 4 rows per TMA
+                    // tile::gather4 per K chunk (a short group repeats its last row; ignored)
+                    const int ng = (nr + 3) >> 2;
+                    if (lane == 0) {
+                        mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
+                        meta[slot] = make_int4(t, r0, nr, flags);
+                        mbar_expect_tx(full + slot, (uint32_t)(ng * 4 * kpad));
+                    }
+                    __syncwarp();
+                    for (int q4 = lane; q4 < ng; q4 += 32) {
+                        int32_t g4[4];
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const int r = min(q4 * 4 + j, nr - 1);
+                            g4[j] = __ldg(ix.M_hs + tl.base + r0 + r);
+                        }
+                        for (int c = 0; c < nch; c++)
+                            tma_gather4(dst + (size_t)c * kTcRows * cw + (size_t)q4 * 4 * cw, &tm_x, c * cw, g4,
+                                        full + slot);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            if (q4 * 4 + j < nr) {
+                                dsid[q4 * 4 + j] = g4[j];
+                                dnorm[q4 * 4 + j] = __ldg(ix.xn + g4[j]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(full + slot);
+                }
+                n++;
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        uint32_t n = 0, tc = 0;
+        int tp = 0, npad = 16;
+        for (;;) {
+            const int slot = n % nst;
+            mbar_wait(full + slot, (n / nst) & 1);
+            const int4 m = meta[slot];
+            if (m.w & TS_END) break;
+            const int buf = n & 1;
+            mbar_wait(accempty + buf, ((n >> 1) & 1) ^ 1);
+            if (m.w & TS_FIRST) {
+                tp = tc & 1;
+                mbar_wait(qfull + tp, (tc >> 1) & 1);
+                const int nq = tinfo[tp].nq;
+                npad = max(16, (nq + 15) & ~15);
+                // queries -> swizzled K-major B operand (zero K padding past row_bytes)
+                const uint8_t *qsrc = qbuf + (size_t)tp * qg * row_bytes;
+                uint8_t *bdst = bsm + (size_t)tp * nch * nmax * cw;
+                const int upr = kpad / 16, rb16 = row_bytes / 16, upc = cw / 16;
+                for (int e = lane; e < nq * upr; e += 32) {
+                    const int g = e / upr, u = e - g * upr;
+                    const uint4 v = u < rb16 ? reinterpret_cast<const uint4 *>(qsrc + (size_t)g * row_bytes)[u]
+                                             : make_uint4(0, 0, 0, 0);
+                    const int c = u / upc;
+                    *reinterpret_cast<uint4 *>(bdst + (size_t)c * nmax * cw + swz(g, u - c * upc, cw)) = v;
+                }
+                fence_async_smem();
+                __syncwarp();
+                tc++;
+            }
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t a0 = smem_u32(rows + (size_t)slot * stage_bytes);
+                const uint32_t b0 = smem_u32(bsm + (size_t)tp * nch * nmax * cw);
+                const uint32_t id = idesc_u8(npad);
+                const uint32_t td = tbase + (uint32_t)(buf * nmax);
+                uint32_t acc = 0;
+                for (int c = 0; c < nch; c++)
+                    for (int s = 0; s < cw / 32; s++) {
+                        mma_u8(td, smem_desc(a0 + c * kTcRows * cw + s * 32, cw),
+                               smem_desc(b0 + c * nmax * cw + s * 32, cw), id, acc);
+                        acc = 1;
+                    }
+                mma_commit(accfull + buf);
+            }
+            __syncwarp();
+            n++;
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue + selection
+        const int e = warp - 2;               // 0..7
+        const int quarter = warp & 3;         // TMEM lanes 32*quarter .. +31
+        const int half = e >> 2;
+        const int row = quarter * 32 + lane;
+        ull *cbuf = scratch + (size_t)e * (32 + 2 * k);
+        ull *tmp = cbuf + 32;
+        ull *fin2 = tmp + k;
+        unsigned long long my_rows = 0, my_qrows = 0;
+        uint32_t n = 0, tc = 0;
+        TcTInfo ti;
+        ti.nq = 0;
+        const TcQMeta *qm = qmeta;
+        const uint32_t *qnp = qn;
+        int tp = 0;
+        for (;;) {
+            const int slot = n % nst;
+            mbar_wait(full + slot, (n / nst) & 1);
+            const int4 m = meta[slot];
+            if (m.w & TS_END) break;
+            if (m.w & TS_FIRST) {
+                tp = tc & 1;
+                mbar_wait(qfull + tp, (tc >> 1) & 1);
+                ti = tinfo[tp];
+                qm = qmeta + (size_t)tp * qg;
+                uint32_t *qnw = qn + (size_t)tp * qg;
+                const uint8_t *qsrc = qbuf + (size_t)tp * qg * row_bytes;
+                for (int g = e; g < ti.nq; g += kTcEpi) {
+                    for (int t = lane; t < k; t += 32) lists[(size_t)g * k + t] = KEY_INF;
+                    uint32_t s = 0;
+                    const uint32_t *w = reinterpret_cast<const uint32_t *>(qsrc + (size_t)g * row_bytes);
+                    for (int i = lane; i < row_bytes / 4; i += 32) s = __dp4a(w[i], w[i], s);
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+                    if (lane == 0) {
+                        qnw[g] = s;
+                        thr[g] = KEY_INF;
+                        lcnt[g] = 0;
+                    }
+                }
+                qnp = qnw;
+                named_bar_sync(1, 32 * kTcEpi);
+            }
+            const int nq = ti.nq, nr = m.z;
+            const int buf = n & 1;
+            const int npad = max(16, (nq + 15) & ~15);
+            uint32_t *D = dtile + (size_t)buf * qg * kTcRows;
+            int32_t *Gd = gtile + (size_t)buf * kTcRows;
+            uint32_t *Mk = mask + (size_t)buf * qg * 4;
+            // (1) accumulators -> exact distances -> threshold / predicate filter
+            mbar_wait(accfull + buf, (n >> 1) & 1);
+            tc_fence_after();
+            const bool valid = row < nr;
+            const int32_t gid = sid[(size_t)slot * kTcRows + row];
+            const int32_t xn = (int32_t)snorm[(size_t)slot * kTcRows + row];
+            if (half == 0) Gd[row] = valid ? gid : -1;
+            const int c_lo = half * (npad >> 1), c_hi = min(nq, (half + 1) * (npad >> 1));
+            for (int c0 = c_lo; c0 < c_hi; c0 += 8) {
+                uint32_t v[8];
+                tmem_ld8(tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * nmax + c0), v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const int g = c0 + j;
+                    if (g < c_hi) {
+                        const int32_t d = xn + (int32_t)qnp[g] - 2 * (int32_t)v[j];
+                        const uint32_t bits = __float_as_uint((float)d);
+                        const ull key = ((ull)bits << 32) | (uint32_t)gid;
+                        bool pass = valid && key < thr[g];
+                        if (pass) {
+                            const TcQMeta &qq = qm[g];
+                            if ((qq.meta & META_PRED) && !verify_pred(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
+                                pass = false;
+                        }
+                        if (pass) D[(size_t)g * kTcRows + row] = bits;
+                        const unsigned b = __ballot_sync(FULL, pass);
+                        if (lane == 0) Mk[g * 4 + quarter] = b;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(accempty + buf);
+                mbar_arrive(empty + slot);
+            }
+            if (threadIdx.x == 64) { my_rows += nr; my_qrows += (unsigned long long)nr * nq; }
+            // (2) the survivor masks and distances of this stage are complete
+            named_bar_sync(1, 32 * kTcEpi);
+            // (3) selection: the owner of query g inserts its surviving rows
+            for (int g = e; g < nq; g += kTcEpi) {
+                ull *L = lists + (size_t)g * k;
+                const uint32_t *Dg = D + (size_t)g * kTcRows;
+                if (k <= 32) {
+                    ull Li = lane < k ? L[lane] : KEY_INF;
+                    for (int w4 = 0; w4 < 4; w4++) {
+                        const uint32_t word = Mk[g * 4 + w4];
+                        if (!word) continue;
+                        const int r = w4 * 32 + lane;
+                        const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
+                        Li = warp_insert_topk(Li, key, k, lane);
+                    }
+                    if (lane < k) L[lane] = Li;
+                    const ull kth = __shfl_sync(FULL, Li, k - 1);
+                    if (lane == 0) thr[g] = kth;
+                } else {
+                    for (int w4 = 0; w4 < 4; w4++) {
+                        const uint32_t word = Mk[g * 4 + w4];
+                        if (!word) continue;
+                        const int r = w4 * 32 + lane;
+                        const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
+                        topk_update_tc(L, lcnt + g, key, k, cbuf, tmp, lane);
+                    }
+                    if (lane == 0) thr[g] = lcnt[g] >= k ? L[k - 1] : KEY_INF;
+                }
+                __syncwarp();
+            }
+            if (m.w & TS_LAST) {
+                const bool multi = ti.n_tiles > 1;
+                for (int g = e; g < nq; g += kTcEpi) {
+                    const ull *L = lists + (size_t)g * k;
+                    const int na = k <= 32 ? __popc(__ballot_sync(FULL, lane < k && L[lane < k ? lane : 0] != KEY_INF))
+                                           : lcnt[g];
+                    if (multi) {
+                        for (int t = lane; t < k; t += 32)
+                            a.partials[((size_t)qm[g].slot * a.max_tiles_per_label + ti.tile_in_seg) * k + t] =
+                                t < na ? L[t] : KEY_INF;
+                    } else {
+                        write_final_tc(a, qm[g], L, na, k, lane);
+                    }
+                    __syncwarp();
+                }
+                if (multi) {
+                    __threadfence();
+                    named_bar_sync(1, 32 * kTcEpi);
+                    if (threadIdx.x == 64) misc[1] = atomicAdd(&a.segs[ti.seg].pad[0], 1) == ti.n_tiles - 1;
+                    named_bar_sync(1, 32 * kTcEpi);
+                    if (misc[1]) {
+                        __threadfence();
+                        for (int g = e; g < nq; g += kTcEpi) {
+                            ull *A0 = tmp, *B0 = fin2;
+                            int na = 0;
+                            for (int t2 = 0; t2 < ti.n_tiles; t2++) {
+                                const volatile ull *P =
+                                    a.partials + ((size_t)qm[g].slot * a.max_tiles_per_label + t2) * k;
+                                for (int c0 = 0; c0 < k; c0 += 32) {
+                                    const int cn = min(32, k - c0);
+                                    const ull v = lane < cn ? P[c0 + lane] : KEY_INF;
+                                    cbuf[lane] = v;
+                                    __syncwarp();
+                                    const int nc = __popc(__ballot_sync(FULL, v != KEY_INF));
+                                    na = warp_merge(A0, na, cbuf, nc, B0, k, lane);
+                                    ull *t3 = A0; A0 = B0; B0 = t3;
+                                    __syncwarp();
+                                }
+                            }
+                            write_final_tc(a, qm[g], A0, na, k, lane);
+                            __syncwarp();
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(qempty + tp);
+                tc++;
+            }
+            n++;
+        }
+        if (threadIdx.x == 64 && my_rows) {
+            atomicAdd(&a.ctr->scan_rows, my_rows);
+            atomicAdd(&a.ctr->scan_qrows, my_qrows);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(SL.tmem_cols));
+    }
+}
+
+// ---------------------------------------------------------------- row norms (build time)
+// out[r] = ||X[ids ? ids[r] : r]||^2 as an exact int32 (u8 rows; ids < 0 -> 0).
+__global__ void k_row_norms_u8(const uint8_t *__restrict__ X, int row_bytes, const int32_t *__restrict__ ids,
+                               int64_t n, uint32_t *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < n; r += nw) {
+        const int64_t src = ids ? (int64_t)ids[r] : r;
+        uint32_t s = 0;
+        if (src >= 0) {
+            const uint32_t *w = reinterpret_cast<const uint32_t *>(X + src * row_bytes);
+            for (int i = lane; i < row_bytes / 4; i += 32) s = __dp4a(w[i], w[i], s);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        if (lane == 0) out[r] = s;
+    }
+}
+
+void launch_row_norms(const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
+                      cudaStream_t s) {
+    if (n <= 0) return;
+    k_row_norms_u8<<<148 * 8, 256, 0, s>>>(X, row_bytes, ids, n, out);
+}
+
+// ---------------------------------------------------------------- tensor maps + launch
+typedef CUresult (*encode_tiled_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+static encode_tiled_fn get_encoder() {
+    static encode_tiled_fn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<encode_tiled_fn>(p);
+    }
+    return fn;
+}
+
+// 2-D byte tensor [n_rows][row_bytes] with a box of `box_rows` rows x cw bytes, swizzled to cw.
+static bool encode_rows(CUtensorMap *m, const void *base, int row_bytes, int64_t n_rows, int cw, int box_rows) {
+    encode_tiled_fn enc = get_encoder();
+    if (!enc || n_rows <= 0) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)n_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)cw, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    const CUtensorMapSwizzle sw = cw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : cw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Encode the two maps the tensor-core scan reads (X_LS tiles, X rows); false if unsupported.
+bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x) {
+    if (ix.dtype != 0) return false;
+    const int cw = ix.row_bytes % 128 == 0 ? 128 : ix.row_bytes % 64 == 0 ? 64 : 32;
+    bool ok = encode_rows(reinterpret_cast<CUtensorMap *>(tm_x), ix.X, ix.row_bytes, ix.n_points, cw, 1);
+    ok = ok && encode_rows(reinterpret_cast<CUtensorMap *>(tm_ls), ix.Xls, ix.row_bytes,
+                           ls_rows_pad > 0 ? ls_rows_pad : 1, cw, kTcRows);
+    return ok;
+}
+
+int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x) {
+    if (max_tiles_bound <= 0) return 0;
+    const TcLayout SL = tc_layout(a.ix.row_bytes, a.k);
+    if (SL.nst < 2) return -1;
+    static thread_local int cached_dev = -1, cached_smem = -1, cached_nsm = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev || (int)SL.total > cached_smem) {
+        cudaDeviceGetAttribute(&cached_nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cached_dev = dev;
+        cached_smem = 227 * 1024;
+    }
+    int grid = cached_nsm;
+    if (grid > max_tiles_bound) grid = max_tiles_bound;
+    k_scan_tc<<<grid, kTcThreads, SL.total, s>>>(a, SL, *reinterpret_cast<const CUtensorMap *>(tm_ls),
+                                                 *reinterpret_cast<const CUtensorMap *>(tm_x));
+    return 1;
+}
+
+}  // namespace vf

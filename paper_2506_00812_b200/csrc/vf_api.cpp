@@ -218,6 +218,15 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     VF_B(ix->Xls.ensure((size_t)std::max<int64_t>(ls_rows_pad, 1) * row_bytes));
     launch_gather_rows(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), ls_rows_pad, ix->Xls.as<uint8_t>(), s);
     VF_B(cudaGetLastError());
+    // -- row norms for the tensor-core scan's ||x||^2 + ||q||^2 - 2 q.x expansion (u8, exact int32)
+    if (d->dtype == VF_U8) {
+        VF_B(ix->xn.ensure((size_t)std::max<int64_t>(N, 1) * 4));
+        VF_B(ix->xn_ls.ensure(m_ls.size() * 4));
+        launch_row_norms(ix->X.as<uint8_t>(), row_bytes, nullptr, N, ix->xn.as<uint32_t>(), s);
+        launch_row_norms(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), (int64_t)m_ls.size(),
+                         ix->xn_ls.as<uint32_t>(), s);
+        VF_B(cudaGetLastError());
+    }
     // -- predicate table: point -> sorted labels, transposed from the posting lists
     std::vector<int64_t> poff((size_t)N + 1, 0);
     for (int l = 0; l < L; l++)
@@ -259,6 +268,12 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     D.pt_off = ix->pt_off.as<int64_t>();
     D.pt_lab = ix->pt_lab.as<int32_t>();
     D.owner = owner.empty() ? nullptr : ix->owner_dev.as<int32_t>();
+    D.xn = d->dtype == VF_U8 ? ix->xn.as<uint32_t>() : nullptr;
+    D.xn_ls = d->dtype == VF_U8 ? ix->xn_ls.as<uint32_t>() : nullptr;
+    {
+        static const bool env_off = [] { const char *e = getenv("VF_SCAN_TC"); return e && atoi(e) == 0; }();
+        ix->scan_tc = d->dtype == VF_U8 && !env_off && scan_tc_encode(D, ls_rows_pad, ix->tm_ls, ix->tm_x);
+    }
     D.rank = rank;
     D.world = world;
     ix->max_ls_size = max_ls;
@@ -280,8 +295,9 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     I.bytes_map_ls = (ls_rows_pad + 4) * 4;
     I.bytes_predicate = (N + 1) * 8 + n_entries * 4;
     I.bytes_directory = (int64_t)L * sizeof(LabelDir) + (owner.empty() ? 0 : (int64_t)L * 4);
+    I.bytes_norms = d->dtype == VF_U8 ? (N + (int64_t)m_ls.size()) * 4 : 0;
     I.bytes_total = I.bytes_vectors + I.bytes_graph + I.bytes_map_hs + I.bytes_ls_vectors + I.bytes_map_ls +
-                    I.bytes_predicate + I.bytes_directory;
+                    I.bytes_predicate + I.bytes_directory + I.bytes_norms;
     I.world_size = world;
     I.rank = rank;
     I.owned_labels = n_hs + n_ls;
@@ -404,7 +420,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl = Plan();
     pl.n_slots = n_slots;
     pl.multi = mtpl > 1;
-    pl.qg = scan_qg(D.row_bytes, k);
+    pl.tc = ix->scan_tc;
+    pl.qg = pl.tc ? scan_tc_qg(D.row_bytes, k) : scan_qg(D.row_bytes, k);
     const int64_t slots = std::max<int64_t>(n_slots, 1);
     pl.max_tiles = slots * mtpl;
     const int n_init = p->n_init > 0 ? p->n_init : R * w;
@@ -508,7 +525,8 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     else nl += launch_prepare(a, s);
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
-    const int sl = launch_scan(a, s, (int)std::min<int64_t>(pl.max_tiles, INT32_MAX));
+    const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
+    const int sl = pl.tc ? launch_scan_tc(a, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(a, s, tb);
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));

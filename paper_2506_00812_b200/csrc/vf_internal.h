@@ -42,6 +42,8 @@ struct DevIndex {
     const int64_t *pt_off; // [n_points+1] predicate table offsets
     const int32_t *pt_lab; // sorted labels per point
     const int32_t *owner;  // [n_labels] owning rank of each label (label sharding, §8(e)); NULL = all local
+    const uint32_t *xn;    // [n_points] ||x||^2 (u8: exact int32) for the tensor-core scan's expansion
+    const uint32_t *xn_ls; // [ls_rows_pad + 4] ||x||^2 of the X_LS rows
     int32_t rank, world;
 };
 
@@ -168,6 +170,12 @@ int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg);
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // a2
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
+// a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
+int scan_tc_qg(int row_bytes, int k);
+bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x);
+int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x);
+void launch_row_norms(const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
+                      cudaStream_t s);
 // label sharding (§8(e)): pack remote items, unpack received ones, scatter returned results
 int launch_pack_remote(const SearchArgs &a, cudaStream_t s, int64_t n_slots, uint8_t *send, const int64_t *dst_off,
                        int32_t *sent_slots, int rec_bytes);

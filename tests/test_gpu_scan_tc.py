@@ -1,0 +1,127 @@
+"""The tensor-core scan (scan_tc.cu: tcgen05.mma.kind::i8 + TMA, u8 indexes) vs the oracle.
+
+u8 distances are exact int32 on both sides (||x||^2 + ||q||^2 - 2 q.x on the GPU, sum of squared
+differences in the oracle), so ids and distances must be bit-identical (BASELINE.json north_star:
+"bit-exact for int8"). The cases cover every swizzle width the kernel picks (row bytes a multiple
+of 128 / 64 / 32, and K padding when it is none of these), 1..64 queries per segment (MMA N 16..64),
+k on both sides of the register-list limit (32), multi-stage and multi-tile labels, HS rows
+gathered per row (exact mode and f3 routing) and the AND predicate inside the epilogue.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import small_random_index
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vf():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2506_00812_b200 import build as B
+    B.build()
+    import paper_2506_00812_b200 as vf
+    return vf
+
+
+def _u8_scan_index(dim, N=4000, L=9, seed=5):
+    """u8 vectors, L labels of ragged sizes (some > 4 stages of 128 rows), every label LS."""
+    rng = np.random.default_rng(seed)
+    X = rng.integers(0, 256, size=(N, dim), dtype=np.uint8)
+    sizes = [1, 37, 128, 129, 255, 600, 1024, 1500, N]
+    sizes = sizes[:L]
+    ids = [np.sort(rng.choice(N, size=s, replace=False)).astype(np.int32) for s in sizes]
+    off = np.zeros(L + 1, np.int64)
+    off[1:] = np.cumsum([len(i) for i in ids])
+    return X, off, np.concatenate(ids)
+
+
+def _queries(dim, n, labels, seed):
+    rng = np.random.default_rng(seed)
+    Q = rng.integers(0, 256, size=(n, dim), dtype=np.uint8)
+    qoff = np.arange(n + 1, dtype=np.int64)
+    qlab = rng.choice(labels, size=n).astype(np.int32)
+    return Q, qoff, qlab
+
+
+@pytest.mark.parametrize("dim", [16, 32, 48, 128, 192, 200])
+def test_u8_scan_all_swizzle_widths(vf, dim):
+    X, off, ids = _u8_scan_index(dim)
+    T = 1 << 30                                     # every label LS: the result is Definition 1
+    g = vf.Index(X, off, ids, T, 8)
+    o = oracle.Index(X, off, ids, T, 8)
+    Q, qoff, qlab = _queries(dim, 700, np.arange(len(off) - 1), seed=dim)
+    for k in (1, 10, 40):
+        a, ad = g.search(Q, qoff, qlab, k=k, itopk=max(k, 16))
+        e, ed = o.exact_knn(Q, qoff, qlab, k=k)
+        assert (a == e).all(), (dim, k)
+        assert (ad == ed.astype(np.float32)).all(), (dim, k)
+
+
+def test_u8_scan_full_query_groups(vf):
+    """Many queries on one label: segments of up to 64 queries (MMA N = 64)."""
+    dim = 192
+    X, off, ids = _u8_scan_index(dim)
+    g = vf.Index(X, off, ids, 1 << 30, 8)
+    o = oracle.Index(X, off, ids, 1 << 30, 8)
+    Q, qoff, _ = _queries(dim, 300, [0], seed=3)
+    qlab = np.array([5, 7] * 150, np.int32)          # 150 queries on each of two labels
+    a, ad = g.search(Q, qoff, qlab, k=10, itopk=16)
+    e, ed = o.exact_knn(Q, qoff, qlab, k=10)
+    assert (a == e).all() and (ad == ed.astype(np.float32)).all()
+    st = g.last_stats()
+    assert st["n_segments"] >= 6                     # 150 queries -> >= 3 segments per label
+
+
+@pytest.mark.parametrize("op", ["single", "and", "or"])
+def test_u8_exact_mode_hs_gathers(vf, op):
+    """exact=1 streams HS labels too, rows gathered from X through M_HS (one TMA box per row)."""
+    from workload import gen
+    cfg, X, off, ids, go, gi = small_random_index(seed=11, N=3000, D=192, L=10, F=2.0, T=300, R=8,
+                                                  dtype="u8")
+    assert (np.diff(off) >= 300).any()
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=400)
+    if op == "single":
+        qoff = np.arange(401, dtype=np.int64)
+        qlab = np.random.default_rng(1).integers(0, cfg.n_labels, size=400).astype(np.int32)
+    else:
+        qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=400, mode=op + "2")
+    a, ad = g.search(Q, qoff, qlab, k=10, op=op, exact=True)
+    e, ed = o.exact_knn(Q, qoff, qlab, k=10, op=op)
+    assert (a == e).all() and (ad == ed.astype(np.float32)).all()
+
+
+@pytest.mark.parametrize("thr", [60, 2**30])
+def test_u8_f3_routing(vf, thr):
+    from workload import gen
+    cfg, X, off, ids, go, gi = small_random_index(seed=12, N=3000, D=64, L=10, F=2.5, T=300, R=8,
+                                                  dtype="u8")
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=400)
+    qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=400, mode="and2")
+    a, ad = g.search(Q, qoff, qlab, k=10, itopk=32, op="and", and_scan_threshold=thr)
+    e, ed = o.search(Q, qoff, qlab, k=10, itopk=32, op="and", and_scan_threshold=thr)
+    assert (a == e).all() and (ad == ed.astype(np.float32)).all()
+
+
+def test_u8_multi_tile_exact(vf):
+    """Labels spanning several 4096-row tiles in exact mode: partial lists merged in-kernel."""
+    dim = 96
+    rng = np.random.default_rng(9)
+    N = 20000
+    X = rng.integers(0, 256, size=(N, dim), dtype=np.uint8)
+    off = np.array([0, N, N + 9000], np.int64)
+    ids = np.concatenate([np.arange(N), np.sort(rng.choice(N, 9000, replace=False))]).astype(np.int32)
+    g = vf.Index(X, off, ids, 1 << 30, 8)
+    o = oracle.Index(X, off, ids, 1 << 30, 8)
+    Q, qoff, qlab = _queries(dim, 150, [0, 1], seed=4)
+    a, ad = g.search(Q, qoff, qlab, k=10, exact=True)
+    e, ed = o.exact_knn(Q, qoff, qlab, k=10)
+    assert (a == e).all() and (ad == ed.astype(np.float32)).all()
+    st = g.last_stats()
+    assert st["n_tiles"] > st["n_segments"]
