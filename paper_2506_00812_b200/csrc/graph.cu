@@ -336,7 +336,8 @@ int graph_max_ctas(const SearchArgs &a) {
     cudaGetDevice(&dev);
     for (int i = 0; i < ncache; i++)
         if (cache[i].f == f && cache[i].dev == dev && cache[i].smem == smem) return cache[i].ctas;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // the attribute is per function: set the ceiling once, never a smaller value a later call needs
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     int per_sm = 0, nsm = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 32 * kWarpsPerGraphCta, smem);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

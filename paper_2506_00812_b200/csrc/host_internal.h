@@ -87,6 +87,7 @@ struct vf_index {
     alignas(64) unsigned char tm_ls[128];       // CUtensorMap of X_LS (tensor-core scan)
     alignas(64) unsigned char tm_x[128];        // CUtensorMap of X rows (HS gathers)
     bool scan_tc = false;                       // tensor-core scan available for this index
+    float tc_vmax = 0.f;                        // fp32: tf32-exact query value bound (0 = u8 / off)
     vf_index_info info{};
     int32_t max_ls_size = 0, max_label_size = 0;
     std::mutex mu;

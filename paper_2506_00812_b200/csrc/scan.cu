@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nst = SL.nst, rps = SL.rps, k = SL.k, qg = SL.qg, row_bytes = ix.row_bytes;
+    if (a.scan_gate == 1 && !*(volatile int32_t *)&a.ctr->scan_fallback) return;   // tensor-core scan ran
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
@@ -496,7 +497,7 @@ int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound) {
         if (cache[i].f == f && cache[i].dev == dev && cache[i].smem == (int)SL.total) nsm = cache[i].nsm;
     if (nsm < 0) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);   // ceiling, per function
         cache[ncache % 16] = Key{f, dev, (int)SL.total, nsm};
         ncache++;
     }

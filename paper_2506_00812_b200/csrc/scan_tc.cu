@@ -1,5 +1,8 @@
 // a2 on the 5th-generation tensor cores -- the label-grouped exact scan (Alg. 2;
-// P:L466-L469) as a tcgen05 contraction for u8 vectors.
+// P:L466-L469) as a tcgen05 contraction: kind::i8 for u8 vectors and
+// kind::tf32 for fp32 vectors whose values are integers small enough that every product and
+// partial sum is exact in fp32 (C5; checked per index at build and per batch for the queries --
+// a batch with any other query runs k_scan instead).
 //
 // Same work decomposition as k_scan (scan.cu): persistent CTAs claim row tiles of one segment
 // (an LS label with up to QG of this batch's queries). What changes is where the distances come
@@ -62,20 +65,26 @@ static TcLayout tc_layout(int row_bytes, int k) {
     L.cw = row_bytes % 128 == 0 ? 128 : row_bytes % 64 == 0 ? 64 : 32;
     L.kpad = (row_bytes + L.cw - 1) / L.cw * L.cw;
     L.nch = L.kpad / L.cw;
+    const size_t stage = (size_t)kTcRows * L.kpad;
+    auto stages_for = [&](int qg) {
+        const size_t nmax = (size_t)(qg + 15) / 16 * 16;
+        const size_t fixed = 2048 + 2 * (size_t)qg * row_bytes + 2 * (size_t)L.nch * nmax * L.cw + 2 * (size_t)qg * 32 +
+                             2 * (size_t)qg * 4 + (size_t)qg * 8 + (size_t)qg * k * 8 + (size_t)qg * 4 +
+                             (size_t)kTcEpi * (32 + 2 * k) * 8 + 2 * (size_t)qg * kTcRows * 4 + 2 * kTcRows * 4 +
+                             2 * (size_t)qg * 16 + 4096;
+        const size_t budget = 225 * 1024;
+        return fixed >= budget ? 0 : (int)((budget - fixed) / (stage + 2 * kTcRows * 4));
+    };
+    // queries per segment: as many as keep >= 3 row stages in flight (>= 2 for wide fp32 rows)
     int qg = kScanQG;
-    while (qg > 16 && ((size_t)qg * k * 8 > 16 * 1024 || (size_t)qg * row_bytes > 16 * 1024)) qg >>= 1;
+    while (qg > 16 && ((size_t)qg * k * 8 > 16 * 1024 || (size_t)qg * row_bytes > 16 * 1024 || stages_for(qg) < 3))
+        qg >>= 1;
     L.qg = qg;
     L.nmax = (qg + 15) / 16 * 16;
     int cols = 32;
     while (cols < 2 * L.nmax) cols <<= 1;
     L.tmem_cols = cols;
-    const size_t stage = (size_t)kTcRows * L.kpad;
-    size_t fixed = 2048 + 2 * (size_t)qg * row_bytes + 2 * (size_t)L.nch * L.nmax * L.cw + 2 * (size_t)qg * 32 +
-                   2 * (size_t)qg * 4 + (size_t)qg * 8 + (size_t)qg * k * 8 + (size_t)qg * 4 +
-                   (size_t)kTcEpi * (32 + 2 * k) * 8 + 2 * (size_t)qg * kTcRows * 4 + 2 * kTcRows * 4 +
-                   2 * (size_t)qg * 16 + 4096;
-    const size_t budget = 225 * 1024;
-    int nst = (int)((budget - fixed) / (stage + 2 * kTcRows * 4));
+    int nst = stages_for(qg);
     if (nst > 6) nst = 6;
     L.nst = nst;
     size_t o = 0;
@@ -107,7 +116,10 @@ static TcLayout tc_layout(int row_bytes, int k) {
     return L;
 }
 
-int scan_tc_qg(int row_bytes, int k) { return tc_layout(row_bytes, k).qg; }
+int scan_tc_qg(int row_bytes, int k) {
+    const TcLayout L = tc_layout(row_bytes, k);
+    return L.nst >= 2 ? L.qg : 0;     // 0: this (row size, k) does not fit the tensor-core scan
+}
 
 // ---------------------------------------------------------------- tcgen05 / TMA helpers
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
@@ -142,16 +154,35 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, int cw) {
            ((uint64_t)1 << 46) | (layout << 61);
 }
 
-// Instruction descriptor, kind::i8: u8 x u8 -> s32, both K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t idesc_u8(int n) {
-    return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+// Instruction descriptor, both operands K-major, M = 128, N = n:
+//   DT 0  kind::i8   u8 x u8 -> s32
+//   DT 1  kind::tf32 tf32 x tf32 -> f32 (exact for the integer-valued data it is enabled for)
+template <int DT>
+__device__ __forceinline__ uint32_t idesc_of(int n) {
+    const uint32_t fmt = DT == 0 ? (2u << 4) : ((1u << 4) | (2u << 7) | (2u << 10));
+    return fmt | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-        ::"r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+template <int DT>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    if constexpr (DT == 0)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+            ::"r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+    else
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+            ::"r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+
+// ||v||^2 of one 4-byte word as an exact integer (u8: four bytes; f32: one integer-valued float)
+template <int DT>
+__device__ __forceinline__ uint32_t sq_word(uint32_t w, uint32_t acc) {
+    if constexpr (DT == 0) return __dp4a(w, w, acc);
+    const int v = __float2int_rn(__uint_as_float(w));
+    return acc + (uint32_t)(v * v);
 }
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -201,6 +232,7 @@ __device__ __forceinline__ void topk_update_tc(ull *L, int *cnt_p, ull key, int 
     __syncwarp();
 }
 
+template <int DT>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_scan_tc(SearchArgs a, TcLayout SL, const __grid_constant__ CUtensorMap tm_ls,
               const __grid_constant__ CUtensorMap tm_x) {
@@ -232,6 +264,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t stage_bytes = (size_t)kTcRows * kpad;
+    // fp32: a batch holding a query the tf32 expansion is not exact for runs k_scan instead
+    if (DT == 1 && *(volatile int32_t *)&a.ctr->scan_fallback) return;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
@@ -394,12 +428,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) {
                 const uint32_t a0 = smem_u32(rows + (size_t)slot * stage_bytes);
                 const uint32_t b0 = smem_u32(bsm + (size_t)tp * nch * nmax * cw);
-                const uint32_t id = idesc_u8(npad);
+                const uint32_t id = idesc_of<DT>(npad);
                 const uint32_t td = tbase + (uint32_t)(buf * nmax);
                 uint32_t acc = 0;
                 for (int c = 0; c < nch; c++)
                     for (int s = 0; s < cw / 32; s++) {
-                        mma_u8(td, smem_desc(a0 + c * kTcRows * cw + s * 32, cw),
+                        mma_issue<DT>(td, smem_desc(a0 + c * kTcRows * cw + s * 32, cw),
                                smem_desc(b0 + c * nmax * cw + s * 32, cw), id, acc);
                         acc = 1;
                     }
@@ -440,7 +474,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     for (int t = lane; t < k; t += 32) lists[(size_t)g * k + t] = KEY_INF;
                     uint32_t s = 0;
                     const uint32_t *w = reinterpret_cast<const uint32_t *>(qsrc + (size_t)g * row_bytes);
-                    for (int i = lane; i < row_bytes / 4; i += 32) s = __dp4a(w[i], w[i], s);
+                    for (int i = lane; i < row_bytes / 4; i += 32) s = sq_word<DT>(w[i], s);
 #pragma unroll
                     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
                     if (lane == 0) {
@@ -474,7 +508,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int j = 0; j < 8; j++) {
                     const int g = c0 + j;
                     if (g < c_hi) {
-                        const int32_t d = xn + (int32_t)qnp[g] - 2 * (int32_t)v[j];
+                        const int32_t dot = DT == 0 ? (int32_t)v[j] : __float2int_rn(__uint_as_float(v[j]));
+                        const int32_t d = xn + (int32_t)qnp[g] - 2 * dot;
                         const uint32_t bits = __float_as_uint((float)d);
                         const ull key = ((ull)bits << 32) | (uint32_t)gid;
                         bool pass = valid && key < thr[g];
@@ -590,9 +625,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // ---------------------------------------------------------------- row norms (build time)
-// out[r] = ||X[ids ? ids[r] : r]||^2 as an exact int32 (u8 rows; ids < 0 -> 0).
-__global__ void k_row_norms_u8(const uint8_t *__restrict__ X, int row_bytes, const int32_t *__restrict__ ids,
-                               int64_t n, uint32_t *__restrict__ out) {
+// out[r] = ||X[ids ? ids[r] : r]||^2 as an exact int32 (ids < 0 -> 0).
+template <int DT>
+__global__ void k_row_norms(const uint8_t *__restrict__ X, int row_bytes, const int32_t *__restrict__ ids,
+                            int64_t n, uint32_t *__restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -601,7 +637,7 @@ __global__ void k_row_norms_u8(const uint8_t *__restrict__ X, int row_bytes, con
         uint32_t s = 0;
         if (src >= 0) {
             const uint32_t *w = reinterpret_cast<const uint32_t *>(X + src * row_bytes);
-            for (int i = lane; i < row_bytes / 4; i += 32) s = __dp4a(w[i], w[i], s);
+            for (int i = lane; i < row_bytes / 4; i += 32) s = sq_word<DT>(w[i], s);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
@@ -609,10 +645,41 @@ __global__ void k_row_norms_u8(const uint8_t *__restrict__ X, int row_bytes, con
     }
 }
 
-void launch_row_norms(const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
+void launch_row_norms(int dtype, const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
                       cudaStream_t s) {
     if (n <= 0) return;
-    k_row_norms_u8<<<148 * 8, 256, 0, s>>>(X, row_bytes, ids, n, out);
+    if (dtype == 0) k_row_norms<0><<<148 * 8, 256, 0, s>>>(X, row_bytes, ids, n, out);
+    else k_row_norms<1><<<148 * 8, 256, 0, s>>>(X, row_bytes, ids, n, out);
+}
+
+// fp32 rows: flag any value that is not an integer of magnitude <= vmax (the tf32 exactness bound)
+__global__ void k_check_tf32_exact(const float *__restrict__ X, int64_t n, int row_floats, int dim, float vmax,
+                                   int32_t *__restrict__ bad) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * row_floats;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const float v = X[e];
+        if ((int)(e % row_floats) < dim && !(v == rintf(v) && fabsf(v) <= vmax)) atomicOr(bad, 1);
+    }
+}
+
+// largest integer magnitude for which every tf32 product and partial sum is exact in fp32
+float tf32_exact_vmax(int dim) {
+    float v = 2047.f;
+    while (v > 0 && (double)dim * v * v >= 16777216.0) v -= 1.f;
+    return v;
+}
+
+bool rows_tf32_exact(const uint8_t *X, int64_t n, int row_bytes, int dim, cudaStream_t s) {
+    int32_t *bad = nullptr, h = 1;
+    if (cudaMalloc(&bad, 4) != cudaSuccess) return false;
+    cudaMemsetAsync(bad, 0, 4, s);
+    if (n > 0)
+        k_check_tf32_exact<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float *>(X), n, row_bytes / 4, dim,
+                                                   tf32_exact_vmax(dim), bad);
+    cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(bad);
+    return h == 0;
 }
 
 // ---------------------------------------------------------------- tensor maps + launch
@@ -650,7 +717,6 @@ static bool encode_rows(CUtensorMap *m, const void *base, int row_bytes, int64_t
 
 // Encode the two maps the tensor-core scan reads (X_LS tiles, X rows); false if unsupported.
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x) {
-    if (ix.dtype != 0) return false;
     const int cw = ix.row_bytes % 128 == 0 ? 128 : ix.row_bytes % 64 == 0 ? 64 : 32;
     bool ok = encode_rows(reinterpret_cast<CUtensorMap *>(tm_x), ix.X, ix.row_bytes, ix.n_points, cw, 1);
     ok = ok && encode_rows(reinterpret_cast<CUtensorMap *>(tm_ls), ix.Xls, ix.row_bytes,
@@ -662,19 +728,19 @@ int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, con
     if (max_tiles_bound <= 0) return 0;
     const TcLayout SL = tc_layout(a.ix.row_bytes, a.k);
     if (SL.nst < 2) return -1;
-    static thread_local int cached_dev = -1, cached_smem = -1, cached_nsm = 0;
+    auto f = a.ix.dtype == 0 ? k_scan_tc<0> : k_scan_tc<1>;
+    static thread_local int cached_dev[2] = {-1, -1}, cached_nsm = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev != cached_dev || (int)SL.total > cached_smem) {
+    if (dev != cached_dev[a.ix.dtype]) {
         cudaDeviceGetAttribute(&cached_nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cached_dev = dev;
-        cached_smem = 227 * 1024;
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cached_dev[a.ix.dtype] = dev;
     }
     int grid = cached_nsm;
     if (grid > max_tiles_bound) grid = max_tiles_bound;
-    k_scan_tc<<<grid, kTcThreads, SL.total, s>>>(a, SL, *reinterpret_cast<const CUtensorMap *>(tm_ls),
-                                                 *reinterpret_cast<const CUtensorMap *>(tm_x));
+    f<<<grid, kTcThreads, SL.total, s>>>(a, SL, *reinterpret_cast<const CUtensorMap *>(tm_ls),
+                                         *reinterpret_cast<const CUtensorMap *>(tm_x));
     return 1;
 }
 

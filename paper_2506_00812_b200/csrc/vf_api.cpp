@@ -219,11 +219,15 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     launch_gather_rows(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), ls_rows_pad, ix->Xls.as<uint8_t>(), s);
     VF_B(cudaGetLastError());
     // -- row norms for the tensor-core scan's ||x||^2 + ||q||^2 - 2 q.x expansion (u8, exact int32)
-    if (d->dtype == VF_U8) {
+    // (fp32: only when every value is an integer in the tf32-exact range)
+    static const bool tc_off = [] { const char *e = getenv("VF_SCAN_TC"); return e && atoi(e) == 0; }();
+    const bool tc_rows = !tc_off && (d->dtype == VF_U8 ||
+                                     rows_tf32_exact(ix->X.as<uint8_t>(), N, row_bytes, d->dim, s));
+    if (tc_rows) {
         VF_B(ix->xn.ensure((size_t)std::max<int64_t>(N, 1) * 4));
         VF_B(ix->xn_ls.ensure(m_ls.size() * 4));
-        launch_row_norms(ix->X.as<uint8_t>(), row_bytes, nullptr, N, ix->xn.as<uint32_t>(), s);
-        launch_row_norms(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), (int64_t)m_ls.size(),
+        launch_row_norms(d->dtype, ix->X.as<uint8_t>(), row_bytes, nullptr, N, ix->xn.as<uint32_t>(), s);
+        launch_row_norms(d->dtype, ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), (int64_t)m_ls.size(),
                          ix->xn_ls.as<uint32_t>(), s);
         VF_B(cudaGetLastError());
     }
@@ -268,12 +272,10 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     D.pt_off = ix->pt_off.as<int64_t>();
     D.pt_lab = ix->pt_lab.as<int32_t>();
     D.owner = owner.empty() ? nullptr : ix->owner_dev.as<int32_t>();
-    D.xn = d->dtype == VF_U8 ? ix->xn.as<uint32_t>() : nullptr;
-    D.xn_ls = d->dtype == VF_U8 ? ix->xn_ls.as<uint32_t>() : nullptr;
-    {
-        static const bool env_off = [] { const char *e = getenv("VF_SCAN_TC"); return e && atoi(e) == 0; }();
-        ix->scan_tc = d->dtype == VF_U8 && !env_off && scan_tc_encode(D, ls_rows_pad, ix->tm_ls, ix->tm_x);
-    }
+    D.xn = tc_rows ? ix->xn.as<uint32_t>() : nullptr;
+    D.xn_ls = tc_rows ? ix->xn_ls.as<uint32_t>() : nullptr;
+    ix->scan_tc = tc_rows && scan_tc_encode(D, ls_rows_pad, ix->tm_ls, ix->tm_x);
+    ix->tc_vmax = ix->scan_tc && d->dtype == VF_F32 ? tf32_exact_vmax(d->dim) : 0.f;
     D.rank = rank;
     D.world = world;
     ix->max_ls_size = max_ls;
@@ -295,7 +297,7 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     I.bytes_map_ls = (ls_rows_pad + 4) * 4;
     I.bytes_predicate = (N + 1) * 8 + n_entries * 4;
     I.bytes_directory = (int64_t)L * sizeof(LabelDir) + (owner.empty() ? 0 : (int64_t)L * 4);
-    I.bytes_norms = d->dtype == VF_U8 ? (N + (int64_t)m_ls.size()) * 4 : 0;
+    I.bytes_norms = tc_rows ? (N + (int64_t)m_ls.size()) * 4 : 0;
     I.bytes_total = I.bytes_vectors + I.bytes_graph + I.bytes_map_hs + I.bytes_ls_vectors + I.bytes_map_ls +
                     I.bytes_predicate + I.bytes_directory + I.bytes_norms;
     I.world_size = world;
@@ -420,8 +422,11 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl = Plan();
     pl.n_slots = n_slots;
     pl.multi = mtpl > 1;
-    pl.tc = ix->scan_tc;
-    pl.qg = pl.tc ? scan_tc_qg(D.row_bytes, k) : scan_qg(D.row_bytes, k);
+    // segments must fit every scan kernel that may run: the tensor-core scan, and for fp32 also
+    // k_scan (a batch with a query outside the tf32-exact range falls back to it on the device)
+    const int tc_qg = ix->scan_tc ? scan_tc_qg(D.row_bytes, k) : 0;
+    pl.tc = tc_qg > 0;
+    pl.qg = !pl.tc ? scan_qg(D.row_bytes, k) : D.dtype == 0 ? tc_qg : std::min(tc_qg, scan_qg(D.row_bytes, k));
     const int64_t slots = std::max<int64_t>(n_slots, 1);
     pl.max_tiles = slots * mtpl;
     const int n_init = p->n_init > 0 ? p->n_init : R * w;
@@ -453,6 +458,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     a.hash_slots = hs;
     a.gtab_slots = (int64_t)gslots;
+    a.tc_vmax = pl.tc ? ix->tc_vmax : 0.f;
+    a.scan_gate = pl.tc ? 1 : 0;
     pl.graph_ctas = graph_max_ctas(a);
     if (pl.graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
     const size_t nwarp = (size_t)pl.graph_ctas * kWarpsPerGraphCta;
@@ -514,6 +521,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     return VF_OK;
 }
 
+static inline int D_dtype(const vf_index *ix) { return ix->dev.dtype; }
+
 vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
                     int rec_bytes, int *launches) {
     SearchArgs &a = pl.a;
@@ -526,7 +535,11 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
-    const int sl = pl.tc ? launch_scan_tc(a, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(a, s, tb);
+    int sl = pl.tc ? launch_scan_tc(a, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(a, s, tb);
+    if (sl >= 0 && pl.tc && D_dtype(ix) == 1) {       // device-side fallback for non-exact query batches
+        const int s2 = launch_scan(a, s, tb);
+        sl = s2 < 0 ? s2 : sl + s2;
+    }
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));

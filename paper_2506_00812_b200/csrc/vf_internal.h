@@ -120,7 +120,7 @@ struct Counters {
     int32_t scan_next;
     int32_t graph_next;
     int32_t n_items;
-    int32_t pad;
+    int32_t scan_fallback;   // fp32 + tensor-core scan: a query outside the tf32-exact range
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
     int32_t remote[kMaxWorld];      // items of this batch owned by each rank (sharded index)
@@ -162,6 +162,8 @@ struct SearchArgs {
     int64_t gtab_slots;       // per-warp global overflow table size (power of two)
     unsigned long long *gtab; // [n_warp_slots][gtab_slots]
     int32_t n_warp_slots;
+    float tc_vmax;            // fp32 tensor-core scan: queries must be integers of magnitude <= this (0: no check)
+    int32_t scan_gate;        // k_scan: 0 always runs, 1 only when ctr->scan_fallback is set
 };
 
 // Launchers (implemented in the .cu files); each returns the number of kernels launched.
@@ -174,8 +176,10 @@ int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
 int scan_tc_qg(int row_bytes, int k);
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x);
 int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x);
-void launch_row_norms(const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
+void launch_row_norms(int dtype, const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
                       cudaStream_t s);
+float tf32_exact_vmax(int dim);
+bool rows_tf32_exact(const uint8_t *X, int64_t n, int row_bytes, int dim, cudaStream_t s);
 // label sharding (§8(e)): pack remote items, unpack received ones, scatter returned results
 int launch_pack_remote(const SearchArgs &a, cudaStream_t s, int64_t n_slots, uint8_t *send, const int64_t *dst_off,
                        int32_t *sent_slots, int rec_bytes);

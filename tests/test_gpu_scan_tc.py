@@ -1,4 +1,5 @@
-"""The tensor-core scan (scan_tc.cu: tcgen05.mma.kind::i8 + TMA, u8 indexes) vs the oracle.
+"""The tensor-core scan (scan_tc.cu: tcgen05.mma kind::i8 for u8, kind::tf32 for integer-valued
+fp32; TMA tensor loads) vs the oracle.
 
 u8 distances are exact int32 on both sides (||x||^2 + ||q||^2 - 2 q.x on the GPU, sum of squared
 differences in the oracle), so ids and distances must be bit-identical (BASELINE.json north_star:
@@ -77,7 +78,7 @@ def test_u8_scan_full_query_groups(vf):
 
 @pytest.mark.parametrize("op", ["single", "and", "or"])
 def test_u8_exact_mode_hs_gathers(vf, op):
-    """exact=1 streams HS labels too, rows gathered from X through M_HS (one TMA box per row)."""
+    """exact=1 streams HS labels too, rows gathered from X through M_HS (TMA tile::gather4)."""
     from workload import gen
     cfg, X, off, ids, go, gi = small_random_index(seed=11, N=3000, D=192, L=10, F=2.0, T=300, R=8,
                                                   dtype="u8")
@@ -125,3 +126,42 @@ def test_u8_multi_tile_exact(vf):
     assert (a == e).all() and (ad == ed.astype(np.float32)).all()
     st = g.last_stats()
     assert st["n_tiles"] > st["n_segments"]
+
+
+@pytest.mark.parametrize("dim", [4, 32, 48, 128])
+def test_f32int_scan_tf32_exact(vf, dim):
+    """Integer-valued fp32 (SIFT-like): kind::tf32 products and sums are exact, so bit-identical."""
+    X8, off, ids = _u8_scan_index(dim, seed=dim + 1)
+    X = X8.astype(np.float32)
+    g = vf.Index(X, off, ids, 1 << 30, 8)
+    assert g.info()["bytes_norms"] > 0              # the tensor-core scan is enabled for this index
+    o = oracle.Index(X, off, ids, 1 << 30, 8)
+    Q8, qoff, qlab = _queries(dim, 500, np.arange(len(off) - 1), seed=dim + 2)
+    Q = Q8.astype(np.float32)
+    for k in (1, 10, 40):
+        a, ad = g.search(Q, qoff, qlab, k=k, itopk=max(k, 16))
+        e, ed = o.exact_knn(Q, qoff, qlab, k=k)
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), (dim, k)
+
+
+def test_f32_non_integral_query_falls_back(vf):
+    """A batch holding a query outside the tf32-exact range runs the fp32 FFMA scan instead: the
+    integral queries stay bit-exact, the fractional one within the generic-fp32 tolerance."""
+    dim = 32
+    X8, off, ids = _u8_scan_index(dim, seed=3)
+    X = X8.astype(np.float32)
+    g = vf.Index(X, off, ids, 1 << 30, 8)
+    o = oracle.Index(X, off, ids, 1 << 30, 8)
+    Q8, qoff, qlab = _queries(dim, 200, np.arange(len(off) - 1), seed=8)
+    Q = Q8.astype(np.float32)
+    Q[17, 3] += 0.5
+    Q[40, 0] = 5000.0                                # integral but above the tf32-exact bound
+    a, ad = g.search(Q, qoff, qlab, k=10, itopk=16)
+    e, ed = o.exact_knn(Q, qoff, qlab, k=10)
+    ok = np.ones(len(Q), bool)
+    ok[[17, 40]] = False
+    assert (a[ok] == e[ok]).all() and (ad[ok] == ed[ok].astype(np.float32)).all()
+    np.testing.assert_allclose(ad[~ok], ed[~ok], rtol=1e-5)
+    # and the next all-integral batch is back on the tensor-core path, still exact
+    b, bd = g.search(Q[ok], np.arange(ok.sum() + 1, dtype=np.int64), qlab[ok], k=10, itopk=16)
+    assert (b == e[ok]).all() and (bd == ed[ok].astype(np.float32)).all()
