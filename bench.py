@@ -441,7 +441,8 @@ def main():
     line = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": tot / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if c.dtype != "u8" else "u8", "data": "synthetic",
+        "vs_baseline": None, "dtype": "u8" if (c.dtype == "u8" or info["bytes_u8_store"] > 0) else "f32",
+        "data": "synthetic",
         "config": {"workload": f"{args.config} (BASELINE.json configs[{ {'tiny': 0, 'sift': 1, 'yfcc': 2}[args.config]}])",
                    "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
                    "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
@@ -451,7 +452,10 @@ def main():
                    "recall_sample": f"first {m_gt} queries (exact-mode ground truth)",
                    "flush": "256 MiB L2 flush before every timed step (outside the step events)",
                    "parallelism": f"label-shard{world}" if world > 1 else "single",
-                   "queries": "per rank (weak scaling)" if world > 1 else "batch"},
+                   "queries": "per rank (weak scaling)" if world > 1 else "batch",
+                   "storage": ("u8 rows (lossless store of integer-valued fp32 in [0,255]; fp32 rows kept "
+                               "for out-of-range query batches)") if (c.dtype != "u8" and info["bytes_u8_store"] > 0)
+                              else c.dtype},
         "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "and_scan_threshold": r[1][5], "qps": n * world * K / (r[4] / 1000.0),
                                    "ms_per_step": r[4] / K, "recall_strict": r[1][1],
                                    "recall_tie_aware": r[1][2]} for t, r in results.items()},

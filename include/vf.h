@@ -178,7 +178,8 @@ typedef struct {
     int64_t bytes_map_ls;               /* M_LS: ls_rows * 4 */
     int64_t bytes_predicate;            /* point -> labels table: (n_points+1)*8 + entries*4 */
     int64_t bytes_directory;            /* per-label metadata */
-    int64_t bytes_norms;                /* u8: ||x||^2 per point and per X_LS row (tensor-core scan) */
+    int64_t bytes_norms;                /* ||x||^2 per point and per X_LS row (tensor-core scan) */
+    int64_t bytes_u8_store;             /* integer-valued fp32 in [0,255]: lossless u8 X and X_LS copies */
     int64_t bytes_total;                /* sum of the above */
     int32_t world_size, rank;
     int64_t owned_labels;               /* labels whose lists live on this rank */

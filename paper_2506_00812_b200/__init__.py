@@ -55,7 +55,8 @@ class IndexInfo(C.Structure):
                [("row_bytes", C.c_int32), ("degree_R", C.c_int32)] + \
                [(n, C.c_int64) for n in ("bytes_vectors", "bytes_graph", "bytes_map_hs",
                                          "bytes_ls_vectors", "bytes_map_ls", "bytes_predicate",
-                                         "bytes_directory", "bytes_norms", "bytes_total")] + \
+                                         "bytes_directory", "bytes_norms", "bytes_u8_store",
+                                         "bytes_total")] + \
                [("world_size", C.c_int32), ("rank", C.c_int32), ("owned_labels", C.c_int64)]
 
 

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
     typedef Acc<DT> A;
     constexpr int RP = 32 / TEAM;                       // rows per pass
     constexpr int GROUP = MAXCPL >= 8 ? 1 : (MAXCPL >= 4 ? 2 : 8 / MAXCPL);  // passes in flight together
+    if (gate_skip(a)) return;     // u8 row store: the other view's kernel takes this batch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int team = lane / TEAM, tl = lane % TEAM;
     uint8_t *wb = smem + (size_t)wid * GL.warp_bytes;

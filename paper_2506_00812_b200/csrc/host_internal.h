@@ -57,7 +57,7 @@ struct DevBuf {
 
 // Per-stream (and per role) scratch of a search.
 struct Scratch {
-    DevBuf raw, Qp, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
+    DevBuf raw, Qp, Q8, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
         item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
     // label sharding: item records out / in, returned results, slots of the sent items
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
@@ -83,11 +83,13 @@ struct vf_index_impl;
 struct vf_index {
     vf::DevIndex dev{};
     int device = 0;
-    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev, xn, xn_ls;
+    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev, xn, xn_ls, X8, Xls8;
+    bool enc8 = false;                          // lossless u8 row store of integer-valued fp32 rows
+    vf::DevIndex dev8{};                        // ... and the u8 view the fast kernels read
     alignas(64) unsigned char tm_ls[128];       // CUtensorMap of X_LS (tensor-core scan)
     alignas(64) unsigned char tm_x[128];        // CUtensorMap of X rows (HS gathers)
-    bool scan_tc = false;                       // tensor-core scan available for this index
-    float tc_vmax = 0.f;                        // fp32: tf32-exact query value bound (0 = u8 / off)
+    bool scan_tc = false;                       // tensor-core scan available (for dev8 when enc8)
+    float chk_lo = 1.f, chk_hi = 0.f;           // fast-path query range check (hi < lo: none)
     vf_index_info info{};
     int32_t max_ls_size = 0, max_label_size = 0;
     std::mutex mu;
@@ -112,6 +114,8 @@ struct Plan {
     int64_t n_slots = 0;
     int qg = 0;
     bool tc = false;          // tensor-core scan (scan_tc.cu)
+    bool checked = false;     // fast path with a query-range check (fp32 fallback kernels launched too)
+    int graph_ctas8 = 0;      // graph grid on the u8 view (enc8)
     int64_t max_tiles = 0;
     int graph_ctas = 0;
     bool multi = false;

@@ -10,15 +10,22 @@ namespace vf {
 // ---------------------------------------------------------------- prepare: pad + hash + route
 constexpr int kPrepWarps = 32;   // queries per block (block-aggregated atomics)
 
-// fp32 + tensor-core scan: flag the batch if this query holds a value the tf32 expansion is not
-// exact for (non-integer or magnitude > tc_vmax); the batch then runs k_scan (warp-wide call).
-__device__ __forceinline__ void tf32_check_row(const SearchArgs &a, const float *row, int lane) {
+// Integer-valued fp32 fast paths (tf32 scan, u8 row store): flag the batch if this padded query row
+// holds a value outside [chk_lo, chk_hi] or not an integer, and write its u8 copy (warp-wide call).
+__device__ __forceinline__ void check_query_row(const SearchArgs &a, const float *row, int64_t q, int lane) {
     bool bad = false;
     for (int i = lane; i < a.ix.dim; i += 32) {
         const float v = row[i];
-        bad |= !(v == rintf(v) && fabsf(v) <= a.tc_vmax);
+        bad |= !(v == rintf(v) && v >= a.chk_lo && v <= a.chk_hi);
     }
-    if (__any_sync(FULL, bad) && lane == 0) atomicOr(&a.ctr->scan_fallback, 1);
+    if (a.q8) {
+        uint8_t *d8 = a.q8 + q * (int64_t)a.q8_row_bytes;
+        for (int i = lane; i < a.q8_row_bytes; i += 32) {
+            const float v = i < a.ix.dim ? row[i] : 0.f;
+            d8[i] = (uint8_t)(v >= 0.f && v <= 255.f ? (int)v : 0);
+        }
+    }
+    if (__any_sync(FULL, bad) && lane == 0) atomicOr(&a.ctr->exact_fallback, 1);
 }
 
 __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const uint8_t *__restrict__ raw,
@@ -61,7 +68,10 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) hacc += __shfl_xor_sync(FULL, hacc, o);
         const uint32_t qh = fmix32(hacc);
-        if (a.tc_vmax > 0.f) tf32_check_row(a, reinterpret_cast<const float *>(dst), lane);
+        if (a.chk_hi >= a.chk_lo) {
+            __syncwarp();
+            check_query_row(a, reinterpret_cast<const float *>(dst), q, lane);
+        }
 
         lo = a.q_off[q];
         nraw = (int)(a.q_off[q + 1] - lo);
@@ -328,7 +338,7 @@ __global__ void k_unpack_items(SearchArgs a, const uint8_t *__restrict__ recv, i
     uint4 *dst = reinterpret_cast<uint4 *>(const_cast<uint8_t *>(a.Qp) + i * (int64_t)a.ix.row_bytes);
     for (int c = lane; c < a.ix.chunks; c += 32) dst[c] = src[c];
     __syncwarp();
-    if (a.tc_vmax > 0.f) tf32_check_row(a, reinterpret_cast<const float *>(dst), lane);
+    if (a.chk_hi >= a.chk_lo) check_query_row(a, reinterpret_cast<const float *>(dst), i, lane);
     if (lane < kRecLabels) a.qlab[i * kRecLabels + lane] = h->labels[lane];
     if (lane == 0) {
         int64_t *qoff = const_cast<int64_t *>(a.q_off);

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nst = SL.nst, rps = SL.rps, k = SL.k, qg = SL.qg, row_bytes = ix.row_bytes;
-    if (a.scan_gate == 1 && !*(volatile int32_t *)&a.ctr->scan_fallback) return;   // tensor-core scan ran
+    if (gate_skip(a)) return;     // the tensor-core / u8 kernels took this batch
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {

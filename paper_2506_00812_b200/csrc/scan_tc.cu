@@ -264,8 +264,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const DevIndex &ix = a.ix;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t stage_bytes = (size_t)kTcRows * kpad;
-    // fp32: a batch holding a query the tf32 expansion is not exact for runs k_scan instead
-    if (DT == 1 && *(volatile int32_t *)&a.ctr->scan_fallback) return;
+    if (gate_skip(a)) return;     // a batch outside the exact range runs k_scan instead
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
@@ -652,13 +651,13 @@ void launch_row_norms(int dtype, const uint8_t *X, int row_bytes, const int32_t 
     else k_row_norms<1><<<148 * 8, 256, 0, s>>>(X, row_bytes, ids, n, out);
 }
 
-// fp32 rows: flag any value that is not an integer of magnitude <= vmax (the tf32 exactness bound)
-__global__ void k_check_tf32_exact(const float *__restrict__ X, int64_t n, int row_floats, int dim, float vmax,
-                                   int32_t *__restrict__ bad) {
+// fp32 rows: flag any value that is not an integer in [lo, hi]
+__global__ void k_check_int_range(const float *__restrict__ X, int64_t n, int row_floats, int dim, float lo, float hi,
+                                  int32_t *__restrict__ bad) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * row_floats;
          e += (int64_t)gridDim.x * blockDim.x) {
         const float v = X[e];
-        if ((int)(e % row_floats) < dim && !(v == rintf(v) && fabsf(v) <= vmax)) atomicOr(bad, 1);
+        if ((int)(e % row_floats) < dim && !(v == rintf(v) && v >= lo && v <= hi)) atomicOr(bad, 1);
     }
 }
 
@@ -669,17 +668,34 @@ float tf32_exact_vmax(int dim) {
     return v;
 }
 
-bool rows_tf32_exact(const uint8_t *X, int64_t n, int row_bytes, int dim, cudaStream_t s) {
+bool rows_int_in_range(const uint8_t *X, int64_t n, int row_bytes, int dim, float lo, float hi, cudaStream_t s) {
     int32_t *bad = nullptr, h = 1;
     if (cudaMalloc(&bad, 4) != cudaSuccess) return false;
     cudaMemsetAsync(bad, 0, 4, s);
     if (n > 0)
-        k_check_tf32_exact<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float *>(X), n, row_bytes / 4, dim,
-                                                   tf32_exact_vmax(dim), bad);
+        k_check_int_range<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float *>(X), n, row_bytes / 4, dim, lo, hi,
+                                                  bad);
     cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFree(bad);
     return h == 0;
+}
+
+// fp32 rows holding integers in [0, 255] -> their exact u8 copy (zero padded to row_bytes8)
+__global__ void k_f32_to_u8(const float *__restrict__ X, int row_floats, int64_t n, int dim, uint8_t *__restrict__ X8,
+                            int row_bytes8) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * row_bytes8;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / row_bytes8;
+        const int c = (int)(e - r * row_bytes8);
+        X8[e] = c < dim ? (uint8_t)(int)X[r * row_floats + c] : 0;
+    }
+}
+
+void launch_f32_to_u8(const uint8_t *X, int row_bytes, int64_t n, int dim, uint8_t *X8, int row_bytes8,
+                      cudaStream_t s) {
+    if (n <= 0) return;
+    k_f32_to_u8<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float *>(X), row_bytes / 4, n, dim, X8, row_bytes8);
 }
 
 // ---------------------------------------------------------------- tensor maps + launch

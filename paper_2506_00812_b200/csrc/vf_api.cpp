@@ -218,16 +218,36 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     VF_B(ix->Xls.ensure((size_t)std::max<int64_t>(ls_rows_pad, 1) * row_bytes));
     launch_gather_rows(ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), ls_rows_pad, ix->Xls.as<uint8_t>(), s);
     VF_B(cudaGetLastError());
-    // -- row norms for the tensor-core scan's ||x||^2 + ||q||^2 - 2 q.x expansion (u8, exact int32)
-    // (fp32: only when every value is an integer in the tf32-exact range)
+    // -- integer-valued fp32 fast paths, both exact:
+    //    (a) every value an integer in [0, 255]: a lossless u8 row store (X8, X_LS8) is the copy the
+    //        kernels read -- 4x fewer bytes, identical distances; the fp32 rows stay for batches
+    //        holding a query outside that range (gated fallback on the device);
+    //    (b) else every value an integer in the tf32-exact range: the scan runs on kind::tf32.
+    // Row norms feed the tensor-core scan's ||x||^2 + ||q||^2 - 2 q.x expansion (exact int32).
     static const bool tc_off = [] { const char *e = getenv("VF_SCAN_TC"); return e && atoi(e) == 0; }();
-    const bool tc_rows = !tc_off && (d->dtype == VF_U8 ||
-                                     rows_tf32_exact(ix->X.as<uint8_t>(), N, row_bytes, d->dim, s));
+    static const bool u8_off = [] { const char *e = getenv("VF_U8_STORE"); return e && atoi(e) == 0; }();
+    const bool enc8 = d->dtype == VF_F32 && !u8_off && rows_int_in_range(ix->X.as<uint8_t>(), N, row_bytes, d->dim,
+                                                                          0.f, 255.f, s);
+    const float vmax = tf32_exact_vmax(d->dim);
+    const bool tc_rows = !tc_off && (d->dtype == VF_U8 || enc8 ||
+                                     rows_int_in_range(ix->X.as<uint8_t>(), N, row_bytes, d->dim, -vmax, vmax, s));
+    const int row_bytes8 = (d->dim + 15) & ~15;
+    if (enc8) {
+        VF_B(ix->X8.ensure((size_t)std::max<int64_t>(N, 1) * row_bytes8));
+        launch_f32_to_u8(ix->X.as<uint8_t>(), row_bytes, N, d->dim, ix->X8.as<uint8_t>(), row_bytes8, s);
+        VF_B(ix->Xls8.ensure((size_t)std::max<int64_t>(ls_rows_pad, 1) * row_bytes8));
+        launch_gather_rows(ix->X8.as<uint8_t>(), row_bytes8, ix->M_ls.as<int32_t>(), ls_rows_pad,
+                           ix->Xls8.as<uint8_t>(), s);
+        VF_B(cudaGetLastError());
+    }
+    const int fast_dt = enc8 ? VF_U8 : d->dtype;
+    const int fast_rb = enc8 ? row_bytes8 : row_bytes;
+    const uint8_t *fast_X = enc8 ? ix->X8.as<uint8_t>() : ix->X.as<uint8_t>();
     if (tc_rows) {
         VF_B(ix->xn.ensure((size_t)std::max<int64_t>(N, 1) * 4));
         VF_B(ix->xn_ls.ensure(m_ls.size() * 4));
-        launch_row_norms(d->dtype, ix->X.as<uint8_t>(), row_bytes, nullptr, N, ix->xn.as<uint32_t>(), s);
-        launch_row_norms(d->dtype, ix->X.as<uint8_t>(), row_bytes, ix->M_ls.as<int32_t>(), (int64_t)m_ls.size(),
+        launch_row_norms(fast_dt, fast_X, fast_rb, nullptr, N, ix->xn.as<uint32_t>(), s);
+        launch_row_norms(fast_dt, fast_X, fast_rb, ix->M_ls.as<int32_t>(), (int64_t)m_ls.size(),
                          ix->xn_ls.as<uint32_t>(), s);
         VF_B(cudaGetLastError());
     }
@@ -272,12 +292,26 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     D.pt_off = ix->pt_off.as<int64_t>();
     D.pt_lab = ix->pt_lab.as<int32_t>();
     D.owner = owner.empty() ? nullptr : ix->owner_dev.as<int32_t>();
-    D.xn = tc_rows ? ix->xn.as<uint32_t>() : nullptr;
-    D.xn_ls = tc_rows ? ix->xn_ls.as<uint32_t>() : nullptr;
-    ix->scan_tc = tc_rows && scan_tc_encode(D, ls_rows_pad, ix->tm_ls, ix->tm_x);
-    ix->tc_vmax = ix->scan_tc && d->dtype == VF_F32 ? tf32_exact_vmax(d->dim) : 0.f;
     D.rank = rank;
     D.world = world;
+    D.xn = tc_rows && !enc8 ? ix->xn.as<uint32_t>() : nullptr;
+    D.xn_ls = tc_rows && !enc8 ? ix->xn_ls.as<uint32_t>() : nullptr;
+    ix->enc8 = enc8;
+    if (enc8) {                 // the u8 view: same directory / graphs / maps, u8 rows
+        DevIndex &E = ix->dev8;
+        E = D;
+        E.dtype = VF_U8;
+        E.row_bytes = row_bytes8;
+        E.chunks = row_bytes8 / 16;
+        E.X = ix->X8.as<uint8_t>();
+        E.Xls = ix->Xls8.as<uint8_t>();
+        E.xn = tc_rows ? ix->xn.as<uint32_t>() : nullptr;
+        E.xn_ls = tc_rows ? ix->xn_ls.as<uint32_t>() : nullptr;
+    }
+    ix->scan_tc = tc_rows && scan_tc_encode(enc8 ? ix->dev8 : D, ls_rows_pad, ix->tm_ls, ix->tm_x);
+    // query range check of the fast path (chk_hi < chk_lo: none)
+    ix->chk_lo = enc8 ? 0.f : ix->scan_tc && d->dtype == VF_F32 ? -vmax : 1.f;
+    ix->chk_hi = enc8 ? 255.f : ix->scan_tc && d->dtype == VF_F32 ? vmax : 0.f;
     ix->max_ls_size = max_ls;
     ix->max_label_size = max_any;
 
@@ -298,8 +332,9 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     I.bytes_predicate = (N + 1) * 8 + n_entries * 4;
     I.bytes_directory = (int64_t)L * sizeof(LabelDir) + (owner.empty() ? 0 : (int64_t)L * 4);
     I.bytes_norms = tc_rows ? (N + (int64_t)m_ls.size()) * 4 : 0;
+    I.bytes_u8_store = enc8 ? (N + ls_rows_pad) * row_bytes8 : 0;
     I.bytes_total = I.bytes_vectors + I.bytes_graph + I.bytes_map_hs + I.bytes_ls_vectors + I.bytes_map_ls +
-                    I.bytes_predicate + I.bytes_directory + I.bytes_norms;
+                    I.bytes_predicate + I.bytes_directory + I.bytes_norms + I.bytes_u8_store;
     I.world_size = world;
     I.rank = rank;
     I.owned_labels = n_hs + n_ls;
@@ -422,11 +457,15 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl = Plan();
     pl.n_slots = n_slots;
     pl.multi = mtpl > 1;
-    // segments must fit every scan kernel that may run: the tensor-core scan, and for fp32 also
-    // k_scan (a batch with a query outside the tf32-exact range falls back to it on the device)
-    const int tc_qg = ix->scan_tc ? scan_tc_qg(D.row_bytes, k) : 0;
+    // segments must fit every scan kernel that may run: the fast one (tensor-core scan, on the u8
+    // view when enc8) and, when a query-range check is active, k_scan on the fp32 rows (a batch
+    // with a query outside the exact range falls back to it on the device)
+    const DevIndex &F = ix->enc8 ? ix->dev8 : D;
+    const int tc_qg = ix->scan_tc ? scan_tc_qg(F.row_bytes, k) : 0;
     pl.tc = tc_qg > 0;
-    pl.qg = !pl.tc ? scan_qg(D.row_bytes, k) : D.dtype == 0 ? tc_qg : std::min(tc_qg, scan_qg(D.row_bytes, k));
+    pl.checked = ix->chk_hi >= ix->chk_lo;
+    pl.qg = pl.tc ? tc_qg : scan_qg(F.row_bytes, k);
+    if (pl.checked) pl.qg = std::min(pl.qg, scan_qg(D.row_bytes, k));
     const int64_t slots = std::max<int64_t>(n_slots, 1);
     pl.max_tiles = slots * mtpl;
     const int n_init = p->n_init > 0 ? p->n_init : R * w;
@@ -458,14 +497,28 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     a.hash_slots = hs;
     a.gtab_slots = (int64_t)gslots;
-    a.tc_vmax = pl.tc ? ix->tc_vmax : 0.f;
-    a.scan_gate = pl.tc ? 1 : 0;
+    a.chk_lo = ix->chk_lo;
+    a.chk_hi = ix->chk_hi;
+    a.q8 = nullptr;
+    a.q8_row_bytes = ix->enc8 ? ix->dev8.row_bytes : 0;
+    a.gate = 0;
     pl.graph_ctas = graph_max_ctas(a);
     if (pl.graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
-    const size_t nwarp = (size_t)pl.graph_ctas * kWarpsPerGraphCta;
+    size_t nwarp = (size_t)pl.graph_ctas * kWarpsPerGraphCta;
+    if (ix->enc8) {
+        SearchArgs a8 = a;
+        a8.ix = ix->dev8;
+        pl.graph_ctas8 = graph_max_ctas(a8);
+        if (pl.graph_ctas8 <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for the u8 row size");
+        nwarp = std::max(nwarp, (size_t)pl.graph_ctas8 * kWarpsPerGraphCta);
+    }
 
     bool fresh = false;
     VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
+    if (ix->enc8) {
+        VF_CUDA(sc->Q8.ensure((size_t)std::max<int64_t>(n, 1) * ix->dev8.row_bytes));
+        a.q8 = sc->Q8.as<uint8_t>();
+    }
     VF_CUDA(sc->qoff.ensure((size_t)(n + 1) * 8));
     VF_CUDA(sc->qlab.ensure((size_t)slots * 4));
     VF_CUDA(sc->qinfo.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(QueryInfo)));
@@ -535,15 +588,35 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
-    int sl = pl.tc ? launch_scan_tc(a, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(a, s, tb);
-    if (sl >= 0 && pl.tc && D_dtype(ix) == 1) {       // device-side fallback for non-exact query batches
-        const int s2 = launch_scan(a, s, tb);
+    // Fast kernels gated on "no query outside the exact range" (gate 1), the fp32 FFMA kernels on
+    // the opposite (gate 2); without a range check only the fast set runs (gate 0).
+    SearchArgs fast = a, slow = a;
+    if (ix->enc8) {
+        fast.ix = ix->dev8;
+        fast.Qp = sc->Q8.as<uint8_t>();
+        fast.q8 = nullptr;
+    }
+    fast.gate = pl.checked ? 1 : 0;
+    slow.gate = 2;
+    int sl = pl.tc ? launch_scan_tc(fast, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(fast, s, tb);
+    if (sl >= 0 && pl.checked) {
+        const int s2 = launch_scan(slow, s, tb);
         sl = s2 < 0 ? s2 : sl + s2;
     }
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));
-    const int gl = launch_graph(a, s, (int)std::min<int64_t>(pl.n_slots, INT32_MAX), pl.graph_ctas);
+    const int gb = (int)std::min<int64_t>(pl.n_slots, INT32_MAX);
+    int gl;
+    if (ix->enc8) {
+        gl = launch_graph(fast, s, gb, pl.graph_ctas8);
+        const int g2 = gl < 0 ? 0 : launch_graph(slow, s, gb, pl.graph_ctas);
+        gl = g2 < 0 ? g2 : gl + g2;
+    } else {
+        SearchArgs ga = a;
+        ga.gate = 0;
+        gl = launch_graph(ga, s, gb, pl.graph_ctas);
+    }
     if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
     nl += gl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));
@@ -717,7 +790,7 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->graph_iterations = (int64_t)c.graph_iters;
     st->graph_V_max = (int64_t)c.graph_V_max;
     st->kernel_launches = sc->last_launches;
-    st->row_bytes = ix->dev.row_bytes;
+    st->row_bytes = ix->enc8 && !c.exact_fallback ? ix->dev8.row_bytes : ix->dev.row_bytes;   // rows the kernels read
     if (sc->profiled) {
         float t;
         cudaEventElapsedTime(&t, sc->ev[1], sc->ev[2]); st->ms_route = t;

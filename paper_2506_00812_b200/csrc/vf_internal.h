@@ -120,7 +120,7 @@ struct Counters {
     int32_t scan_next;
     int32_t graph_next;
     int32_t n_items;
-    int32_t scan_fallback;   // fp32 + tensor-core scan: a query outside the tf32-exact range
+    int32_t exact_fallback;  // a query of this batch is outside the fast path's exact range (gate)
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
     int32_t remote[kMaxWorld];      // items of this batch owned by each rank (sharded index)
@@ -162,9 +162,20 @@ struct SearchArgs {
     int64_t gtab_slots;       // per-warp global overflow table size (power of two)
     unsigned long long *gtab; // [n_warp_slots][gtab_slots]
     int32_t n_warp_slots;
-    float tc_vmax;            // fp32 tensor-core scan: queries must be integers of magnitude <= this (0: no check)
-    int32_t scan_gate;        // k_scan: 0 always runs, 1 only when ctr->scan_fallback is set
+    // Exact fast paths for integer-valued fp32: queries are checked in k_prepare /
+    // k_unpack_items; a batch holding any query outside [chk_lo, chk_hi] or non-integral sets
+    // ctr->exact_fallback and runs the fp32 FFMA kernels instead (both sets are launched, gated).
+    float chk_lo, chk_hi;     // range check (chk_hi < chk_lo: no check)
+    uint8_t *q8;              // u8 row store: k_prepare also writes the u8 query rows here
+    int32_t q8_row_bytes;
+    int32_t gate;             // 0 always run; 1 run iff !exact_fallback; 2 run iff exact_fallback
 };
+
+__device__ __forceinline__ bool gate_skip(const SearchArgs &a) {
+    if (a.gate == 0) return false;
+    const bool fb = *(volatile const int32_t *)&a.ctr->exact_fallback != 0;
+    return a.gate == 1 ? fb : !fb;
+}
 
 // Launchers (implemented in the .cu files); each returns the number of kernels launched.
 int launch_prepare(const SearchArgs &a, cudaStream_t s);   // pad queries + route (a1)
@@ -179,7 +190,9 @@ int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, con
 void launch_row_norms(int dtype, const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
                       cudaStream_t s);
 float tf32_exact_vmax(int dim);
-bool rows_tf32_exact(const uint8_t *X, int64_t n, int row_bytes, int dim, cudaStream_t s);
+bool rows_int_in_range(const uint8_t *X, int64_t n, int row_bytes, int dim, float lo, float hi, cudaStream_t s);
+void launch_f32_to_u8(const uint8_t *X, int row_bytes, int64_t n, int dim, uint8_t *X8, int row_bytes8,
+                      cudaStream_t s);
 // label sharding (§8(e)): pack remote items, unpack received ones, scatter returned results
 int launch_pack_remote(const SearchArgs &a, cudaStream_t s, int64_t n_slots, uint8_t *send, const int64_t *dst_off,
                        int32_t *sent_slots, int rec_bytes);

@@ -288,3 +288,19 @@ def test_and_scan_routing_f3_bit_exact(vf, tiny, thr):
     oi, od, octr = o.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", and_scan_threshold=thr, counters=True)
     assert (ids == oi).all() and (d == od.astype(np.float32)).all()
     _items_match(g, octr)
+
+
+def test_u8_store_fallback_batch(vf, tiny):
+    """Integer-valued fp32 is served from the lossless u8 row store; a batch holding a fractional
+    query runs the fp32 kernels on both paths: every other query stays bit-exact."""
+    w, go, gi = tiny
+    g, o = _pair(vf, w.X, w, go, gi)
+    assert g.info()["bytes_u8_store"] > 0
+    Q = w.Q.copy()
+    Q[5, 0] += 0.25
+    ids, d = g.search(Q, w.q_off, w.q_lab, k=10, itopk=32)
+    oi, od = o.search(Q, w.q_off, w.q_lab, k=10, itopk=32)
+    keep = np.arange(len(Q)) != 5
+    assert (ids[keep] == oi[keep]).all() and (d[keep] == od[keep].astype(np.float32)).all()
+    assert g.last_stats()["row_bytes"] == (w.X.shape[1] * 4 + 15) // 16 * 16     # the fp32 rows ran
+    assert np.intersect1d(ids[5], oi[5]).size >= 9

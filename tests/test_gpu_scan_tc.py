@@ -128,28 +128,35 @@ def test_u8_multi_tile_exact(vf):
     assert st["n_tiles"] > st["n_segments"]
 
 
+@pytest.mark.parametrize("store", ["u8", "tf32"])
 @pytest.mark.parametrize("dim", [4, 32, 48, 128])
-def test_f32int_scan_tf32_exact(vf, dim):
-    """Integer-valued fp32 (SIFT-like): kind::tf32 products and sums are exact, so bit-identical."""
+def test_f32int_scan_exact(vf, dim, store):
+    """Integer-valued fp32: values in [0, 255] are kept as a lossless u8 row store (kind::i8);
+    other integers in the tf32-exact range run kind::tf32, whose products and partial sums are
+    exact. Either way ids and distances are bit-identical to the fp32 oracle."""
     X8, off, ids = _u8_scan_index(dim, seed=dim + 1)
-    X = X8.astype(np.float32)
+    shift = 0 if store == "u8" else 128
+    X = X8.astype(np.float32) - shift
     g = vf.Index(X, off, ids, 1 << 30, 8)
-    assert g.info()["bytes_norms"] > 0              # the tensor-core scan is enabled for this index
+    info = g.info()
+    assert info["bytes_norms"] > 0                  # the tensor-core scan is enabled for this index
+    assert (info["bytes_u8_store"] > 0) == (store == "u8")
     o = oracle.Index(X, off, ids, 1 << 30, 8)
     Q8, qoff, qlab = _queries(dim, 500, np.arange(len(off) - 1), seed=dim + 2)
-    Q = Q8.astype(np.float32)
+    Q = Q8.astype(np.float32) - shift
     for k in (1, 10, 40):
         a, ad = g.search(Q, qoff, qlab, k=k, itopk=max(k, 16))
         e, ed = o.exact_knn(Q, qoff, qlab, k=k)
         assert (a == e).all() and (ad == ed.astype(np.float32)).all(), (dim, k)
 
 
-def test_f32_non_integral_query_falls_back(vf):
-    """A batch holding a query outside the tf32-exact range runs the fp32 FFMA scan instead: the
-    integral queries stay bit-exact, the fractional one within the generic-fp32 tolerance."""
+@pytest.mark.parametrize("store", ["u8", "tf32"])
+def test_f32_non_integral_query_falls_back(vf, store):
+    """A batch holding a query outside the fast path's exact range runs the fp32 FFMA kernels
+    instead: the integral queries stay bit-exact, the others within the generic-fp32 tolerance."""
     dim = 32
     X8, off, ids = _u8_scan_index(dim, seed=3)
-    X = X8.astype(np.float32)
+    X = X8.astype(np.float32) - (0 if store == "u8" else 128)
     g = vf.Index(X, off, ids, 1 << 30, 8)
     o = oracle.Index(X, off, ids, 1 << 30, 8)
     Q8, qoff, qlab = _queries(dim, 200, np.arange(len(off) - 1), seed=8)
