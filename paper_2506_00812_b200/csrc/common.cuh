@@ -147,6 +147,26 @@ __device__ __forceinline__ ull warp_insert_topk(ull Li, ull key, int k, int lane
     return Li;
 }
 
+// Same contract as warp_insert_topk, for batches where many of the 32 offered keys may qualify:
+// sort them (bitonic), then keep the 32 smallest of the two sorted lists -- min against the
+// reversed candidates is a bitonic sequence -- and clean it up in 5 compare-exchange steps.
+__device__ __forceinline__ ull warp_merge_topk(ull Li, ull key, int k, int lane) {
+    const ull kth = __shfl_sync(FULL, Li, k - 1);
+    const unsigned m = __ballot_sync(FULL, key < kth);
+    if (m == 0) return Li;
+    if (__popc(m) <= 4) return warp_insert_topk(Li, key, k, lane);
+    const ull s = warp_sort32(key < kth ? key : KEY_INF, lane);
+    const ull r = __shfl_sync(FULL, s, 31 - lane);
+    ull c = Li < r ? Li : r;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const ull o = __shfl_xor_sync(FULL, c, j);
+        const bool lo = (lane & j) == 0;
+        c = lo ? (c < o ? c : o) : (c < o ? o : c);
+    }
+    return lane < k ? c : KEY_INF;
+}
+
 // ---------------------------------------------------------------- TMA bulk copy + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);

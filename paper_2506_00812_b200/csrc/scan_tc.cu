@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         if (!word) continue;
                         const int r = w4 * 32 + lane;
                         const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
-                        Li = warp_insert_topk(Li, key, k, lane);
+                        Li = warp_merge_topk(Li, key, k, lane);
                     }
                     if (lane < k) L[lane] = Li;
                     const ull kth = __shfl_sync(FULL, Li, k - 1);

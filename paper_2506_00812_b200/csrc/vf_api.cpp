@@ -446,7 +446,9 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     const int scan_max = (p->exact || p->and_scan_threshold > 0) ? ix->max_label_size : ix->max_ls_size;
     // row tiles: small in the normal path (load balance across SMs; a label split over several
     // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
-    int tile_rows = p->exact ? 4096 : 512;
+    // (the tensor-core scan finalises a label split over tiles with a grid-wide fence and a merge,
+    // which costs more than its streaming loses to imbalance: whole LS labels per tile there)
+    int tile_rows = p->exact ? 4096 : (ix->scan_tc ? 2048 : 512);
     if (!p->exact) {
         static const int env_tile = [] { const char *e = getenv("VF_TILE_ROWS"); return e ? atoi(e) : 0; }();
         if (env_tile >= 64) tile_rows = env_tile & ~63;   // experiment knob (scripts/ab.py)
