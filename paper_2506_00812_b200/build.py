@@ -34,6 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
               "-I" + CSRC]
+    common += os.environ.get("VF_NVCC_EXTRA", "").split()      # e.g. -DVF_TC_PROF (diagnostics builds)
     objs = []
     for f in CU + CPP:
         src = os.path.join(CSRC, f)

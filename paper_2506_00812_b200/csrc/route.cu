@@ -205,6 +205,7 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 tl.n_tiles = ntile;
                 tl.hs = d.size >= a.ix.T;
                 tl.pad = 0;
+                tl.n_pieces = -1;
                 a.tiles[tb + g * ntile + t] = tl;
             }
         }
@@ -235,6 +236,101 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
         a.scan_q[a.ls_itembase[d.bslot] + it.rank] = sq;
         if (it.rank == 0) a.ls_count[d.bslot] = 0;   // bucket counters stay zero between searches
     }
+}
+
+// ---------------------------------------------------------------- AND pre-filter (HS scan tiles)
+// An AND item scanned on an HS label (f3 routing, or exact mode) keeps only the points of C_l* that
+// carry every other query label -- typically a tiny fraction. Checking that needs the point's id and
+// label list (~3 sectors), gathering its vector 192+ bytes, so the rows of such tiles are filtered
+// here first, by the whole GPU: survivors (rows passing the predicate of at least one query of the
+// segment) are compacted into the pool, and the scan gathers only those and re-verifies per query.
+// A tile that overflows its piece list or the pool stays unfiltered (every row scanned): exact.
+constexpr int kFiltThreads = 256;
+constexpr int kFiltBuf = 4096;
+
+__global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
+    __shared__ int32_t buf[kFiltBuf];
+    __shared__ int64_t q_off[kScanQG];
+    __shared__ int32_t q_nl[kScanQG];
+    __shared__ int32_t p_off[kMaxPieces], p_cnt[kMaxPieces];
+    __shared__ int s_tile, s_ok, s_n, s_np, s_bad, s_flush_off;
+    const int ntiles = a.ctr->n_tiles;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&a.ctr->filter_next, 1);
+        __syncthreads();
+        const int t = s_tile;
+        if (t >= ntiles) break;
+        const Tile tl = a.tiles[t];
+        if (!tl.hs) {
+            __syncthreads();
+            continue;
+        }
+        if (threadIdx.x == 0) { s_ok = 1; s_n = 0; s_np = 0; s_bad = 0; }
+        __syncthreads();
+        if (threadIdx.x < tl.nq) {
+            const ScanQuery sq = a.scan_q[tl.item_base + threadIdx.x];
+            q_off[threadIdx.x] = sq.p_off;
+            q_nl[threadIdx.x] = sq.nl;
+            if (!(sq.meta & META_PRED)) s_ok = 0;
+        }
+        __syncthreads();
+        if (!s_ok) {
+            __syncthreads();
+            continue;
+        }
+        for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads) {
+            const int r = r0 + threadIdx.x;
+            if (r < tl.row_end) {
+                const int32_t gid = __ldg(a.ix.M_hs + tl.base + r);
+                bool pass = false;
+                for (int g = 0; g < tl.nq && !pass; g++)
+                    pass = verify_pred(a.ix, gid, a.qlab + q_off[g], q_nl[g], tl.label);
+                if (pass) buf[atomicAdd(&s_n, 1)] = gid;
+            }
+            __syncthreads();
+            const bool last = r0 + kFiltThreads >= tl.row_end;
+            if (s_n > kFiltBuf - kFiltThreads || (last && s_n > 0)) {
+                if (threadIdx.x == 0) {
+                    if (s_np == kMaxPieces) {
+                        s_bad = 1;
+                    } else {
+                        const int off = atomicAdd(&a.ctr->pool_used, s_n);
+                        if ((int64_t)off + s_n > a.pool_cap) {
+                            s_bad = 1;
+                        } else {
+                            p_off[s_np] = off;
+                            p_cnt[s_np] = s_n;
+                            s_np++;
+                            s_flush_off = off;
+                        }
+                    }
+                }
+                __syncthreads();
+                if (!s_bad)
+                    for (int i = threadIdx.x; i < s_n; i += kFiltThreads) a.pool[s_flush_off + i] = buf[i];
+                __syncthreads();
+                if (threadIdx.x == 0) s_n = 0;
+                __syncthreads();
+            }
+            if (s_bad) break;
+        }
+        if (threadIdx.x == 0) {
+            Tile *T = a.tiles + t;
+            if (s_bad) {
+                T->n_pieces = -1;
+            } else {
+                for (int i = 0; i < s_np; i++) { T->piece_off[i] = p_off[i]; T->piece_cnt[i] = p_cnt[i]; }
+                T->n_pieces = s_np;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int launch_hs_filter(const SearchArgs &a, cudaStream_t s) {
+    if (!a.pool || a.pool_cap <= 0) return 0;
+    k_hs_filter<<<148 * 8, kFiltThreads, 0, s>>>(a);
+    return 1;
 }
 
 int launch_prepare(const SearchArgs &a, cudaStream_t s) {

@@ -10,7 +10,9 @@
 // 2^24), so the query-group x row-tile dot products are one tcgen05.mma.kind::i8 per 32-byte K
 // step (M = 128 rows, N = the segment's queries padded to 16), accumulated exactly in TMEM.
 //
-// 320 threads, warp-specialised:
+// 352 threads, warp-specialised:
+//   warp 10 tile scheduler: claims tiles and resolves their metadata into a double-buffered tile
+//           slot ahead of the producer (no global round trip between consecutive tiles' stages).
 //   warp 0  producer: claims tiles, prefetches the segment's query rows + metadata (double buffer
 //           by tile parity), and per 128-row stage issues 2-D TMA tensor loads of the rows in the
 //           128/64/32-byte-swizzled K-major layout the MMA reads (LS: one box per K chunk of the
@@ -26,13 +28,14 @@
 //           named barrier the warp owning each query inserts only the surviving rows into that
 //           query's register-resident top-k list. Multi-tile segments are finished as in k_scan.
 #include <cuda.h>
+#include <cstdio>
 #include "common.cuh"
 
 namespace vf {
 
 namespace {
 
-constexpr int kTcThreads = 320;
+constexpr int kTcThreads = 352;
 constexpr int kTcEpi = 8;             // epilogue warps
 constexpr int kTcRows = 128;          // rows per stage = MMA M
 enum : int { TS_FIRST = 1, TS_LAST = 2, TS_END = 4 };
@@ -47,7 +50,8 @@ struct TcQMeta {
 
 struct TcTInfo {
     int64_t base;
-    int32_t tile, seg, label, nq, tile_in_seg, n_tiles, hs, pad;
+    int32_t tile, seg, label, nq, tile_in_seg, n_tiles, hs, row_begin, row_end, n_pieces;
+    int32_t piece_off[kMaxPieces], piece_cnt[kMaxPieces];
 };
 
 }  // namespace
@@ -94,7 +98,7 @@ static TcLayout tc_layout(int row_bytes, int k) {
         o += bytes;
         return r;
     };
-    L.off_bar = take(8 * (2 * (size_t)nst + 8), 8);
+    L.off_bar = take(8 * (2 * (size_t)nst + 10), 8);
     L.off_misc = take(16, 16);
     L.off_meta = take(16 * (size_t)nst, 16);
     L.off_tinfo = take(2 * sizeof(TcTInfo), 16);
@@ -203,6 +207,19 @@ __device__ __forceinline__ uint32_t swz(int r, int u, int cw) {
     return o ^ (((o >> 7) & m) << 4);
 }
 
+// Diagnostics build (-DVF_TC_PROF): per-role cycle breakdown of CTAs 0-1, printed at exit.
+#ifdef VF_TC_PROF
+#define TP_DECL unsigned long long tp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp_t0 = clock64();
+#define TP_MARK(i) { const unsigned long long t1_ = clock64(); tp_acc[i] += t1_ - tp_t0; tp_t0 = t1_; }
+#define TP_DUMP(name) if (lane == 0 && blockIdx.x < 2) \
+    printf("TCPROF blk %d warp %d %s: %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, warp, name, tp_acc[0], \
+           tp_acc[1], tp_acc[2], tp_acc[3], tp_acc[4], tp_acc[5], tp_acc[6], tp_acc[7]);
+#else
+#define TP_DECL
+#define TP_MARK(i)
+#define TP_DUMP(name)
+#endif
+
 __device__ __forceinline__ void write_final_tc(const SearchArgs &a, const TcQMeta &q, const ull *L, int n, int k,
                                                int lane) {
     for (int t = lane; t < k; t += 32) {
@@ -243,6 +260,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + SL.off_bar);
     uint64_t *full = bars, *empty = bars + nst;
     uint64_t *qfull = bars + 2 * nst, *qempty = qfull + 2, *accfull = qfull + 4, *accempty = qfull + 6;
+    uint64_t *tready = qfull + 8;
     uint32_t *misc = reinterpret_cast<uint32_t *>(smem + SL.off_misc);   // [0] TMEM base, [1] flag
     int4 *meta = reinterpret_cast<int4 *>(smem + SL.off_meta);
     TcTInfo *tinfo = reinterpret_cast<TcTInfo *>(smem + SL.off_tinfo);
@@ -276,6 +294,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(qempty + i, kTcEpi);
             mbar_init(accfull + i, 1);
             mbar_init(accempty + i, kTcEpi);
+            mbar_init(tready + i, 1);
         }
         fence_mbar_init();
     }
@@ -289,28 +308,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc_fence_after();
     const uint32_t tbase = misc[0];
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        uint32_t n = 0, tc = 0;
+    if (warp == 10) {
+        // ------------------------------------------------------------ tile scheduler
+        // Claims tiles and resolves their metadata (Tile record, per-query ScanQuery records) into
+        // the tile slot of its parity ahead of the producer, so no dependent global round trip sits
+        // between one tile's last row stage and the next tile's first.
+        uint32_t tc = 0;
         const int ntiles = a.ctr->n_tiles;
         for (;;) {
+            const int tp = tc & 1;
+            if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
+            __syncwarp();
             int t = 0;
             if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
             t = __shfl_sync(FULL, t, 0);
             if (t >= ntiles) {
                 if (lane == 0) {
-                    const int slot = n % nst;
-                    mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
-                    meta[slot] = make_int4(-1, 0, 0, TS_END);
-                    mbar_arrive(full + slot);
+                    tinfo[tp].tile = -1;
+                    mbar_arrive(tready + tp);
                 }
                 break;
             }
             const Tile tl = a.tiles[t];
-            const bool hs = tl.hs != 0;
-            const int tp = tc & 1;
-            if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
-            __syncwarp();
             const int nq = tl.nq;
             TcQMeta *qm = qmeta + (size_t)tp * qg;
             for (int g = lane; g < nq; g += 32) {
@@ -328,26 +347,67 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 TcTInfo ti;
                 ti.base = tl.base;
                 ti.tile = t; ti.seg = tl.seg; ti.label = tl.label; ti.nq = nq;
-                ti.tile_in_seg = tl.tile_in_seg; ti.n_tiles = tl.n_tiles; ti.hs = hs; ti.pad = 0;
+                ti.tile_in_seg = tl.tile_in_seg; ti.n_tiles = tl.n_tiles; ti.hs = tl.hs != 0;
+                ti.row_begin = tl.row_begin; ti.row_end = tl.row_end; ti.n_pieces = tl.n_pieces;
+                for (int i = 0; i < kMaxPieces; i++) { ti.piece_off[i] = tl.piece_off[i]; ti.piece_cnt[i] = tl.piece_cnt[i]; }
                 tinfo[tp] = ti;
             }
             __syncwarp();
+            if (lane == 0) mbar_arrive(tready + tp);
+            tc++;
+        }
+    } else if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        uint32_t n = 0, tc = 0;
+        TP_DECL
+        for (;;) {
+            const int tp = tc & 1;
+            TP_MARK(3)
+            if (lane == 0) mbar_wait(tready + tp, (tc >> 1) & 1);
+            __syncwarp();
+            TP_MARK(0)
+            const TcTInfo tl = tinfo[tp];
+            if (tl.tile < 0) {
+                if (lane == 0) {
+                    const int slot = n % nst;
+                    mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
+                    meta[slot] = make_int4(-1, 0, 0, TS_END);
+                    mbar_arrive(full + slot);
+                }
+                break;
+            }
+            const int t = tl.tile;
+            const bool hs = tl.hs != 0;
+            const int nq = tl.nq;
+            const TcQMeta *qm = qmeta + (size_t)tp * qg;
             if (lane == 0) mbar_arrive_expect_tx(qfull + tp, (uint32_t)nq * row_bytes);
             __syncwarp();
             for (int g = lane; g < nq; g += 32)
                 tma_load_1d(qbuf + ((size_t)tp * qg + g) * row_bytes, a.Qp + (int64_t)qm[g].qid * row_bytes,
                             (uint32_t)row_bytes, qfull + tp);
             tc++;
-            for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kTcRows) {
-                const int nr = min(kTcRows, tl.row_end - r0);
+            // rows of the tile: its range of the label, or only the AND pre-filter's survivors
+            const bool filt = hs && tl.n_pieces >= 0;
+            int total = tl.row_end - tl.row_begin;
+            if (filt) {
+                total = 0;
+                for (int i = 0; i < tl.n_pieces; i++) total += tl.piece_cnt[i];
+            }
+            const int nstage = max(1, (total + kTcRows - 1) / kTcRows);
+            for (int si = 0; si < nstage; si++) {
+                const int v0 = si * kTcRows;
+                const int r0 = tl.row_begin + v0;
+                const int nr = max(0, min(kTcRows, total - v0));
                 const int slot = n % nst;
                 uint8_t *dst = rows + (size_t)slot * stage_bytes;
                 int32_t *dsid = sid + (size_t)slot * kTcRows;
                 uint32_t *dnorm = snorm + (size_t)slot * kTcRows;
-                const int flags = (r0 == tl.row_begin ? TS_FIRST : 0) | (r0 + nr >= tl.row_end ? TS_LAST : 0);
+                const int flags = (si == 0 ? TS_FIRST : 0) | (si == nstage - 1 ? TS_LAST : 0);
+                TP_MARK(3)
                 if (!hs) {
                     if (lane == 0) {
                         mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
+                        TP_MARK(1)
                         meta[slot] = make_int4(t, r0, nr, flags);
                         const uint32_t idb = (uint32_t)((nr * 4 + 15) & ~15);
                         mbar_arrive_expect_tx(full + slot, (uint32_t)stage_bytes + 2 * idb);
@@ -373,7 +433,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const int r = min(q4 * 4 + j, nr - 1);
-                            g4[j] = __ldg(ix.M_hs + tl.base + r0 + r);
+                            if (filt) {
+                                int v = v0 + r, p = 0;
+                                while (v >= tl.piece_cnt[p]) { v -= tl.piece_cnt[p]; p++; }
+                                g4[j] = __ldg(a.pool + tl.piece_off[p] + v);
+                            } else {
+                                g4[j] = __ldg(ix.M_hs + tl.base + r0 + r);
+                            }
                         }
                         for (int c = 0; c < nch; c++)
                             tma_gather4(dst + (size_t)c * kTcRows * cw + (size_t)q4 * 4 * cw, &tm_x, c * cw, g4,
@@ -389,20 +455,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(full + slot);
                 }
+                TP_MARK(2)
                 n++;
             }
         }
+        TP_DUMP("producer(tready,empty,issue,other)")
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         uint32_t n = 0, tc = 0;
         int tp = 0, npad = 16;
+        TP_DECL
         for (;;) {
             const int slot = n % nst;
+            TP_MARK(4)
             mbar_wait(full + slot, (n / nst) & 1);
+            TP_MARK(0)
             const int4 m = meta[slot];
             if (m.w & TS_END) break;
             const int buf = n & 1;
             mbar_wait(accempty + buf, ((n >> 1) & 1) ^ 1);
+            TP_MARK(1)
             if (m.w & TS_FIRST) {
                 tp = tc & 1;
                 mbar_wait(qfull + tp, (tc >> 1) & 1);
@@ -422,6 +494,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 fence_async_smem();
                 __syncwarp();
                 tc++;
+                TP_MARK(2)
             }
             tc_fence_after();
             if (lane == 0) {
@@ -439,8 +512,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mma_commit(accfull + buf);
             }
             __syncwarp();
+            TP_MARK(3)
             n++;
         }
+        TP_DUMP("mma(full,accempty,first,issue,other)")
     } else {
         // ------------------------------------------------------------ epilogue + selection
         const int e = warp - 2;               // 0..7
@@ -457,9 +532,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const TcQMeta *qm = qmeta;
         const uint32_t *qnp = qn;
         int tp = 0;
+        TP_DECL
         for (;;) {
             const int slot = n % nst;
+            TP_MARK(7)
             mbar_wait(full + slot, (n / nst) & 1);
+            TP_MARK(0)
             const int4 m = meta[slot];
             if (m.w & TS_END) break;
             if (m.w & TS_FIRST) {
@@ -484,6 +562,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 qnp = qnw;
                 named_bar_sync(1, 32 * kTcEpi);
+                TP_MARK(1)
             }
             const int nq = ti.nq, nr = m.z;
             const int buf = n & 1;
@@ -492,7 +571,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             int32_t *Gd = gtile + (size_t)buf * kTcRows;
             uint32_t *Mk = mask + (size_t)buf * qg * 4;
             // (1) accumulators -> exact distances -> threshold / predicate filter
+            TP_MARK(7)
             mbar_wait(accfull + buf, (n >> 1) & 1);
+            TP_MARK(2)
             tc_fence_after();
             const bool valid = row < nr;
             const int32_t gid = sid[(size_t)slot * kTcRows + row];
@@ -530,8 +611,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mbar_arrive(empty + slot);
             }
             if (threadIdx.x == 64) { my_rows += nr; my_qrows += (unsigned long long)nr * nq; }
+            TP_MARK(3)
             // (2) the survivor masks and distances of this stage are complete
             named_bar_sync(1, 32 * kTcEpi);
+            TP_MARK(4)
             // (3) selection: the owner of query g inserts its surviving rows
             for (int g = e; g < nq; g += kTcEpi) {
                 ull *L = lists + (size_t)g * k;
@@ -560,6 +643,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 __syncwarp();
             }
+            TP_MARK(5)
             if (m.w & TS_LAST) {
                 const bool multi = ti.n_tiles > 1;
                 for (int g = e; g < nq; g += kTcEpi) {
@@ -607,9 +691,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(qempty + tp);
                 tc++;
+                TP_MARK(6)
             }
             n++;
         }
+        if (warp == 2 || warp == 6) TP_DUMP("epi(full,first,accfull,compute,bar,select,last,other)")
         if (threadIdx.x == 64 && my_rows) {
             atomicAdd(&a.ctr->scan_rows, my_rows);
             atomicAdd(&a.ctr->scan_qrows, my_qrows);

@@ -504,6 +504,11 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.q8 = nullptr;
     a.q8_row_bytes = ix->enc8 ? ix->dev8.row_bytes : 0;
     a.gate = 0;
+    // AND items scanned on HS labels (f3 routing or exact mode) are pre-filtered for the
+    // tensor-core scan (k_hs_filter); the survivor pool is sized per search, overflow is exact
+    pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0);
+    a.pool = nullptr;
+    a.pool_cap = 0;
     pl.graph_ctas = graph_max_ctas(a);
     if (pl.graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
     size_t nwarp = (size_t)pl.graph_ctas * kWarpsPerGraphCta;
@@ -517,6 +522,13 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
 
     bool fresh = false;
     VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
+    if (pl.filter) {
+        int64_t cap = 16ll << 20;                       // 64 MB of survivor ids
+        if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
+        VF_CUDA(sc->pool.ensure((size_t)cap * 4));
+        a.pool = sc->pool.as<int32_t>();
+        a.pool_cap = (int32_t)cap;
+    }
     if (ix->enc8) {
         VF_CUDA(sc->Q8.ensure((size_t)std::max<int64_t>(n, 1) * ix->dev8.row_bytes));
         a.q8 = sc->Q8.as<uint8_t>();
@@ -588,6 +600,7 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     if (recv) nl += launch_unpack_items(a, s, recv, n_recv, rec_bytes);
     else nl += launch_prepare(a, s);
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
+    if (pl.filter) nl += launch_hs_filter(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     // Fast kernels gated on "no query outside the exact range" (gate 1), the fp32 FFMA kernels on

@@ -86,8 +86,10 @@ struct Segment {
     int32_t pad[3];
 };
 
-// A row tile of a segment: everything the scan producer needs in one 48-byte record, so claiming a
-// tile costs one dependent load (written by k_segments).
+constexpr int kMaxPieces = 6;        // survivor pieces of a pre-filtered HS tile (k_hs_filter)
+
+// A row tile of a segment: everything the scan producer needs in one record, so claiming a tile
+// costs one dependent load (written by k_segments; survivor pieces by k_hs_filter).
 struct Tile {
     int64_t base;        // first row of the label in X_LS (or in M_HS for an HS label, exact mode)
     int32_t seg;
@@ -100,6 +102,13 @@ struct Tile {
     int32_t n_tiles;
     int32_t hs;          // 1: HS label scanned in exact mode (rows gathered through M_HS)
     int32_t pad;
+    // AND pre-filter (HS tiles whose queries all carry a predicate): -1 = not filtered (every row
+    // of the range is scanned), else the rows passing some query's predicate, as pieces of the
+    // survivor pool -- the tensor-core scan gathers only those
+    int32_t n_pieces;
+    int32_t piece_off[kMaxPieces];
+    int32_t piece_cnt[kMaxPieces];
+    int32_t pad2[3];
 };
 
 // Per scan item, in scan_slots order: what the scan needs about its query (written by k_scatter).
@@ -121,6 +130,8 @@ struct Counters {
     int32_t graph_next;
     int32_t n_items;
     int32_t exact_fallback;  // a query of this batch is outside the fast path's exact range (gate)
+    int32_t filter_next;     // k_hs_filter tile cursor
+    int32_t pool_used;       // survivor pool bump allocator
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
     int32_t remote[kMaxWorld];      // items of this batch owned by each rank (sharded index)
@@ -169,6 +180,8 @@ struct SearchArgs {
     uint8_t *q8;              // u8 row store: k_prepare also writes the u8 query rows here
     int32_t q8_row_bytes;
     int32_t gate;             // 0 always run; 1 run iff !exact_fallback; 2 run iff exact_fallback
+    int32_t *pool;            // AND pre-filter survivor ids (k_hs_filter)
+    int32_t pool_cap;
 };
 
 __device__ __forceinline__ bool gate_skip(const SearchArgs &a) {
@@ -183,6 +196,7 @@ int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg);
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // a2
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
+int launch_hs_filter(const SearchArgs &a, cudaStream_t s);  // AND pre-filter of HS scan tiles
 // a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
 int scan_tc_qg(int row_bytes, int k);
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x);

@@ -172,3 +172,23 @@ def test_f32_non_integral_query_falls_back(vf, store):
     # and the next all-integral batch is back on the tensor-core path, still exact
     b, bd = g.search(Q[ok], np.arange(ok.sum() + 1, dtype=np.int64), qlab[ok], k=10, itopk=16)
     assert (b == e[ok]).all() and (bd == ed[ok].astype(np.float32)).all()
+
+
+def test_and_prefilter_pool_overflow_is_exact(vf, monkeypatch):
+    """HS AND tiles are pre-filtered into a survivor pool; tiles that overflow it (or their piece
+    list) are scanned in full. Either way the results equal Definition 1."""
+    from workload import gen
+    cfg, X, off, ids, go, gi = small_random_index(seed=21, N=6000, D=64, L=8, F=3.0, T=500, R=8,
+                                                  dtype="u8")
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=300)
+    qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=300, mode="and2")
+    e, ed = o.exact_knn(Q, qoff, qlab, k=10, op="and")
+    for cap in (None, "1", "300"):
+        if cap is None:
+            monkeypatch.delenv("VF_POOL_CAP", raising=False)
+        else:
+            monkeypatch.setenv("VF_POOL_CAP", cap)
+        a, ad = g.search(Q, qoff, qlab, k=10, op="and", exact=True)
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), cap
