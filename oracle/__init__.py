@@ -114,8 +114,11 @@ class Index:
                                         _ptr(self.graph_off), _ptr(self.graph_ids))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().or_index_free(self._h)
+        if getattr(self, "_h", None) and lib is not None:     # module globals may be gone at exit
+            try:
+                lib().or_index_free(self._h)
+            except TypeError:
+                pass
             self._h = None
 
     def point_labels(self):

@@ -247,13 +247,16 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
 // A tile that overflows its piece list or the pool stays unfiltered (every row scanned): exact.
 constexpr int kFiltThreads = 256;
 constexpr int kFiltBuf = 4096;
+constexpr int kFiltUnion = 64;
 
 __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
     __shared__ int32_t buf[kFiltBuf];
     __shared__ int64_t q_off[kScanQG];
     __shared__ int32_t q_nl[kScanQG];
     __shared__ int32_t p_off[kMaxPieces], p_cnt[kMaxPieces];
-    __shared__ int s_tile, s_ok, s_n, s_np, s_bad, s_flush_off;
+    __shared__ int s_tile, s_ok, s_n, s_np, s_bad, s_flush_off, s_nu;
+    __shared__ int32_t s_u[kFiltUnion];           // union of the segment's other query labels, sorted
+    __shared__ unsigned long long s_qm[kScanQG];  // per query: its labels' bits in s_u
     const int ntiles = a.ctr->n_tiles;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&a.ctr->filter_next, 1);
@@ -278,13 +281,56 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
             __syncthreads();
             continue;
         }
+        // the segment's other labels -> bit positions (one thread; <= 64 distinct, else per-query
+        // verification); each query then passes iff its mask is a subset of the point's bits
+        if (threadIdx.x == 0) {
+            int nu = 0;
+            for (int g = 0; g < tl.nq && nu <= 64; g++)
+                for (int i = 0; i < q_nl[g] && nu <= 64; i++) {
+                    const int32_t l = a.qlab[q_off[g] + i];
+                    if (l == tl.label) continue;
+                    int j = nu;
+                    while (j > 0 && s_u[j - 1] > l) j--;
+                    if (j > 0 && s_u[j - 1] == l) continue;
+                    if (nu == kFiltUnion) { nu = 65; break; }
+                    for (int m = nu; m > j; m--) s_u[m] = s_u[m - 1];
+                    s_u[j] = l;
+                    nu++;
+                }
+            s_nu = nu;
+        }
+        __syncthreads();
+        const int nu = s_nu;
+        if (nu <= 64 && threadIdx.x < tl.nq) {
+            unsigned long long qm = 0;
+            for (int i = 0; i < q_nl[threadIdx.x]; i++) {
+                const int32_t l = a.qlab[q_off[threadIdx.x] + i];
+                for (int j = 0; j < nu; j++)
+                    if (s_u[j] == l) qm |= 1ull << j;
+            }
+            s_qm[threadIdx.x] = qm;
+        }
+        __syncthreads();
         for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads) {
             const int r = r0 + threadIdx.x;
             if (r < tl.row_end) {
                 const int32_t gid = __ldg(a.ix.M_hs + tl.base + r);
                 bool pass = false;
-                for (int g = 0; g < tl.nq && !pass; g++)
-                    pass = verify_pred(a.ix, gid, a.qlab + q_off[g], q_nl[g], tl.label);
+                if (nu <= 64) {
+                    const int64_t lo = __ldg(a.ix.pt_off + gid), hi = __ldg(a.ix.pt_off + gid + 1);
+                    unsigned long long bits = 0;
+                    for (int64_t e = lo; e < hi; e++) {
+                        const int32_t l = __ldg(a.ix.pt_lab + e);
+                        if (nu == 0 || l > s_u[nu - 1]) break;
+                        int b0 = 0, b1 = nu - 1;
+                        while (b0 < b1) { const int mid = (b0 + b1) >> 1; if (s_u[mid] < l) b0 = mid + 1; else b1 = mid; }
+                        if (s_u[b0] == l) bits |= 1ull << b0;
+                    }
+                    for (int g = 0; g < tl.nq && !pass; g++) pass = (bits & s_qm[g]) == s_qm[g];
+                } else {
+                    for (int g = 0; g < tl.nq && !pass; g++)
+                        pass = verify_pred(a.ix, gid, a.qlab + q_off[g], q_nl[g], tl.label);
+                }
                 if (pass) buf[atomicAdd(&s_n, 1)] = gid;
             }
             __syncthreads();

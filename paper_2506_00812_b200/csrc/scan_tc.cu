@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         ti.nq = 0;
         const TcQMeta *qm = qmeta;
         const uint32_t *qnp = qn;
-        int tp = 0;
+        int tp = 0, parts = 1;
         TP_DECL
         for (;;) {
             const int slot = n % nst;
@@ -547,8 +547,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 qm = qmeta + (size_t)tp * qg;
                 uint32_t *qnw = qn + (size_t)tp * qg;
                 const uint8_t *qsrc = qbuf + (size_t)tp * qg * row_bytes;
+                // few queries: P warps share a query, each keeping the top-k of every P-th
+                // 32-row word in a private list (merged at the tile's last stage)
+                parts = (k <= 32 && ti.nq <= 4 && a.tc_parts) ? (ti.nq == 1 ? 8 : ti.nq == 2 ? 4 : 2) : 1;
+                if (parts > 1 && e < ti.nq * parts)
+                    for (int t = lane; t < k; t += 32) lists[(size_t)e * k + t] = KEY_INF;
                 for (int g = e; g < ti.nq; g += kTcEpi) {
-                    for (int t = lane; t < k; t += 32) lists[(size_t)g * k + t] = KEY_INF;
+                    if (parts == 1)
+                        for (int t = lane; t < k; t += 32) lists[(size_t)g * k + t] = KEY_INF;
                     uint32_t s = 0;
                     const uint32_t *w = reinterpret_cast<const uint32_t *>(qsrc + (size_t)g * row_bytes);
                     for (int i = lane; i < row_bytes / 4; i += 32) s = sq_word<DT>(w[i], s);
@@ -616,6 +622,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             named_bar_sync(1, 32 * kTcEpi);
             TP_MARK(4)
             // (3) selection: the owner of query g inserts its surviving rows
+            if (parts > 1) {
+                if (e < nq * parts) {
+                    const int g = e / parts, part = e % parts;
+                    ull *L = lists + (size_t)e * k;
+                    const uint32_t *Dg = D + (size_t)g * kTcRows;
+                    ull Li = lane < k ? L[lane] : KEY_INF;
+                    for (int w4 = 0; w4 < 4; w4++) {
+                        if ((int)((n * 4 + w4) % parts) != part) continue;
+                        const uint32_t word = Mk[g * 4 + w4];
+                        if (!word) continue;
+                        const int r = w4 * 32 + lane;
+                        const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
+                        Li = warp_merge_topk(Li, key, k, lane);
+                    }
+                    if (lane < k) L[lane] = Li;
+                    const ull kth = __shfl_sync(FULL, Li, k - 1);
+                    if (lane == 0 && kth != KEY_INF) atomicMin(thr + g, kth);   // any part's k-th bounds
+                }
+                __syncwarp();
+            } else
             for (int g = e; g < nq; g += kTcEpi) {
                 ull *L = lists + (size_t)g * k;
                 const uint32_t *Dg = D + (size_t)g * kTcRows;
@@ -646,8 +672,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             TP_MARK(5)
             if (m.w & TS_LAST) {
                 const bool multi = ti.n_tiles > 1;
-                for (int g = e; g < nq; g += kTcEpi) {
-                    const ull *L = lists + (size_t)g * k;
+                if (parts > 1) {
+                    // every part's list is final: the warp of part 0 merges its query's parts
+                    named_bar_sync(1, 32 * kTcEpi);
+                    if (e < nq * parts && e % parts == 0) {
+                        ull Li = lists[(size_t)e * k + (lane < k ? lane : 0)];
+                        if (lane >= k) Li = KEY_INF;
+                        for (int q = 1; q < parts; q++) {
+                            const ull o = lane < k ? lists[(size_t)(e + q) * k + lane] : KEY_INF;
+                            Li = warp_merge_topk(Li, o, k, lane);
+                        }
+                        if (lane < k) lists[(size_t)e * k + lane] = Li;
+                    }
+                    // the other parts' lists are read above: nobody may reset them (next tile's
+                    // FIRST) before every merge is done
+                    named_bar_sync(1, 32 * kTcEpi);
+                }
+                for (int g = (parts > 1 ? (e % parts == 0 ? e / parts : nq) : e); g < nq;
+                     g += (parts > 1 ? nq : kTcEpi)) {
+                    const ull *L = lists + (size_t)(parts > 1 ? e : g) * k;
                     const int na = k <= 32 ? __popc(__ballot_sync(FULL, lane < k && L[lane < k ? lane : 0] != KEY_INF))
                                            : lcnt[g];
                     if (multi) {

@@ -509,6 +509,10 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0);
     a.pool = nullptr;
     a.pool_cap = 0;
+    {
+        const char *e = getenv("VF_TC_PARTS");
+        a.tc_parts = e ? atoi(e) : 1;
+    }
     pl.graph_ctas = graph_max_ctas(a);
     if (pl.graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
     size_t nwarp = (size_t)pl.graph_ctas * kWarpsPerGraphCta;

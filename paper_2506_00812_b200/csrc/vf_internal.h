@@ -180,6 +180,7 @@ struct SearchArgs {
     uint8_t *q8;              // u8 row store: k_prepare also writes the u8 query rows here
     int32_t q8_row_bytes;
     int32_t gate;             // 0 always run; 1 run iff !exact_fallback; 2 run iff exact_fallback
+    int32_t tc_parts;         // TC scan: split few-query tiles over several warps (VF_TC_PARTS=0 off)
     int32_t *pool;            // AND pre-filter survivor ids (k_hs_filter)
     int32_t pool_cap;
 };

@@ -192,3 +192,44 @@ def test_and_prefilter_pool_overflow_is_exact(vf, monkeypatch):
             monkeypatch.setenv("VF_POOL_CAP", cap)
         a, ad = g.search(Q, qoff, qlab, k=10, op="and", exact=True)
         assert (a == e).all() and (ad == ed.astype(np.float32)).all(), cap
+
+
+@pytest.mark.parametrize("per_label", [1, 2, 3, 4, 5])
+def test_u8_scan_few_queries_long_labels(vf, per_label):
+    """1-5 queries per label over labels of 600-4000 rows (many 128-row stages): the regime where
+    several epilogue warps share one query's rows (split selection, merged at the last stage)."""
+    dim = 128
+    X, off, ids = _u8_scan_index(dim, N=4000, seed=31)
+    g = vf.Index(X, off, ids, 1 << 30, 8)
+    o = oracle.Index(X, off, ids, 1 << 30, 8)
+    labels = [5, 6, 7, 8]                            # 600, 1024, 1500, 4000 rows
+    n = per_label * len(labels)
+    Q, qoff, _ = _queries(dim, n, [0], seed=per_label)
+    qlab = np.repeat(np.array(labels, np.int32), per_label)
+    for k in (1, 10, 32):
+        a, ad = g.search(Q, qoff, qlab, k=k, itopk=max(k, 16))
+        e, ed = o.exact_knn(Q, qoff, qlab, k=k)
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), (per_label, k)
+
+
+def test_u8_scan_mixed_query_group_sizes_exact_mode(vf):
+    """Consecutive tiles alternating between split (<= 4 queries) and unsplit query groups, long
+    labels, exact mode: the split lists are merged before any warp starts the next tile."""
+    dim = 64
+    rng = np.random.default_rng(17)
+    N = 30000
+    X = rng.integers(0, 256, size=(N, dim), dtype=np.uint8)
+    sizes = [9000, 5000, 12000, 700, 3000, 20000, 150]
+    ids = [np.sort(rng.choice(N, size=s_, replace=False)).astype(np.int32) for s_ in sizes]
+    off = np.zeros(len(sizes) + 1, np.int64)
+    off[1:] = np.cumsum(sizes)
+    ids = np.concatenate(ids)
+    g = vf.Index(X, off, ids, 1 << 30, 8)
+    o = oracle.Index(X, off, ids, 1 << 30, 8)
+    per = [1, 40, 2, 3, 70, 4, 9]                    # queries per label
+    qlab = np.repeat(np.arange(len(sizes), dtype=np.int32), per)
+    Q, qoff, _ = _queries(dim, len(qlab), [0], seed=23)
+    e, ed = o.exact_knn(Q, qoff, qlab, k=10)
+    for ex in (False, True):
+        a, ad = g.search(Q, qoff, qlab, k=10, itopk=16, exact=ex)
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), ex
