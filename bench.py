@@ -228,6 +228,7 @@ def main():
     Q = torch.from_numpy(w.Q).to(dev)
     qo = torch.from_numpy(w.q_off).to(dev)
     ql = torch.from_numpy(w.q_lab).to(dev)
+    n_ql = int(w.q_off[-1])            # = len(q_lab): lets vf_search skip reading q_off[n] back
     ids = torch.empty((n, k), dtype=torch.int32, device=dev)
     dd = torch.empty((n, k), dtype=torch.float32, device=dev)
 
@@ -261,7 +262,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
             e1.record(stream)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
@@ -274,7 +275,7 @@ def main():
             if itopk < k:
                 continue
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
             torch.cuda.synchronize()
             r_strict, r_tie = recall_vs(ids[:m_gt].cpu().numpy(), dd[:m_gt].cpu().numpy(), gt, gd, k)
             qms = quick_ms(itopk, w_, as_)
@@ -299,7 +300,7 @@ def main():
         """W warm-up + exactly K timed steps; per-step CUDA events around vf_search only."""
         for _ in range(args.warmup):
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         stats = []
@@ -309,10 +310,12 @@ def main():
             flush.fill_(float(i))
             ev[i][0].record(stream)
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
             ev[i][1].record(stream)
-            stats.append(ix.last_stats(stream))   # syncs; between steps, outside the events
+        # no host sync inside the loop: the host enqueues step i+1 while the device runs step i,
+        # so the events time the device work (host-side cost is what `e2e` measures)
         torch.cuda.synchronize()
+        stats.append(ix.last_stats(stream))       # phases + work counters of the last step
         barrier()
         ms = [a.elapsed_time(b) for a, b in ev]
         return ms, stats
@@ -344,14 +347,14 @@ def main():
         odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
         for _ in range(args.warmup):
             ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
             ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
         e1.record(stream)
         torch.cuda.synchronize()
         et = e0.elapsed_time(e1)
@@ -390,7 +393,7 @@ def main():
                                        and_scan_threshold=as_, stream=stream)
                     else:
                         ix.search_into(Qd, qod, qld, oid, odd, k=k, itopk=itopk, search_width=w_, op=op,
-                                       and_scan_threshold=as_, stream=stream)
+                                       and_scan_threshold=as_, stream=stream, n_query_labels=int(w.q_off[bsz]))
                         stream.synchronize()
                     if it_ >= 50:
                         ts.append(time.perf_counter() - t0)

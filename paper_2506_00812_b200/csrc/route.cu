@@ -177,18 +177,28 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
         const LabelDir d = a.ix.dir[it.label];
         const int count = a.ls_count[d.bslot];
         const int nseg = (count + qg - 1) / qg;
-        const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
+        // tiles per segment: small query groups on short lists are cut into kWarpTileRows-row tiles
+        // for the warp-per-tile scan (load balance); everything else uses tile_rows
+        auto seg_rows = [&](int g) {
+            const int nq = min(qg, count - g * qg);
+            return (a.split_tiles && nq <= kWarpScanQ && d.size <= kWarpScanRows) ? kWarpTileRows : a.tile_rows;
+        };
+        int total = 0;
+        for (int g = 0; g < nseg; g++) total += (d.size + seg_rows(g) - 1) / seg_rows(g);
         const int seg0 = atomicAdd(&a.ctr->n_segs, nseg);
         const int ib = atomicAdd(&a.ctr->n_scan_items, count);
-        const int tb = atomicAdd(&a.ctr->n_tiles, nseg * ntile);
+        int tb = atomicAdd(&a.ctr->n_tiles, total);
         a.ls_segbase[d.bslot] = seg0;
         a.ls_itembase[d.bslot] = ib;
         for (int g = 0; g < nseg; g++) {
+            const int tr = seg_rows(g);
+            const int ntile = (d.size + tr - 1) / tr;
+            const bool warp_tiles = tr == kWarpTileRows && a.split_tiles;
             Segment sg;
             sg.label = it.label;
             sg.item_base = ib + g * qg;
             sg.n_items = min(qg, count - g * qg);
-            sg.tile_base = tb + g * ntile;
+            sg.tile_base = tb;
             sg.n_tiles = ntile;
             sg.pad[0] = sg.pad[1] = sg.pad[2] = 0;
             a.segs[seg0 + g] = sg;
@@ -196,8 +206,8 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 Tile tl;
                 tl.base = d.base;
                 tl.seg = seg0 + g;
-                tl.row_begin = t * a.tile_rows;
-                tl.row_end = min(d.size, (t + 1) * a.tile_rows);
+                tl.row_begin = t * tr;
+                tl.row_end = min(d.size, (t + 1) * tr);
                 tl.tile_in_seg = t;
                 tl.label = it.label;
                 tl.nq = sg.n_items;
@@ -206,8 +216,13 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 tl.hs = d.size >= a.ix.T;
                 tl.pad = 0;
                 tl.n_pieces = -1;
-                a.tiles[tb + g * ntile + t] = tl;
+                a.tiles[tb + t] = tl;
+                if (a.split_tiles) {
+                    if (warp_tiles) a.wtiles[atomicAdd(&a.ctr->n_wtiles, 1)] = tb + t;
+                    else a.btiles[atomicAdd(&a.ctr->n_btiles, 1)] = tb + t;
+                }
             }
+            tb += ntile;
         }
     }
 }
@@ -221,7 +236,7 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
         const int seg = a.ls_segbase[d.bslot] + it.rank / qg;
         a.scan_slots[a.ls_itembase[d.bslot] + it.rank] = (int32_t)s;
         a.item_seg[s] = seg;
-        const int ntile = (d.size + a.tile_rows - 1) / a.tile_rows;
+        const int ntile = a.segs[seg].n_tiles;     // written by k_segments
         if (ntile > 1) {
             it.meta |= META_MULTI;       // finalised in the scan kernel (last tile done)
             a.items[s] = it;

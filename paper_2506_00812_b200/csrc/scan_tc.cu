@@ -10,7 +10,7 @@
 // 2^24), so the query-group x row-tile dot products are one tcgen05.mma.kind::i8 per 32-byte K
 // step (M = 128 rows, N = the segment's queries padded to 16), accumulated exactly in TMEM.
 //
-// 352 threads, warp-specialised:
+// 352 threads, warp-specialised (an epilogue and a selection group pipelined through mbarriers):
 //   warp 10 tile scheduler: claims tiles and resolves their metadata into a double-buffered tile
 //           slot ahead of the producer (no global round trip between consecutive tiles' stages).
 //   warp 0  producer: claims tiles, prefetches the segment's query rows + metadata (double buffer
@@ -21,12 +21,13 @@
 //   warp 1  MMA: owns the TMEM allocation (2 accumulator buffers); per tile it converts the query
 //           rows into the swizzled B operand, per stage one elected lane issues the K-step MMAs
 //           and commits them to the accumulator's mbarrier.
-//   warps 2-9 epilogue + selection: a warp reads its TMEM lane quarter (32 rows) for half of the
-//           query columns, forms exact distances, drops every (row, query) pair whose key is not
-//           below the query's current k-th key (a stale threshold only lets more through) or that
-//           fails the AND predicate, and publishes survivors as per-query 128-bit masks; after one
-//           named barrier the warp owning each query inserts only the surviving rows into that
-//           query's register-resident top-k list. Multi-tile segments are finished as in k_scan.
+//   warps 2-5 epilogue: a warp reads its TMEM lane quarter (32 rows) for every query column,
+//           forms exact distances, drops every (row, query) pair whose key is not below the
+//           query's current k-th key (a stale threshold only lets more through) or that fails the
+//           AND predicate, and publishes survivors as per-query 128-bit masks (double-buffered).
+//   warps 6-9 selection: the warp owning a query inserts only its surviving rows into the
+//           query's register-resident top-k list while the epilogue works on the next stage.
+//           Multi-tile segments are finished as in k_scan.
 #include <cuda.h>
 #include <cstdio>
 #include "common.cuh"
@@ -36,7 +37,8 @@ namespace vf {
 namespace {
 
 constexpr int kTcThreads = 352;
-constexpr int kTcEpi = 8;             // epilogue warps
+constexpr int kTcEpiW = 4;            // epilogue warps (one per TMEM lane quarter)
+constexpr int kTcSelW = 4;            // selection warps
 constexpr int kTcRows = 128;          // rows per stage = MMA M
 enum : int { TS_FIRST = 1, TS_LAST = 2, TS_END = 4 };
 
@@ -57,13 +59,16 @@ struct TcTInfo {
 }  // namespace
 
 struct TcLayout {
-    int nst, qg, k, row_bytes, cw, nch, kpad, nmax, tmem_cols;
+    int nst, qg, k, row_bytes, cw, nch, kpad, nmax, tmem_cols, ctas;
     size_t off_bar, off_misc, off_meta, off_tinfo, off_rows, off_sid, off_snorm, off_qbuf, off_bsm, off_qmeta,
-        off_qn, off_thr, off_lists, off_lcnt, off_scratch, off_dist, off_gid, off_mask, total;
+        off_qn, off_thr, off_lists, off_lcnt, off_scratch, off_dist, off_gid, off_mask, off_sinfo, total;
 };
 
-static TcLayout tc_layout(int row_bytes, int k) {
+constexpr int kTcCtasPerSm = 2;       // up to two independent pipelines per SM (latency-bound chains)
+
+static TcLayout tc_layout_for(int row_bytes, int k, int ctas) {
     TcLayout L{};
+    L.ctas = ctas;
     L.row_bytes = row_bytes;
     L.k = k;
     L.cw = row_bytes % 128 == 0 ? 128 : row_bytes % 64 == 0 ? 64 : 32;
@@ -73,15 +78,15 @@ static TcLayout tc_layout(int row_bytes, int k) {
     auto stages_for = [&](int qg) {
         const size_t nmax = (size_t)(qg + 15) / 16 * 16;
         const size_t fixed = 2048 + 2 * (size_t)qg * row_bytes + 2 * (size_t)L.nch * nmax * L.cw + 2 * (size_t)qg * 32 +
-                             2 * (size_t)qg * 4 + (size_t)qg * 8 + (size_t)qg * k * 8 + (size_t)qg * 4 +
-                             (size_t)kTcEpi * (32 + 2 * k) * 8 + 2 * (size_t)qg * kTcRows * 4 + 2 * kTcRows * 4 +
+                             2 * (size_t)qg * 4 + 2 * (size_t)qg * 8 + 2 * (size_t)qg * k * 8 + 2 * (size_t)qg * 4 +
+                             (size_t)kTcSelW * (32 + 2 * k) * 8 + 2 * (size_t)qg * kTcRows * 4 + 2 * kTcRows * 4 +
                              2 * (size_t)qg * 16 + 4096;
-        const size_t budget = 225 * 1024;
+        const size_t budget = (227 * 1024) / ctas - 2048;
         return fixed >= budget ? 0 : (int)((budget - fixed) / (stage + 2 * kTcRows * 4));
     };
-    // queries per segment: as many as keep >= 3 row stages in flight (>= 2 for wide fp32 rows)
+    // queries per segment: as many as keep >= 3 row stages in flight per CTA (>= 2 for wide rows)
     int qg = kScanQG;
-    while (qg > 16 && ((size_t)qg * k * 8 > 16 * 1024 || (size_t)qg * row_bytes > 16 * 1024 || stages_for(qg) < 3))
+    while (qg > 16 && ((size_t)qg * k * 8 > 8 * 1024 || (size_t)qg * row_bytes > 8 * 1024 || stages_for(qg) < 3))
         qg >>= 1;
     L.qg = qg;
     L.nmax = (qg + 15) / 16 * 16;
@@ -98,8 +103,9 @@ static TcLayout tc_layout(int row_bytes, int k) {
         o += bytes;
         return r;
     };
-    L.off_bar = take(8 * (2 * (size_t)nst + 10), 8);
+    L.off_bar = take(8 * (2 * (size_t)nst + 16), 8);
     L.off_misc = take(16, 16);
+    L.off_sinfo = take(2 * 16, 16);
     L.off_meta = take(16 * (size_t)nst, 16);
     L.off_tinfo = take(2 * sizeof(TcTInfo), 16);
     L.off_rows = take(stage * nst, 1024);
@@ -109,15 +115,22 @@ static TcLayout tc_layout(int row_bytes, int k) {
     L.off_qbuf = take(2 * (size_t)qg * row_bytes, 16);
     L.off_qmeta = take(2 * (size_t)qg * sizeof(TcQMeta), 16);
     L.off_qn = take(2 * (size_t)qg * 4, 16);
-    L.off_thr = take((size_t)qg * 8, 16);
-    L.off_lists = take((size_t)qg * k * 8, 16);
-    L.off_lcnt = take((size_t)qg * 4, 16);
-    L.off_scratch = take((size_t)kTcEpi * (32 + 2 * k) * 8, 16);
+    L.off_thr = take(2 * (size_t)qg * 8, 16);           // per tile parity
+    L.off_lists = take(2 * (size_t)qg * k * 8, 16);
+    L.off_lcnt = take(2 * (size_t)qg * 4, 16);
+    L.off_scratch = take((size_t)kTcSelW * (32 + 2 * k) * 8, 16);
     L.off_dist = take(2 * (size_t)qg * kTcRows * 4, 16);
     L.off_gid = take(2 * (size_t)kTcRows * 4, 16);
     L.off_mask = take(2 * (size_t)qg * 16, 16);
     L.total = o + 1024;     // slack for aligning the dynamic window to 1024 bytes
+    if (L.total > (size_t)(227 * 1024) / ctas) L.nst = 0;
     return L;
+}
+
+// two CTAs per SM when the row size leaves >= 2 stages each, else one (nst < 2: k_scan instead)
+static TcLayout tc_layout(int row_bytes, int k) {
+    const TcLayout L2 = tc_layout_for(row_bytes, k, 2);
+    return L2.nst >= 2 ? L2 : tc_layout_for(row_bytes, k, 1);
 }
 
 int scan_tc_qg(int row_bytes, int k) {
@@ -220,6 +233,50 @@ __device__ __forceinline__ uint32_t swz(int r, int u, int cw) {
 #define TP_DUMP(name)
 #endif
 
+// position of the j-th (0-based) set bit of w (j < popc(w)): binary search on popcounts
+__device__ __forceinline__ int nth_bit(uint32_t w, int j) {
+    int pos = 0;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {
+        const int c = __popc(w & ((1u << sh) - 1));
+        if (j >= c) { j -= c; w >>= sh; pos += sh; }
+    }
+    return pos;
+}
+
+// The survivors of one 128-row stage for one query, compacted: candidate c (c < popc(mask & wsel))
+// of the stage's four 32-row words lands in lane c (lanes past the count get KEY_INF). Words not
+// selected by `wsel` (bit w4) belong to another warp. Returns the number of candidates.
+__device__ __forceinline__ int stage_candidates(const uint32_t *Mk4, unsigned wsel, const uint32_t *Dg,
+                                                const int32_t *Gd, int base, int lane, ull &key) {
+    const uint4 mw = *reinterpret_cast<const uint4 *>(Mk4);
+    const uint32_t w0 = (wsel & 1) ? mw.x : 0u, w1 = (wsel & 2) ? mw.y : 0u;
+    const uint32_t w2 = (wsel & 4) ? mw.z : 0u, w3 = (wsel & 8) ? mw.w : 0u;
+    const int c0 = __popc(w0), c1 = c0 + __popc(w1), c2 = c1 + __popc(w2), c3 = c2 + __popc(w3);
+    const int c = base + lane;
+    key = KEY_INF;
+    if (c < c3) {
+        int r;
+        if (c < c0) r = nth_bit(w0, c);
+        else if (c < c1) r = 32 + nth_bit(w1, c - c0);
+        else if (c < c2) r = 64 + nth_bit(w2, c - c1);
+        else r = 96 + nth_bit(w3, c - c2);
+        key = ((ull)Dg[r] << 32) | (uint32_t)Gd[r];
+    }
+    return c3;
+}
+
+// Out-of-line copies of the large warp helpers: eleven warps in five roles share one instruction
+// cache, and inlining these (bitonic networks, binary searches) at every call site tripled the
+// kernel's code size (ncu: no_instructions stalls).
+__device__ __noinline__ ull merge_topk_ol(ull Li, ull key, int k, int lane) {
+    return warp_merge_topk(Li, key, k, lane);
+}
+__device__ __noinline__ bool verify_pred_ol(const DevIndex &ix, int32_t gid, const int32_t *P, int np,
+                                            int32_t excl) {
+    return verify_pred(ix, gid, P, np, excl);
+}
+
 __device__ __forceinline__ void write_final_tc(const SearchArgs &a, const TcQMeta &q, const ull *L, int n, int k,
                                                int lane) {
     for (int t = lane; t < k; t += 32) {
@@ -233,7 +290,7 @@ __device__ __forceinline__ void write_final_tc(const SearchArgs &a, const TcQMet
     }
 }
 
-__device__ __forceinline__ void topk_update_tc(ull *L, int *cnt_p, ull key, int k, ull *cbuf, ull *tmp, int lane) {
+__device__ __noinline__ void topk_update_tc(ull *L, int *cnt_p, ull key, int k, ull *cbuf, ull *tmp, int lane) {
     const int cnt = *cnt_p;
     const ull thr = cnt < k ? KEY_INF : L[k - 1];
     const bool take = key < thr;
@@ -250,7 +307,7 @@ __device__ __forceinline__ void topk_update_tc(ull *L, int *cnt_p, ull key, int 
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
     k_scan_tc(SearchArgs a, TcLayout SL, const __grid_constant__ CUtensorMap tm_ls,
               const __grid_constant__ CUtensorMap tm_x) {
     extern __shared__ uint8_t smem_raw[];
@@ -260,7 +317,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + SL.off_bar);
     uint64_t *full = bars, *empty = bars + nst;
     uint64_t *qfull = bars + 2 * nst, *qempty = qfull + 2, *accfull = qfull + 4, *accempty = qfull + 6;
-    uint64_t *tready = qfull + 8;
+    uint64_t *tready = qfull + 8, *dready = qfull + 10, *dfree = qfull + 12, *tfree = qfull + 14;
+    int4 *sinfo = reinterpret_cast<int4 *>(smem + SL.off_sinfo);
     uint32_t *misc = reinterpret_cast<uint32_t *>(smem + SL.off_misc);   // [0] TMEM base, [1] flag
     int4 *meta = reinterpret_cast<int4 *>(smem + SL.off_meta);
     TcTInfo *tinfo = reinterpret_cast<TcTInfo *>(smem + SL.off_tinfo);
@@ -287,14 +345,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
             mbar_init(full + i, 1);
-            mbar_init(empty + i, kTcEpi);
+            mbar_init(empty + i, kTcEpiW);
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(qfull + i, 1);
-            mbar_init(qempty + i, kTcEpi);
+            mbar_init(qempty + i, kTcSelW);
             mbar_init(accfull + i, 1);
-            mbar_init(accempty + i, kTcEpi);
+            mbar_init(accempty + i, kTcEpiW);
             mbar_init(tready + i, 1);
+            mbar_init(dready + i, kTcEpiW);
+            mbar_init(dfree + i, kTcSelW);
+            mbar_init(tfree + i, kTcSelW);
         }
         fence_mbar_init();
     }
@@ -303,6 +364,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      "r"(SL.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    for (int i = threadIdx.x; i < 2 * qg * k; i += kTcThreads) lists[i] = KEY_INF;
+    for (int i = threadIdx.x; i < 2 * qg; i += kTcThreads) { thr[i] = KEY_INF; lcnt[i] = 0; }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -314,7 +377,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // the tile slot of its parity ahead of the producer, so no dependent global round trip sits
         // between one tile's last row stage and the next tile's first.
         uint32_t tc = 0;
-        const int ntiles = a.ctr->n_tiles;
+        const int ntiles = a.split_tiles ? a.ctr->n_btiles : a.ctr->n_tiles;
         for (;;) {
             const int tp = tc & 1;
             if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
@@ -322,7 +385,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             int t = 0;
             if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
             t = __shfl_sync(FULL, t, 0);
-            if (t >= ntiles) {
+            if (t < ntiles && a.split_tiles) t = a.btiles[t];
+            else if (t >= ntiles) t = INT32_MAX;
+            if (t == INT32_MAX) {
                 if (lane == 0) {
                     tinfo[tp].tile = -1;
                     mbar_arrive(tready + tp);
@@ -516,92 +581,93 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             n++;
         }
         TP_DUMP("mma(full,accempty,first,issue,other)")
-    } else {
-        // ------------------------------------------------------------ epilogue + selection
-        const int e = warp - 2;               // 0..7
-        const int quarter = warp & 3;         // TMEM lanes 32*quarter .. +31
-        const int half = e >> 2;
+    } else if (warp < 2 + kTcEpiW) {
+        // ------------------------------------------------------------ epilogue (4 warps)
+        // Warp w owns TMEM lane quarter w & 3 (rows 32q .. 32q+31 of the stage) for every query
+        // column; it hands each stage to the selection warps through dready / dfree and never waits
+        // for their top-k work (the D buffers are double-buffered).
+        const int e = warp - 2;                       // 0..3
+        const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
-        ull *cbuf = scratch + (size_t)e * (32 + 2 * k);
-        ull *tmp = cbuf + 32;
-        ull *fin2 = tmp + k;
         unsigned long long my_rows = 0, my_qrows = 0;
         uint32_t n = 0, tc = 0;
         TcTInfo ti;
         ti.nq = 0;
         const TcQMeta *qm = qmeta;
         const uint32_t *qnp = qn;
-        int tp = 0, parts = 1;
+        const ull *thrp = thr;
+        int tp = 0;
+        uint32_t first_n = 0;
         TP_DECL
         for (;;) {
             const int slot = n % nst;
+            const int buf = n & 1;
             TP_MARK(7)
             mbar_wait(full + slot, (n / nst) & 1);
             TP_MARK(0)
             const int4 m = meta[slot];
-            if (m.w & TS_END) break;
+            if (m.w & TS_END) {
+                mbar_wait(dfree + buf, ((n >> 1) & 1) ^ 1);
+                if (e == 0 && lane == 0) sinfo[buf] = make_int4(0, TS_END, tp, 0);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(dready + buf);
+                break;
+            }
             if (m.w & TS_FIRST) {
                 tp = tc & 1;
+                first_n = n;
                 mbar_wait(qfull + tp, (tc >> 1) & 1);
                 ti = tinfo[tp];
                 qm = qmeta + (size_t)tp * qg;
+                // this parity's thresholds were reset by the selection warps after the tile two back
+                mbar_wait(tfree + tp, ((tc >> 1) & 1) ^ 1);
                 uint32_t *qnw = qn + (size_t)tp * qg;
                 const uint8_t *qsrc = qbuf + (size_t)tp * qg * row_bytes;
-                // few queries: P warps share a query, each keeping the top-k of every P-th
-                // 32-row word in a private list (merged at the tile's last stage)
-                parts = (k <= 32 && ti.nq <= 4 && a.tc_parts) ? (ti.nq == 1 ? 8 : ti.nq == 2 ? 4 : 2) : 1;
-                if (parts > 1 && e < ti.nq * parts)
-                    for (int t = lane; t < k; t += 32) lists[(size_t)e * k + t] = KEY_INF;
-                for (int g = e; g < ti.nq; g += kTcEpi) {
-                    if (parts == 1)
-                        for (int t = lane; t < k; t += 32) lists[(size_t)g * k + t] = KEY_INF;
+                for (int g = e; g < ti.nq; g += kTcEpiW) {
                     uint32_t s = 0;
                     const uint32_t *w = reinterpret_cast<const uint32_t *>(qsrc + (size_t)g * row_bytes);
                     for (int i = lane; i < row_bytes / 4; i += 32) s = sq_word<DT>(w[i], s);
 #pragma unroll
                     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-                    if (lane == 0) {
-                        qnw[g] = s;
-                        thr[g] = KEY_INF;
-                        lcnt[g] = 0;
-                    }
+                    if (lane == 0) qnw[g] = s;
                 }
                 qnp = qnw;
-                named_bar_sync(1, 32 * kTcEpi);
+                thrp = thr + (size_t)tp * qg;
+                named_bar_sync(2, 32 * kTcEpiW);       // every query norm of the tile is in place
+                tc++;
                 TP_MARK(1)
             }
             const int nq = ti.nq, nr = m.z;
-            const int buf = n & 1;
-            const int npad = max(16, (nq + 15) & ~15);
             uint32_t *D = dtile + (size_t)buf * qg * kTcRows;
             int32_t *Gd = gtile + (size_t)buf * kTcRows;
             uint32_t *Mk = mask + (size_t)buf * qg * 4;
-            // (1) accumulators -> exact distances -> threshold / predicate filter
-            TP_MARK(7)
+            mbar_wait(dfree + buf, ((n >> 1) & 1) ^ 1);    // the selection is done with stage n-2
+            if (n == first_n + 1)                          // ... and, for the tile's second stage, with
+                mbar_wait(dfree + (buf ^ 1), ((n - 1) >> 1) & 1);   // its first: thresholds are real
+            TP_MARK(6)
             mbar_wait(accfull + buf, (n >> 1) & 1);
             TP_MARK(2)
             tc_fence_after();
             const bool valid = row < nr;
             const int32_t gid = sid[(size_t)slot * kTcRows + row];
             const int32_t xn = (int32_t)snorm[(size_t)slot * kTcRows + row];
-            if (half == 0) Gd[row] = valid ? gid : -1;
-            const int c_lo = half * (npad >> 1), c_hi = min(nq, (half + 1) * (npad >> 1));
-            for (int c0 = c_lo; c0 < c_hi; c0 += 8) {
+            Gd[row] = valid ? gid : -1;
+            for (int c0 = 0; c0 < nq; c0 += 8) {
                 uint32_t v[8];
                 tmem_ld8(tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * nmax + c0), v);
                 tmem_wait_ld();
 #pragma unroll
                 for (int j = 0; j < 8; j++) {
                     const int g = c0 + j;
-                    if (g < c_hi) {
+                    if (g < nq) {
                         const int32_t dot = DT == 0 ? (int32_t)v[j] : __float2int_rn(__uint_as_float(v[j]));
                         const int32_t d = xn + (int32_t)qnp[g] - 2 * dot;
                         const uint32_t bits = __float_as_uint((float)d);
                         const ull key = ((ull)bits << 32) | (uint32_t)gid;
-                        bool pass = valid && key < thr[g];
+                        bool pass = valid && key < thrp[g];
                         if (pass) {
                             const TcQMeta &qq = qm[g];
-                            if ((qq.meta & META_PRED) && !verify_pred(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
+                            if ((qq.meta & META_PRED) && !verify_pred_ol(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
                                 pass = false;
                         }
                         if (pass) D[(size_t)g * kTcRows + row] = bits;
@@ -615,84 +681,138 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) {
                 mbar_arrive(accempty + buf);
                 mbar_arrive(empty + slot);
+                if (e == 0) sinfo[buf] = make_int4(nr, m.w, tp, 0);
+                mbar_arrive(dready + buf);
             }
             if (threadIdx.x == 64) { my_rows += nr; my_qrows += (unsigned long long)nr * nq; }
             TP_MARK(3)
-            // (2) the survivor masks and distances of this stage are complete
-            named_bar_sync(1, 32 * kTcEpi);
-            TP_MARK(4)
-            // (3) selection: the owner of query g inserts its surviving rows
-            if (parts > 1) {
-                if (e < nq * parts) {
-                    const int g = e / parts, part = e % parts;
-                    ull *L = lists + (size_t)e * k;
-                    const uint32_t *Dg = D + (size_t)g * kTcRows;
-                    ull Li = lane < k ? L[lane] : KEY_INF;
-                    for (int w4 = 0; w4 < 4; w4++) {
-                        if ((int)((n * 4 + w4) % parts) != part) continue;
-                        const uint32_t word = Mk[g * 4 + w4];
-                        if (!word) continue;
-                        const int r = w4 * 32 + lane;
-                        const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
-                        Li = warp_merge_topk(Li, key, k, lane);
-                    }
-                    if (lane < k) L[lane] = Li;
-                    const ull kth = __shfl_sync(FULL, Li, k - 1);
-                    if (lane == 0 && kth != KEY_INF) atomicMin(thr + g, kth);   // any part's k-th bounds
-                }
-                __syncwarp();
-            } else
-            for (int g = e; g < nq; g += kTcEpi) {
-                ull *L = lists + (size_t)g * k;
-                const uint32_t *Dg = D + (size_t)g * kTcRows;
-                if (k <= 32) {
-                    ull Li = lane < k ? L[lane] : KEY_INF;
-                    for (int w4 = 0; w4 < 4; w4++) {
-                        const uint32_t word = Mk[g * 4 + w4];
-                        if (!word) continue;
-                        const int r = w4 * 32 + lane;
-                        const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
-                        Li = warp_merge_topk(Li, key, k, lane);
-                    }
-                    if (lane < k) L[lane] = Li;
-                    const ull kth = __shfl_sync(FULL, Li, k - 1);
-                    if (lane == 0) thr[g] = kth;
+            n++;
+        }
+        if (warp == 2) { TP_DUMP("epi(full,first,accfull,compute,-,-,dfree,other)") }
+        if (threadIdx.x == 64 && my_rows) {
+            atomicAdd(&a.ctr->scan_rows, my_rows);
+            atomicAdd(&a.ctr->scan_qrows, my_qrows);
+        }
+    } else {
+        // ------------------------------------------------------------ selection (4 warps)
+        // The warp owning query g (g = sw mod 4) merges each stage's survivors into the query's
+        // register-resident top-k and tightens its threshold; a tile with 1-2 queries splits each
+        // query's 32-row words over 2-4 warps (private lists, atomicMin thresholds, merged at the
+        // tile's last stage). After a tile this parity's lists / thresholds are reset for the tile
+        // two ahead (tfree) and its query slot released (qempty).
+        const int sw = warp - 2 - kTcEpiW;            // 0..3
+        ull *cbuf = scratch + (size_t)sw * (32 + 2 * k);
+        ull *tmp = cbuf + 32;
+        ull *fin2 = tmp + k;
+        uint32_t n = 0;
+        int tp = 0, parts = 1, nq = 0;
+        TcTInfo ti;
+        ti.nq = 0;
+        const TcQMeta *qm = qmeta;
+        ull *L0 = lists, *thr0 = thr;
+        int *lc0 = lcnt;
+        TP_DECL
+        for (;;) {
+            const int buf = n & 1;
+            TP_MARK(7)
+            mbar_wait(dready + buf, (n >> 1) & 1);
+            TP_MARK(0)
+            const int4 si = sinfo[buf];               // (rows, flags, tile parity)
+            if (si.y & TS_END) break;
+            if (si.y & TS_FIRST) {
+                tp = si.z;
+                ti = tinfo[tp];
+                nq = ti.nq;
+                qm = qmeta + (size_t)tp * qg;
+                parts = (k <= 32 && nq <= 2 && a.tc_parts) ? (nq == 1 ? 4 : 2) : 1;
+                L0 = lists + (size_t)tp * qg * k;
+                thr0 = thr + (size_t)tp * qg;
+                lc0 = lcnt + (size_t)tp * qg;
+                // the lists this warp will use in this tile start empty
+                if (parts > 1) {
+                    if (sw < nq * parts && lane < k) L0[(size_t)sw * k + lane] = KEY_INF;
                 } else {
-                    for (int w4 = 0; w4 < 4; w4++) {
-                        const uint32_t word = Mk[g * 4 + w4];
-                        if (!word) continue;
-                        const int r = w4 * 32 + lane;
-                        const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
-                        topk_update_tc(L, lcnt + g, key, k, cbuf, tmp, lane);
+                    for (int g = sw; g < nq; g += kTcSelW) {
+                        for (int t = lane; t < k; t += 32) L0[(size_t)g * k + t] = KEY_INF;
+                        if (lane == 0) lc0[g] = 0;
                     }
-                    if (lane == 0) thr[g] = lcnt[g] >= k ? L[k - 1] : KEY_INF;
                 }
                 __syncwarp();
             }
-            TP_MARK(5)
-            if (m.w & TS_LAST) {
+            const uint32_t *D = dtile + (size_t)buf * qg * kTcRows;
+            const int32_t *Gd = gtile + (size_t)buf * kTcRows;
+            const uint32_t *Mk = mask + (size_t)buf * qg * 4;
+            if (parts > 1) {
+                if (sw < nq * parts) {
+                    const int g = sw / parts, part = sw % parts;
+                    ull *L = L0 + (size_t)sw * k;
+                    const uint32_t *Dg = D + (size_t)g * kTcRows;
+                    ull Li = lane < k ? L[lane] : KEY_INF;
+                    unsigned wsel = 0;
+                    for (int w4 = 0; w4 < 4; w4++)
+                        if ((int)((n * 4 + w4) % parts) == part) wsel |= 1u << w4;
+                    for (int base = 0;; base += 32) {
+                        ull key;
+                        const int nc = stage_candidates(Mk + g * 4, wsel, Dg, Gd, base, lane, key);
+                        if (base >= nc) break;
+                        Li = merge_topk_ol(Li, key, k, lane);
+                    }
+                    if (lane < k) L[lane] = Li;
+                    const ull kth = __shfl_sync(FULL, Li, k - 1);
+                    if (lane == 0 && kth != KEY_INF) atomicMin(thr0 + g, kth);   // any part's k-th bounds
+                }
+            } else {
+                for (int g = sw; g < nq; g += kTcSelW) {
+                    ull *L = L0 + (size_t)g * k;
+                    const uint32_t *Dg = D + (size_t)g * kTcRows;
+                    if (k <= 32) {
+                        ull Li = lane < k ? L[lane] : KEY_INF;
+                        for (int base = 0;; base += 32) {
+                            ull key;
+                            const int nc = stage_candidates(Mk + g * 4, 0xFu, Dg, Gd, base, lane, key);
+                            if (base >= nc) break;
+                            Li = merge_topk_ol(Li, key, k, lane);
+                        }
+                        if (lane < k) L[lane] = Li;
+                        const ull kth = __shfl_sync(FULL, Li, k - 1);
+                        if (lane == 0) thr0[g] = kth;
+                    } else {
+                        for (int w4 = 0; w4 < 4; w4++) {
+                            const uint32_t word = Mk[g * 4 + w4];
+                            if (!word) continue;
+                            const int r = w4 * 32 + lane;
+                            const ull key = (word >> lane) & 1 ? (((ull)Dg[r] << 32) | (uint32_t)Gd[r]) : KEY_INF;
+                            topk_update_tc(L, lc0 + g, key, k, cbuf, tmp, lane);
+                        }
+                        if (lane == 0) thr0[g] = lc0[g] >= k ? L[k - 1] : KEY_INF;
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dfree + buf);
+            TP_MARK(1)
+            if (si.y & TS_LAST) {
                 const bool multi = ti.n_tiles > 1;
                 if (parts > 1) {
                     // every part's list is final: the warp of part 0 merges its query's parts
-                    named_bar_sync(1, 32 * kTcEpi);
-                    if (e < nq * parts && e % parts == 0) {
-                        ull Li = lists[(size_t)e * k + (lane < k ? lane : 0)];
+                    named_bar_sync(3, 32 * kTcSelW);
+                    if (sw < nq * parts && sw % parts == 0) {
+                        ull Li = L0[(size_t)sw * k + (lane < k ? lane : 0)];
                         if (lane >= k) Li = KEY_INF;
                         for (int q = 1; q < parts; q++) {
-                            const ull o = lane < k ? lists[(size_t)(e + q) * k + lane] : KEY_INF;
-                            Li = warp_merge_topk(Li, o, k, lane);
+                            const ull o = lane < k ? L0[(size_t)(sw + q) * k + lane] : KEY_INF;
+                            Li = merge_topk_ol(Li, o, k, lane);
                         }
-                        if (lane < k) lists[(size_t)e * k + lane] = Li;
+                        if (lane < k) L0[(size_t)sw * k + lane] = Li;
                     }
-                    // the other parts' lists are read above: nobody may reset them (next tile's
-                    // FIRST) before every merge is done
-                    named_bar_sync(1, 32 * kTcEpi);
+                    named_bar_sync(3, 32 * kTcSelW);   // no list is reset before every merge is done
                 }
-                for (int g = (parts > 1 ? (e % parts == 0 ? e / parts : nq) : e); g < nq;
-                     g += (parts > 1 ? nq : kTcEpi)) {
-                    const ull *L = lists + (size_t)(parts > 1 ? e : g) * k;
+                for (int g = (parts > 1 ? (sw % parts == 0 ? sw / parts : nq) : sw); g < nq;
+                     g += (parts > 1 ? nq : kTcSelW)) {
+                    const ull *L = L0 + (size_t)(parts > 1 ? sw : g) * k;
                     const int na = k <= 32 ? __popc(__ballot_sync(FULL, lane < k && L[lane < k ? lane : 0] != KEY_INF))
-                                           : lcnt[g];
+                                           : lc0[g];
                     if (multi) {
                         for (int t = lane; t < k; t += 32)
                             a.partials[((size_t)qm[g].slot * a.max_tiles_per_label + ti.tile_in_seg) * k + t] =
@@ -703,13 +823,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     __syncwarp();
                 }
                 if (multi) {
+                    // last-block-done: the CTA completing the segment's last tile merges the partials
                     __threadfence();
-                    named_bar_sync(1, 32 * kTcEpi);
-                    if (threadIdx.x == 64) misc[1] = atomicAdd(&a.segs[ti.seg].pad[0], 1) == ti.n_tiles - 1;
-                    named_bar_sync(1, 32 * kTcEpi);
-                    if (misc[1]) {
+                    named_bar_sync(3, 32 * kTcSelW);
+                    if (sw == 0 && lane == 0) misc[2] = atomicAdd(&a.segs[ti.seg].pad[0], 1) == ti.n_tiles - 1;
+                    named_bar_sync(3, 32 * kTcSelW);
+                    if (misc[2]) {
                         __threadfence();
-                        for (int g = e; g < nq; g += kTcEpi) {
+                        for (int g = sw; g < nq; g += kTcSelW) {
                             ull *A0 = tmp, *B0 = fin2;
                             int na = 0;
                             for (int t2 = 0; t2 < ti.n_tiles; t2++) {
@@ -730,19 +851,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             __syncwarp();
                         }
                     }
+                    named_bar_sync(3, 32 * kTcSelW);   // misc[2] is read before the next tile writes it
                 }
+                // reset the thresholds of this parity for the tile two ahead (lists are reset by
+                // their warps when that tile starts)
+                if (lane == 0)
+                    for (int g = sw; g < nq; g += kTcSelW) thr0[g] = KEY_INF;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(qempty + tp);
-                tc++;
+                if (lane == 0) {
+                    mbar_arrive(qempty + tp);
+                    mbar_arrive(tfree + tp);
+                }
                 TP_MARK(6)
             }
             n++;
         }
-        if (warp == 2 || warp == 6) TP_DUMP("epi(full,first,accfull,compute,bar,select,last,other)")
-        if (threadIdx.x == 64 && my_rows) {
-            atomicAdd(&a.ctr->scan_rows, my_rows);
-            atomicAdd(&a.ctr->scan_qrows, my_qrows);
-        }
+        if (warp == 6) { TP_DUMP("sel(dready,select,-,-,-,-,last,other)") }
     }
     tc_fence_before();
     __syncthreads();
@@ -882,7 +1006,7 @@ int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, con
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cached_dev[a.ix.dtype] = dev;
     }
-    int grid = cached_nsm;
+    int grid = cached_nsm * SL.ctas;
     if (grid > max_tiles_bound) grid = max_tiles_bound;
     f<<<grid, kTcThreads, SL.total, s>>>(a, SL, *reinterpret_cast<const CUtensorMap *>(tm_ls),
                                          *reinterpret_cast<const CUtensorMap *>(tm_x));

@@ -509,6 +509,21 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0);
     a.pool = nullptr;
     a.pool_cap = 0;
+    // small tiles (<= 4 queries, <= 4096 rows) to the warp-per-tile scan, the rest to tcgen05
+    {
+        const char *ws_env = getenv("VF_WARP_SCAN");       // experiment switch (read per search)
+        const bool ws_off = ws_env && atoi(ws_env) == 0;
+        const DevIndex &F8 = ix->enc8 ? ix->dev8 : D;
+        pl.wsplit = pl.tc && !ws_off && warp_scan_supported(F8.dtype, F8.row_bytes, k);
+        a.split_tiles = pl.wsplit ? 1 : 0;
+        a.wtiles = a.btiles = nullptr;
+        if (pl.wsplit && a.max_tiles_per_label < kWarpScanRows / kWarpTileRows) {
+            a.max_tiles_per_label = kWarpScanRows / kWarpTileRows;     // small-group lists, cut finer
+            pl.multi = true;
+            pl.max_tiles = std::max<int64_t>(n_slots, 1) * a.max_tiles_per_label;
+            a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
+        }
+    }
     {
         const char *e = getenv("VF_TC_PARTS");
         a.tc_parts = e ? atoi(e) : 1;
@@ -526,6 +541,12 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
 
     bool fresh = false;
     VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
+    if (pl.wsplit) {
+        VF_CUDA(sc->wtiles.ensure((size_t)pl.max_tiles * 4));
+        VF_CUDA(sc->btiles.ensure((size_t)pl.max_tiles * 4));
+        a.wtiles = sc->wtiles.as<int32_t>();
+        a.btiles = sc->btiles.as<int32_t>();
+    }
     if (pl.filter) {
         int64_t cap = 16ll << 20;                       // 64 MB of survivor ids
         if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
@@ -549,7 +570,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     VF_CUDA(sc->tiles.ensure((size_t)pl.max_tiles * sizeof(Tile)));
     VF_CUDA(sc->item_seg.ensure((size_t)slots * 4));
     VF_CUDA(sc->item_res.ensure((size_t)slots * k * 8));
-    if (pl.multi) VF_CUDA(sc->partials.ensure((size_t)slots * mtpl * k * 8));
+    if (pl.multi) VF_CUDA(sc->partials.ensure((size_t)slots * a.max_tiles_per_label * k * 8));
     VF_CUDA(sc->ctr.ensure(sizeof(Counters)));
     const size_t nls = (size_t)std::max(D.n_bslots, 1);
     VF_CUDA(sc->ls_count.ensure(nls * 4, &fresh));
@@ -618,6 +639,10 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     fast.gate = pl.checked ? 1 : 0;
     slow.gate = 2;
     int sl = pl.tc ? launch_scan_tc(fast, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(fast, s, tb);
+    if (sl >= 0 && pl.wsplit) {
+        const int s3 = launch_scan_warp(fast, s, tb);
+        sl = s3 < 0 ? s3 : sl + s3;
+    }
     if (sl >= 0 && pl.checked) {
         const int s2 = launch_scan(slow, s, tb);
         sl = s2 < 0 ? s2 : sl + s2;
@@ -734,6 +759,8 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     int64_t n_slots = 0;
     if (!off_dev) {
         n_slots = qoff[n];
+    } else if (p->n_query_labels > 0) {
+        n_slots = p->n_query_labels;             // the caller's label-array length (no sync)
     } else {
         VF_CUDA(cudaMemcpyAsync(&n_slots, qoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         VF_CUDA(cudaStreamSynchronize(s));
