@@ -371,7 +371,7 @@ def main():
     #    point; end to end through the C-ABI with pinned host buffers (H2D, launches, D2H inside) and
     #    with device-resident buffers; wall clock per blocking call, p50 / p99 over many calls
     latency = None
-    if main_tgt in results and world == 1:
+    if main_tgt in results and world == 1 and args.lat_calls > 0:
         itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
         latency = {}
         for bsz in (1, 10, 100):

@@ -509,10 +509,12 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0);
     a.pool = nullptr;
     a.pool_cap = 0;
-    // small tiles (<= 4 queries, <= 4096 rows) to the warp-per-tile scan, the rest to tcgen05
+    // small tiles (<= 4 queries, <= 4096 rows) to the warp-per-tile scan, the rest to tcgen05 (opt-in)
     {
-        const char *ws_env = getenv("VF_WARP_SCAN");       // experiment switch (read per search)
-        const bool ws_off = ws_env && atoi(ws_env) == 0;
+        // opt-in (VF_WARP_SCAN=1, read per search): measured slower than the tensor-core scan on
+        // both BASELINE workloads (scripts/ab_env.py), kept for small-group studies
+        const char *ws_env = getenv("VF_WARP_SCAN");
+        const bool ws_off = !(ws_env && atoi(ws_env) == 1);
         const DevIndex &F8 = ix->enc8 ? ix->dev8 : D;
         pl.wsplit = pl.tc && !ws_off && warp_scan_supported(F8.dtype, F8.row_bytes, k);
         a.split_tiles = pl.wsplit ? 1 : 0;

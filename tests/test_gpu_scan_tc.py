@@ -233,3 +233,26 @@ def test_u8_scan_mixed_query_group_sizes_exact_mode(vf):
     for ex in (False, True):
         a, ad = g.search(Q, qoff, qlab, k=10, itopk=16, exact=ex)
         assert (a == e).all() and (ad == ed.astype(np.float32)).all(), ex
+
+
+@pytest.mark.parametrize("op", ["single", "and"])
+def test_warp_scan_opt_in_is_exact(vf, monkeypatch, op):
+    """VF_WARP_SCAN=1 sends tiles of <= 4 queries on lists of <= 4096 rows to the warp-per-tile
+    scan (k_scan_warp, 256-row tiles merged through partials); results stay bit-exact."""
+    from workload import gen
+    monkeypatch.setenv("VF_WARP_SCAN", "1")
+    cfg, X, off, ids, go, gi = small_random_index(seed=41, N=5000, D=96, L=12, F=2.5, T=800, R=8,
+                                                  dtype="u8")
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=300)
+    if op == "single":
+        qoff = np.arange(301, dtype=np.int64)
+        qlab = np.random.default_rng(2).integers(0, cfg.n_labels, size=300).astype(np.int32)
+    else:
+        qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=300, mode="and2")
+    for exact in (False, True):
+        a, ad = g.search(Q, qoff, qlab, k=10, itopk=32, op=op, exact=exact)
+        e, ed = (o.exact_knn(Q, qoff, qlab, k=10, op=op) if exact else
+                 o.search(Q, qoff, qlab, k=10, itopk=32, op=op))
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), exact
