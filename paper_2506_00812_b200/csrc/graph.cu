@@ -210,10 +210,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
             }
             __syncwarp();
             ull ck = lane < nc ? cbuf[lane] : KEY_INF;
-            ck = warp_sort32(ck, lane);
-            cbuf[lane] = ck;
+            // a full Top keeps its best M keys: a child not below the M-th can never enter it, so
+            // it is dropped before the sort / merge (it is already counted as visited)
+            if (ntop == M && ck >= cur[M - 1]) ck = KEY_INF;
+            const unsigned sm = __ballot_sync(FULL, ck != KEY_INF);
+            const int ns = __popc(sm);
+            if (ns == 0) return;
+            if (ns == 1) {
+                ck = __shfl_sync(FULL, ck, __ffs(sm) - 1);
+                if (lane == 0) cbuf[0] = ck;
+            } else {
+                ck = warp_sort32(ck, lane);
+                cbuf[lane] = ck;
+            }
             __syncwarp();
-            ntop = warp_merge(cur, ntop, cbuf, nc, oth, M, lane);
+            ntop = warp_merge(cur, ntop, cbuf, ns, oth, M, lane);
             ull *t2 = cur; cur = oth; oth = t2;
         };
 
