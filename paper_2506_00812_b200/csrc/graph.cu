@@ -216,6 +216,32 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
             const unsigned sm = __ballot_sync(FULL, ck != KEY_INF);
             const int ns = __popc(sm);
             if (ns == 0) return;
+            if (M <= 32) {
+                // Top fits one key per lane: merge in registers (no shared-memory rank search)
+                ull Li = lane < ntop ? cur[lane] : KEY_INF;
+                if (ns == 1) {
+                    const ull kk = __shfl_sync(FULL, ck, __ffs(sm) - 1);
+                    const int pos = __popc(__ballot_sync(FULL, Li < kk));
+                    const ull up = __shfl_up_sync(FULL, Li, 1);
+                    if (lane > pos) Li = up;
+                    else if (lane == pos) Li = kk;
+                } else {
+                    // the 32 smallest of two sorted lists: min against the reversed candidates is a
+                    // bitonic sequence, sorted by five compare-exchange steps
+                    const ull srt = warp_sort32(ck, lane);
+                    const ull r = __shfl_sync(FULL, srt, 31 - lane);
+                    Li = Li < r ? Li : r;
+#pragma unroll
+                    for (int j = 16; j > 0; j >>= 1) {
+                        const ull o = __shfl_xor_sync(FULL, Li, j);
+                        Li = ((lane & j) == 0) ? (Li < o ? Li : o) : (Li < o ? o : Li);
+                    }
+                }
+                if (lane < M) cur[lane] = Li;
+                ntop = min(M, ntop + ns);
+                __syncwarp();
+                return;
+            }
             if (ns == 1) {
                 ck = __shfl_sync(FULL, ck, __ffs(sm) - 1);
                 if (lane == 0) cbuf[0] = ck;

@@ -263,6 +263,7 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
 constexpr int kFiltThreads = 256;
 constexpr int kFiltBuf = 4096;
 constexpr int kFiltUnion = 64;
+constexpr int kFiltRows = 4;          // rows per thread per round
 
 __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
     __shared__ int32_t buf[kFiltBuf];
@@ -326,31 +327,54 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
             s_qm[threadIdx.x] = qm;
         }
         __syncthreads();
-        for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads) {
-            const int r = r0 + threadIdx.x;
-            if (r < tl.row_end) {
-                const int32_t gid = __ldg(a.ix.M_hs + tl.base + r);
+        for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads * kFiltRows) {
+            // kFiltRows rows per thread, their dependent chains (id -> label offsets -> labels)
+            // interleaved so several memory latencies overlap
+            int32_t gid[kFiltRows];
+            int64_t lo[kFiltRows], hi[kFiltRows];
+#pragma unroll
+            for (int u = 0; u < kFiltRows; u++) {
+                const int r = r0 + u * kFiltThreads + threadIdx.x;
+                gid[u] = r < tl.row_end ? __ldg(a.ix.M_hs + tl.base + r) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < kFiltRows; u++) {
+                lo[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u]) : 0;
+                hi[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u] + 1) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kFiltRows; u++) {
+                if (gid[u] < 0) continue;
                 bool pass = false;
                 if (nu <= 64) {
-                    const int64_t lo = __ldg(a.ix.pt_off + gid), hi = __ldg(a.ix.pt_off + gid + 1);
                     unsigned long long bits = 0;
-                    for (int64_t e = lo; e < hi; e++) {
-                        const int32_t l = __ldg(a.ix.pt_lab + e);
-                        if (nu == 0 || l > s_u[nu - 1]) break;
-                        int b0 = 0, b1 = nu - 1;
-                        while (b0 < b1) { const int mid = (b0 + b1) >> 1; if (s_u[mid] < l) b0 = mid + 1; else b1 = mid; }
-                        if (s_u[b0] == l) bits |= 1ull << b0;
+                    const int32_t umax = nu > 0 ? s_u[nu - 1] : -1;
+                    // the point's sorted labels, 8 independent loads per round
+                    for (int64_t e0 = lo[u]; e0 < hi[u]; e0 += 8) {
+                        int32_t l8[8];
+#pragma unroll
+                        for (int t = 0; t < 8; t++) l8[t] = e0 + t < hi[u] ? __ldg(a.ix.pt_lab + e0 + t) : INT32_MAX;
+                        bool stop = false;
+#pragma unroll
+                        for (int t = 0; t < 8; t++) {
+                            const int32_t l = l8[t];
+                            if (l > umax) { stop = true; break; }
+                            int b0 = 0, b1 = nu - 1;
+                            while (b0 < b1) { const int mid = (b0 + b1) >> 1; if (s_u[mid] < l) b0 = mid + 1; else b1 = mid; }
+                            if (s_u[b0] == l) bits |= 1ull << b0;
+                        }
+                        if (stop) break;
                     }
                     for (int g = 0; g < tl.nq && !pass; g++) pass = (bits & s_qm[g]) == s_qm[g];
                 } else {
                     for (int g = 0; g < tl.nq && !pass; g++)
-                        pass = verify_pred(a.ix, gid, a.qlab + q_off[g], q_nl[g], tl.label);
+                        pass = verify_pred(a.ix, gid[u], a.qlab + q_off[g], q_nl[g], tl.label);
                 }
-                if (pass) buf[atomicAdd(&s_n, 1)] = gid;
+                if (pass) buf[atomicAdd(&s_n, 1)] = gid[u];
             }
             __syncthreads();
-            const bool last = r0 + kFiltThreads >= tl.row_end;
-            if (s_n > kFiltBuf - kFiltThreads || (last && s_n > 0)) {
+            const bool last = r0 + kFiltThreads * kFiltRows >= tl.row_end;
+            if (s_n > kFiltBuf - kFiltThreads * kFiltRows || (last && s_n > 0)) {
                 if (threadIdx.x == 0) {
                     if (s_np == kMaxPieces) {
                         s_bad = 1;
