@@ -207,6 +207,10 @@ typedef struct {
     double ms_route, ms_scan, ms_graph, ms_merge, ms_copy, ms_total;
     int32_t kernel_launches;            /* kernels this search launched */
     int32_t row_bytes;
+    /* means of the ms_* phases over the profiled searches on this stream since profiling was last
+     * enabled (the most recent 64 of them); n_profiled = how many were averaged */
+    int64_t n_profiled;
+    double mean_ms_route, mean_ms_scan, mean_ms_graph, mean_ms_merge, mean_ms_copy, mean_ms_total;
 } vf_search_stats;
 
 vf_status vf_set_profiling(vf_index *index, int32_t enable);

@@ -66,7 +66,9 @@ class SearchStats(C.Structure):
                                          "graph_V", "graph_E", "graph_iterations", "graph_V_max")] + \
                [(n, C.c_double) for n in ("ms_route", "ms_scan", "ms_graph", "ms_merge", "ms_copy",
                                           "ms_total")] + \
-               [("kernel_launches", C.c_int32), ("row_bytes", C.c_int32)]
+               [("kernel_launches", C.c_int32), ("row_bytes", C.c_int32), ("n_profiled", C.c_int64)] + \
+               [(n, C.c_double) for n in ("mean_ms_route", "mean_ms_scan", "mean_ms_graph", "mean_ms_merge",
+                                          "mean_ms_copy", "mean_ms_total")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -62,7 +62,13 @@ struct Scratch {
     // label sharding: item records out / in, returned results, slots of the sent items
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
     size_t gtab_slots = 0, gtab_warps = 0;
-    cudaEvent_t ev[8];
+    // profiled searches record their phase events into a ring: ev points at the current set, so
+    // the mean over every search since profiling was enabled (<= kProfRing of them) is readable
+    // without a host sync between searches
+    static constexpr int kProfRing = 64;
+    cudaEvent_t evs[kProfRing][8];
+    cudaEvent_t *ev = evs[0];
+    int64_t prof_n = 0, prof_first = 0;
     bool ev_ok = false;
     bool profiled = false;
     SearchArgs last{};
@@ -71,7 +77,8 @@ struct Scratch {
     bool has_last = false;
     ~Scratch() {
         if (ev_ok)
-            for (auto &e : ev) cudaEventDestroy(e);
+            for (auto &set : evs)
+                for (auto &e : set) cudaEventDestroy(e);
     }
 };
 

@@ -360,6 +360,7 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         sc->last_slots = jb.n_slots;
         sc->last_launches += launches;
         sc->profiled = jb.ix->profiling;
+        if (sc->profiled) sc->prof_n++;
         sc->has_last = true;
     }
     VF_CUDA(cudaGetLastError());

@@ -431,6 +431,13 @@ extern "C" vf_status vf_set_profiling(vf_index *index, int32_t enable) {
     if (!index) return fail(VF_ERR_INVALID_ARG, "NULL index");
     index->profiling = enable != 0;
     for (vf_index *s : index->vshards) s->profiling = enable != 0;
+    // (re)enabling starts a new averaging window on every stream's scratch
+    auto reset = [](vf_index *ix) {
+        std::lock_guard<std::mutex> g(ix->mu);
+        for (auto &kv : ix->scratch) kv.second->prof_first = kv.second->prof_n;
+    };
+    reset(index);
+    for (vf_index *s : index->vshards) reset(s);
     return VF_OK;
 }
 
@@ -590,9 +597,11 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.gtab_slots = (int64_t)sc->gtab_slots;   // the kernels index the tables with the allocated geometry
     a.n_warp_slots = (int32_t)sc->gtab_warps;
     if (!sc->ev_ok) {
-        for (auto &e : sc->ev) VF_CUDA(cudaEventCreate(&e));
+        for (auto &set : sc->evs)
+            for (auto &e : set) VF_CUDA(cudaEventCreate(&e));
         sc->ev_ok = true;
     }
+    sc->ev = sc->evs[sc->prof_n % Scratch::kProfRing];
     a.Qp = sc->Qp.as<uint8_t>();
     a.q_off = sc->qoff.as<int64_t>();
     a.qlab = sc->qlab.as<int32_t>();
@@ -809,6 +818,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     sc->last_slots = n_slots;
     sc->last_launches = launches;
     sc->profiled = prof;
+    if (prof) sc->prof_n++;
     sc->has_last = true;
     if (!out_dev) VF_CUDA(cudaStreamSynchronize(s));
     return VF_OK;
@@ -839,17 +849,35 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->graph_V_max = (int64_t)c.graph_V_max;
     st->kernel_launches = sc->last_launches;
     st->row_bytes = ix->enc8 && !c.exact_fallback ? ix->dev8.row_bytes : ix->dev.row_bytes;   // rows the kernels read
-    if (sc->profiled) {
+    auto phases = [](cudaEvent_t *e, double *out) {
         float t;
-        cudaEventElapsedTime(&t, sc->ev[1], sc->ev[2]); st->ms_route = t;
-        cudaEventElapsedTime(&t, sc->ev[2], sc->ev[3]); st->ms_scan = t;
-        cudaEventElapsedTime(&t, sc->ev[3], sc->ev[4]); st->ms_graph = t;
-        cudaEventElapsedTime(&t, sc->ev[4], sc->ev[5]); st->ms_merge = t;
+        cudaEventElapsedTime(&t, e[1], e[2]); out[0] = t;
+        cudaEventElapsedTime(&t, e[2], e[3]); out[1] = t;
+        cudaEventElapsedTime(&t, e[3], e[4]); out[2] = t;
+        cudaEventElapsedTime(&t, e[4], e[5]); out[3] = t;
         float c0, c1;
-        cudaEventElapsedTime(&c0, sc->ev[0], sc->ev[1]);
-        cudaEventElapsedTime(&c1, sc->ev[5], sc->ev[6]);
-        st->ms_copy = c0 + c1;
-        cudaEventElapsedTime(&t, sc->ev[0], sc->ev[6]); st->ms_total = t;
+        cudaEventElapsedTime(&c0, e[0], e[1]);
+        cudaEventElapsedTime(&c1, e[5], e[6]);
+        out[4] = c0 + c1;
+        cudaEventElapsedTime(&t, e[0], e[6]); out[5] = t;
+    };
+    if (sc->profiled && sc->prof_n > 0) {
+        double v[6];
+        phases(sc->evs[(sc->prof_n - 1) % Scratch::kProfRing], v);
+        st->ms_route = v[0]; st->ms_scan = v[1]; st->ms_graph = v[2];
+        st->ms_merge = v[3]; st->ms_copy = v[4]; st->ms_total = v[5];
+        const int64_t lo = std::max(sc->prof_first, sc->prof_n - Scratch::kProfRing);
+        double sum[6] = {0, 0, 0, 0, 0, 0};
+        for (int64_t i = lo; i < sc->prof_n; i++) {
+            phases(sc->evs[i % Scratch::kProfRing], v);
+            for (int j = 0; j < 6; j++) sum[j] += v[j];
+        }
+        const int64_t m = sc->prof_n - lo;
+        st->n_profiled = m;
+        if (m > 0) {
+            st->mean_ms_route = sum[0] / m; st->mean_ms_scan = sum[1] / m; st->mean_ms_graph = sum[2] / m;
+            st->mean_ms_merge = sum[3] / m; st->mean_ms_copy = sum[4] / m; st->mean_ms_total = sum[5] / m;
+        }
     }
     return VF_OK;
 }
