@@ -33,9 +33,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG_INDEX = {"tiny": 0, "sift": 1, "yfcc": 2}
-# the 0.90 operating point our arm measured per workload (itopk, search_width, and_scan_threshold);
+# the 0.90 operating point our arm measured per workload (itopk, search_width, and_scan_threshold,
+# scan_threshold);
 # the reference arm (the oracle) runs at it so both arms answer the same searches
-OP_POINT = {"tiny": (32, 1, 0), "sift": (16, 2, 0), "yfcc": (48, 2, 2000)}
+OP_POINT = {"tiny": (32, 1, 0, 0), "sift": (16, 2, 0, 0), "yfcc": (48, 2, 2000, 0)}
 ITOPK_GRID = (16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512)
 METRIC = "QPS at recall@10 >=0.90 and >=0.99 (1/2/4/8 B200); p50 latency at batch 1"
 
@@ -164,15 +165,16 @@ def run_reference(args, config):
     Q, qo, ql = w.Q[:n], w.q_off[:n + 1], w.q_lab[:w.q_off[n]]
     threads = os.cpu_count() or 1
     # our arm's 0.90 operating point for this workload (profiles/r01_bench_*.json)
-    itopk, w_, as_ = OP_POINT[config] if args.ref_itopk <= 0 else (args.ref_itopk, 1, 0)
+    itopk, w_, as_, st_ = OP_POINT[config] if args.ref_itopk <= 0 else (args.ref_itopk, 1, 0, 0)
     op = "and" if c.query_mode in ("and2", "mix_and") else ("or" if c.query_mode == "or2" else "single")
     for _ in range(args.warmup):
         o.search(Q[:64], qo[:65], ql[:qo[64]], k=c.k, itopk=itopk, search_width=w_, op=op, nthreads=threads,
-                 and_scan_threshold=as_)
+                 and_scan_threshold=as_, scan_threshold=st_)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        o.search(Q, qo, ql, k=c.k, itopk=itopk, search_width=w_, op=op, nthreads=threads, and_scan_threshold=as_)
+        o.search(Q, qo, ql, k=c.k, itopk=itopk, search_width=w_, op=op, nthreads=threads, and_scan_threshold=as_,
+                 scan_threshold=st_)
         times.append(time.perf_counter() - t0)
     total = float(np.sum(times))
     qps = n * args.steps / total
@@ -181,7 +183,7 @@ def run_reference(args, config):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"{config} (BASELINE.json configs[{CFG_INDEX[config]}])",
                                              "n_queries_per_step": n, "itopk": itopk, "search_width": w_,
-                                             "and_scan_threshold": as_, "k": c.k, "flush": "n/a (CPU)"},
+                                             "and_scan_threshold": as_, "scan_threshold": st_, "k": c.k, "flush": "n/a (CPU)"},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "oracle",
                              "sample": f"first {n} queries of the {config} batch per step, itopk={itopk}, w={w_}"},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -201,6 +203,9 @@ def main():
     ap.add_argument("--lat-calls", type=int, default=1000, help="timed calls per small-batch latency point")
     ap.add_argument("--and-scan", default=None,
                     help="f3 selectivity-aware AND routing thresholds swept (0 = the paper's method)")
+    ap.add_argument("--scan-thr", default=None,
+                    help="f2 search-time specificity thresholds T' swept (0 = the build's T; labels with "
+                         "|C_l| < max(T, T') are scanned exactly)")
     ap.add_argument("--gt-sample", type=int, default=-1,
                     help="queries whose exact ground truth is computed for recall (-1: all; yfcc: 5000)")
     ap.add_argument("--cpu-sample", type=int, default=2000)
@@ -214,6 +219,8 @@ def main():
 
     if args.and_scan is None:
         args.and_scan = "0,2000,50000" if args.config == "yfcc" else "0"
+    if args.scan_thr is None:
+        args.scan_thr = "0,10000" if args.config == "sift" else "0"
     if args.gt_sample < 0:
         args.gt_sample = 5000 if args.config == "yfcc" else 0
     if args.impl == "reference":
@@ -284,14 +291,14 @@ def main():
     targets = [float(x) for x in args.targets.split(",")]
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
 
-    def quick_ms(itopk, w_, as_=0):
+    def quick_ms(itopk, w_, as_=0, st_=0):
         ms = []
         for _ in range(3):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
             e1.record(stream)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
@@ -299,21 +306,23 @@ def main():
 
     sweep = []
     and_scans = [int(x) for x in args.and_scan.split(",")] if op == "and" else [0]
-    for as_, w_ in [(a_, b_) for a_ in and_scans for b_ in (int(x) for x in args.widths.split(","))]:
+    scan_thrs = [int(x) for x in args.scan_thr.split(",")]
+    for as_, st_, w_ in [(a_, t_, b_) for a_ in and_scans for t_ in scan_thrs
+                         for b_ in (int(x) for x in args.widths.split(","))]:
         for itopk in ITOPK_GRID:
             if itopk < k:
                 continue
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
             torch.cuda.synchronize()
             r_strict, r_tie = recall_vs(ids[:m_gt].cpu().numpy(), dd[:m_gt].cpu().numpy(), gt, gd, k)
-            qms = quick_ms(itopk, w_, as_)
+            qms = quick_ms(itopk, w_, as_, st_)
             if world > 1:   # every rank takes the same decisions (the searches are collective)
                 t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
                 dist.all_reduce(t)
                 r_strict, r_tie, qms = (float(x) / world for x in t.tolist())
-            sweep.append((itopk, r_strict, r_tie, w_, qms, as_))
-            log(f"and_scan={as_} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
+            sweep.append((itopk, r_strict, r_tie, w_, qms, as_, st_))
+            log(f"and_scan={as_} scan_thr={st_} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
                 f"{n / qms / 1e3:.2f} MQPS")
             if r_tie >= max(targets):
                 break
@@ -325,11 +334,11 @@ def main():
     ix.set_profiling(True)
     hbm_peak, peak_kind = measured_peaks()
 
-    def timed(itopk, w_, as_):
+    def timed(itopk, w_, as_, st_):
         """W warm-up + exactly K timed steps; per-step CUDA events around vf_search only."""
         for _ in range(args.warmup):
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         stats = []
@@ -341,7 +350,7 @@ def main():
             flush.fill_(float(i))
             ev[i][0].record(stream)
             ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
             ev[i][1].record(stream)
         # no host sync inside the loop: the host enqueues step i+1 while the device runs step i,
         # so the events time the device work (host-side cost is what `e2e` measures)
@@ -357,8 +366,8 @@ def main():
         for tgt, opnt in ops.items():
             if opnt is None:
                 continue
-            itopk, w_, as_ = opnt[0], opnt[3], opnt[5]
-            ms, stats = timed(itopk, w_, as_)
+            itopk, w_, as_, st_ = opnt[0], opnt[3], opnt[5], opnt[6]
+            ms, stats = timed(itopk, w_, as_, st_)
             tot = float(np.sum(ms))
             if world > 1:
                 t = torch.tensor([tot], device=dev)
@@ -371,7 +380,7 @@ def main():
     main_tgt = targets[0]
     e2e = None
     if main_tgt in results:
-        itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
+        itopk, w_, as_, st_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5], results[main_tgt][1][6]
         Qh = torch.from_numpy(w.Q).pin_memory()
         qoh = torch.from_numpy(w.q_off).pin_memory()
         qlh = torch.from_numpy(w.q_lab).pin_memory()
@@ -379,14 +388,14 @@ def main():
         odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
         for _ in range(args.warmup):
             ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
             ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
         e1.record(stream)
         torch.cuda.synchronize()
         et = e0.elapsed_time(e1)
@@ -404,7 +413,7 @@ def main():
     #    with device-resident buffers; wall clock per blocking call, p50 / p99 over many calls
     latency = None
     if main_tgt in results and world == 1 and args.lat_calls > 0:
-        itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
+        itopk, w_, as_, st_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5], results[main_tgt][1][6]
         latency = {}
         for bsz in (1, 10, 100):
             Qh = torch.from_numpy(w.Q[:bsz].copy()).pin_memory()
@@ -422,10 +431,11 @@ def main():
                     t0 = time.perf_counter()
                     if mode == "host":
                         ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                                       and_scan_threshold=as_, stream=stream)
+                                       and_scan_threshold=as_, stream=stream, scan_threshold=st_)
                     else:
                         ix.search_into(Qd, qod, qld, oid, odd, k=k, itopk=itopk, search_width=w_, op=op,
-                                       and_scan_threshold=as_, stream=stream, n_query_labels=int(w.q_off[bsz]))
+                                       and_scan_threshold=as_, stream=stream, n_query_labels=int(w.q_off[bsz]),
+                                       scan_threshold=st_)
                         stream.synchronize()
                     if it_ >= 50:
                         ts.append(time.perf_counter() - t0)
@@ -438,7 +448,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
         import oracle
-        itopk, w_, as_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5]
+        itopk, w_, as_, st_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5], results[main_tgt][1][6]
         o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
         m = min(n, args.cpu_sample)
         threads = os.cpu_count() or 1
@@ -446,7 +456,7 @@ def main():
         while el < args.cpu_seconds and passes < 1000:
             t0 = time.perf_counter()
             o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], k=k, itopk=itopk, search_width=w_, op=op,
-                     nthreads=threads, and_scan_threshold=as_)
+                     nthreads=threads, and_scan_threshold=as_, scan_threshold=st_)
             el += time.perf_counter() - t0
             passes += 1
         cpu = {"value": m * passes / el, "unit": "queries/s", "cores": threads, "kind": "oracle",
@@ -486,6 +496,7 @@ def main():
                    "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
                    "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
                    "R": R, "itopk": itopk, "search_width": opnt[3], "and_scan_threshold": opnt[5],
+                   "scan_threshold": opnt[6],
                    "recall_target": main_tgt,
                    "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
                    "recall_sample": f"first {m_gt} queries (exact-mode ground truth)",
@@ -495,10 +506,10 @@ def main():
                    "storage": ("u8 rows (lossless store of integer-valued fp32 in [0,255]; fp32 rows kept "
                                "for out-of-range query batches)") if (c.dtype != "u8" and info["bytes_u8_store"] > 0)
                               else c.dtype},
-        "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "and_scan_threshold": r[1][5], "qps": n * world * K / (r[4] / 1000.0),
+        "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "and_scan_threshold": r[1][5], "scan_threshold": r[1][6], "qps": n * world * K / (r[4] / 1000.0),
                                    "ms_per_step": r[4] / K, "recall_strict": r[1][1],
                                    "recall_tie_aware": r[1][2]} for t, r in results.items()},
-        "sweep": [{"and_scan_threshold": s[5], "search_width": s[3], "itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2],
+        "sweep": [{"and_scan_threshold": s[5], "scan_threshold": s[6], "search_width": s[3], "itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2],
                    "ms": s[4]} for s in sweep],
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,

@@ -116,11 +116,15 @@ typedef struct {
      * the exact scan of C_l* with the predicate instead of the inline-filtered graph search, whose
      * traversal collapses when few points pass the filter. */
     int32_t and_scan_threshold;
+    /* Search-time specificity threshold (the T sweep of P:L339):
+     * an item whose label has |C_l| < max(T, scan_threshold) is served by the exact scan. Values
+     * <= the build's T change nothing (LS labels have no graph); INT32_MAX = scan everything, the
+     * same results as `exact`. 0 = the index's T. */
+    int32_t scan_threshold;
     /* Length of the query-label array (= qlabel_offsets[n]) when the offsets live in DEVICE memory:
      * > 0 lets vf_search size its work without reading qlabel_offsets[n] back (no stream sync, so
      * consecutive searches overlap their host and device work). 0 = read it (one stream sync).
      * Must equal qlabel_offsets[n] when given; ignored for host offsets. */
-    int32_t pad0;
     int64_t n_query_labels;
 } vf_search_params;
 

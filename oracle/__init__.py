@@ -54,11 +54,11 @@ def lib():
         L.or_entry_hash.restype = u32
         L.or_entry_hash.argtypes = [u32, u32, i32, u32, u32]
         L.or_route.restype = i64
-        L.or_route.argtypes = [p, i64, p, p, C.c_int, C.c_int, C.c_int, i32, p, i64, p]
+        L.or_route.argtypes = [p, i64, p, p, C.c_int, C.c_int, C.c_int, i32, i32, p, i64, p]
         L.or_merge.argtypes = [C.c_int, C.c_int, p, p, p, p]
         L.or_search.restype = C.c_int
         L.or_search.argtypes = [p, i64, p, p, p, C.c_int, C.c_int, C.c_int, i32, i32, i32, i32,
-                                i32, u32, i32, p, p, p, i32, C.c_int, i32]
+                                i32, u32, i32, p, p, p, i32, C.c_int, i32, i32]
         L.or_exact_knn.restype = C.c_int
         L.or_exact_knn.argtypes = [p, i64, p, p, p, C.c_int, i32, p, p, C.c_int]
         L.or_index_pt_off.restype = i64
@@ -133,7 +133,8 @@ class Index:
     # -- the method ----------------------------------------------------------------
     def search(self, Q, q_off, q_lab, k=10, itopk=64, op="single", recall_mode="greedy",
                exact=False, search_width=1, n_init=0, max_iterations=0, seed=0x5EED1234,
-               forced_entry=-1, nthreads=None, counters=False, max_items_per_q=8, and_scan_threshold=0):
+               forced_entry=-1, nthreads=None, counters=False, max_items_per_q=8, and_scan_threshold=0,
+               scan_threshold=0):
         Q = np.ascontiguousarray(Q, dtype=self.X.dtype)
         q_off = np.ascontiguousarray(q_off, dtype=np.int64)
         q_lab = np.ascontiguousarray(q_lab, dtype=np.int32)
@@ -145,7 +146,7 @@ class Index:
                              RECALL_MODE[recall_mode], int(exact), k, itopk, search_width, n_init,
                              max_iterations, seed & 0xFFFFFFFF, forced_entry, _ptr(ids), _ptr(d),
                              _ptr(ctr) if ctr is not None else None, max_items_per_q,
-                             nthreads or nthreads_default(), int(and_scan_threshold))
+                             nthreads or nthreads_default(), int(and_scan_threshold), int(scan_threshold))
         if rc != 0:
             raise ValueError("oracle: invalid query (SINGLE with more than one label)")
         return (ids, d, ctr) if counters else (ids, d)
@@ -162,7 +163,8 @@ class Index:
                            _ptr(d), nthreads or nthreads_default())
         return ids, d
 
-    def route(self, q_off, q_lab, op="single", recall_mode="greedy", exact=False, and_scan_threshold=0):
+    def route(self, q_off, q_lab, op="single", recall_mode="greedy", exact=False, and_scan_threshold=0,
+              scan_threshold=0):
         q_off = np.ascontiguousarray(q_off, dtype=np.int64)
         q_lab = np.ascontiguousarray(q_lab, dtype=np.int32)
         n = len(q_off) - 1
@@ -170,7 +172,8 @@ class Index:
         out = np.empty((nmax, 5), np.int32)
         pred = np.empty(max(1, int(np.sum(np.diff(q_off) ** 2)) + 1), np.int32)
         m = lib().or_route(self._h, n, _ptr(q_off), _ptr(q_lab), OP[op], RECALL_MODE[recall_mode],
-                           int(exact), int(and_scan_threshold), _ptr(out), nmax, _ptr(pred))
+                           int(exact), int(and_scan_threshold), int(scan_threshold), _ptr(out), nmax,
+                           _ptr(pred))
         if m < 0:
             raise ValueError("oracle: invalid query")
         return out[:m].copy(), pred

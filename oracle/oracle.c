@@ -279,12 +279,13 @@ static void exact_one(const or_index *ix, const void *q, const int32_t *lq_in, i
  * and_scan_threshold > 0 enables the selectivity-aware AND routing of SURVEY §8(f) f3 (NOT in
  * the paper; include/vf.h): a greedy item with HS l* goes to SCAN when the expected AND-set size
  * est = |C_l*| * prod over the other labels (ascending) of |C_o| / N, evaluated left to right in
- * fp64, is below the threshold. */
+ * fp64, is below the threshold. scan_threshold > T raises the routing threshold for this search
+ * (the T sweep of P:L339 / P:L766-L768); <= T changes nothing. */
 typedef struct { int32_t qid, label, path; int64_t pred_start; int32_t pred_len; } item_t;
 
 static int64_t route_query(const or_index *ix, int32_t qid, const int32_t *lq_in, int nl, int op,
-                           int recall_mode, int exact, int32_t and_scan_threshold, item_t *items,
-                           int32_t *pred_buf, int64_t *pred_pos)
+                           int recall_mode, int exact, int32_t and_scan_threshold, int32_t scan_threshold,
+                           item_t *items, int32_t *pred_buf, int64_t *pred_pos)
 {
     int32_t lq[4096];
     if (nl > 4096) return -1;
@@ -292,8 +293,10 @@ static int64_t route_query(const or_index *ix, int32_t qid, const int32_t *lq_in
     nl = sort_dedup(lq, nl);
     if (op == OR_SINGLE && nl > 1) return -1;
     int64_t n = 0;
+    /* search-time threshold (f2): SCAN iff |C_l| < max(T, scan_threshold) */
+    const int64_t T_eff = scan_threshold > ix->T ? (int64_t)scan_threshold : (int64_t)ix->T;
 #define PATH_OF(l) (label_size(ix, (l)) == 0 ? OR_PATH_NONE : \
-                    ((exact || label_size(ix, (l)) < ix->T) ? OR_PATH_SCAN : OR_PATH_GRAPH))
+                    ((exact || label_size(ix, (l)) < T_eff) ? OR_PATH_SCAN : OR_PATH_GRAPH))
     if (op == OR_SINGLE || op == OR_OR) {
         for (int t = 0; t < nl; t++) {
             if (label_size(ix, lq[t]) == 0) continue;
@@ -332,7 +335,8 @@ static int64_t route_query(const or_index *ix, int32_t qid, const int32_t *lq_in
 
 /* Python-facing router: out_items[n_max][5] = {qid, label, path, pred_start, pred_len}. */
 int64_t or_route(const or_index *ix, int64_t n_q, const int64_t *q_off, const int32_t *q_lab, int op,
-                 int recall_mode, int exact, int32_t and_scan_threshold, int32_t *out_items, int64_t n_max,
+                 int recall_mode, int exact, int32_t and_scan_threshold, int32_t scan_threshold,
+                 int32_t *out_items, int64_t n_max,
                  int32_t *pred_buf)
 {
     int64_t n = 0, pp = 0;
@@ -340,7 +344,7 @@ int64_t or_route(const or_index *ix, int64_t n_q, const int64_t *q_off, const in
     for (int64_t i = 0; i < n_q; i++) {
         int nl = (int)(q_off[i + 1] - q_off[i]);
         int64_t m = route_query(ix, (int32_t)i, q_lab + q_off[i], nl, op, recall_mode, exact,
-                                and_scan_threshold, tmp, pred_buf, &pp);
+                                and_scan_threshold, scan_threshold, tmp, pred_buf, &pp);
         if (m < 0) { free(tmp); return -1; }
         for (int64_t t = 0; t < m; t++) {
             if (n >= n_max) { free(tmp); return -2; }
@@ -488,7 +492,7 @@ typedef struct {
     const or_index *ix;
     int64_t n_q; const void *Q; const int64_t *q_off; const int32_t *q_lab;
     int op, recall_mode, exact;
-    int32_t and_scan_threshold;
+    int32_t and_scan_threshold, scan_threshold;
     beam_params bp;
     int32_t forced_entry;
     int32_t *out_ids; double *out_dists;
@@ -515,7 +519,7 @@ static void search_one(job_t *jb, int64_t i)
     int32_t *pred = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nl * nl + 1));
     int64_t pp = 0;
     int64_t m = route_query(ix, (int32_t)i, lq, nl, jb->op, jb->recall_mode, jb->exact,
-                            jb->and_scan_threshold, items, pred, &pp);
+                            jb->and_scan_threshold, jb->scan_threshold, items, pred, &pp);
     if (m < 0) { jb->err = 1; m = 0; }
     uint32_t qh = or_query_hash(ix->dtype, ix->dim, q);
     entry_t *all = (entry_t *)malloc(sizeof(entry_t) * (size_t)(m * k + 1));
@@ -574,13 +578,14 @@ int or_search(const or_index *ix, int64_t n_q, const void *Q, const int64_t *q_o
               int op, int recall_mode, int exact, int32_t k, int32_t itopk, int32_t search_width,
               int32_t n_init, int32_t max_iterations, uint32_t seed, int32_t forced_entry,
               int32_t *out_ids, double *out_dists, int64_t *item_ctr, int32_t max_items_per_q,
-              int nthreads, int32_t and_scan_threshold)
+              int nthreads, int32_t and_scan_threshold, int32_t scan_threshold)
 {
     job_t jb;
     memset(&jb, 0, sizeof(jb));
     jb.ix = ix; jb.n_q = n_q; jb.Q = Q; jb.q_off = q_off; jb.q_lab = q_lab;
     jb.op = op; jb.recall_mode = recall_mode; jb.exact = exact;
     jb.and_scan_threshold = and_scan_threshold;
+    jb.scan_threshold = scan_threshold;
     jb.bp.k = k; jb.bp.itopk = itopk < k ? k : itopk;
     jb.bp.search_width = search_width < 1 ? 1 : (search_width > 64 ? 64 : search_width);
     jb.bp.n_init = n_init > 0 ? n_init : ix->R * jb.bp.search_width;

@@ -46,7 +46,7 @@ class SearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("itopk", C.c_int32), ("search_width", C.c_int32),
                 ("n_init", C.c_int32), ("max_iterations", C.c_int32), ("seed", C.c_uint32),
                 ("op", C.c_int32), ("recall_mode", C.c_int32), ("exact", C.c_int32),
-                ("and_scan_threshold", C.c_int32), ("pad0", C.c_int32), ("n_query_labels", C.c_int64)]
+                ("and_scan_threshold", C.c_int32), ("scan_threshold", C.c_int32), ("n_query_labels", C.c_int64)]
 
 
 class IndexInfo(C.Structure):
@@ -196,14 +196,15 @@ class Index:
 
     def search_into(self, Q, q_off, q_lab, out_ids, out_dists, k=10, itopk=64, op="single",
                     recall_mode="greedy", exact=False, search_width=1, n_init=0, max_iterations=0,
-                    seed=0x5EED1234, and_scan_threshold=0, stream=None, n_query_labels=0):
+                    seed=0x5EED1234, and_scan_threshold=0, stream=None, n_query_labels=0,
+                    scan_threshold=0):
         """vf_search with caller-provided buffers (numpy host arrays or torch tensors on either
         side). Asynchronous on `stream` when the outputs are device tensors. With device label
         offsets, `n_query_labels` = q_off[-1] (if the caller knows it) avoids a stream sync."""
         p = SearchParams(int(k), int(itopk), int(search_width), int(n_init), int(max_iterations),
                          int(seed) & 0xFFFFFFFF, OPS[op] if isinstance(op, str) else int(op),
                          MODES[recall_mode] if isinstance(recall_mode, str) else int(recall_mode),
-                         1 if exact else 0, int(and_scan_threshold), 0, int(n_query_labels))
+                         1 if exact else 0, int(and_scan_threshold), int(scan_threshold), int(n_query_labels))
         n = int(q_off.shape[0]) - 1
         _check(lib().vf_search(self._h, _ptr(Q), n, _ptr(q_off), _ptr(q_lab), C.byref(p),
                                _ptr(out_ids), _ptr(out_dists), _stream_ptr(stream)))

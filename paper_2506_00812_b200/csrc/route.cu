@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
             }
             for (int t = 0; t < nch; t++) {           // routing equation
                 const int32_t s = lsize(chosen[t]);
-                cpath[t] = (a.exact || s < ix.T || and_scan) ? PATH_SCAN : PATH_GRAPH;
+                cpath[t] = (a.exact || s < a.scan_thr || and_scan) ? PATH_SCAN : PATH_GRAPH;
                 // label sharding: an item whose label lives on another rank is shipped there
                 if (ix.owner && ix.owner[chosen[t]] != ix.rank) cpath[t] |= META_REMOTE;
                 ngraph += cpath[t] == PATH_GRAPH;

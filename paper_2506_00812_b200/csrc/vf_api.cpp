@@ -450,7 +450,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     const int R = D.R, k = p->k;
     const int w = p->search_width < 1 ? 1 : p->search_width;
     // labels the scan may stream: LS lists, or every list in exact mode / with f3 AND routing
-    const int scan_max = (p->exact || p->and_scan_threshold > 0) ? ix->max_label_size : ix->max_ls_size;
+    const int scan_max = (p->exact || p->and_scan_threshold > 0 || p->scan_threshold > D.T) ? ix->max_label_size
+                                                                                           : ix->max_ls_size;
     // row tiles: small in the normal path (load balance across SMs; a label split over several
     // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
     // (the tensor-core scan finalises a label split over tiles with a grid-wide fence and a merge,
@@ -501,6 +502,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.recall_mode = p->recall_mode;
     a.exact = p->exact ? 1 : 0;
     a.and_scan_thr = p->and_scan_threshold;
+    a.scan_thr = std::max(D.T, p->scan_threshold);
     a.tile_rows = tile_rows;
     a.max_tiles_per_label = mtpl;
     a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
@@ -513,7 +515,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.gate = 0;
     // AND items scanned on HS labels (f3 routing or exact mode) are pre-filtered for the
     // tensor-core scan (k_hs_filter); the survivor pool is sized per search, overflow is exact
-    pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0);
+    pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0 || p->scan_threshold > D.T);
     a.pool = nullptr;
     a.pool_cap = 0;
     // small tiles (<= 4 queries, <= 4096 rows) to the warp-per-tile scan, the rest to tcgen05 (opt-in)

@@ -170,7 +170,8 @@ struct SearchArgs {
     int32_t k, itopk, w, n_init, max_iter;
     uint32_t seed;
     int32_t op, recall_mode, exact;
-    int32_t and_scan_thr;     // selectivity-aware AND routing (f3), 0 = off
+    int32_t and_scan_thr;
+    int32_t scan_thr;      // effective specificity threshold of this search: max(T, scan_threshold) (f2)     // selectivity-aware AND routing (f3), 0 = off
     int32_t tile_rows;
     int32_t max_tiles_per_label;
     int32_t max_tiles;

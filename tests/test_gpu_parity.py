@@ -304,3 +304,20 @@ def test_u8_store_fallback_batch(vf, tiny):
     assert (ids[keep] == oi[keep]).all() and (d[keep] == od[keep].astype(np.float32)).all()
     assert g.last_stats()["row_bytes"] == (w.X.shape[1] * 4 + 15) // 16 * 16     # the fp32 rows ran
     assert np.intersect1d(ids[5], oi[5]).size >= 9
+
+
+@pytest.mark.parametrize("thr", [0, 500, 1500, 3000, 2**31 - 1])
+def test_scan_threshold_f2_bit_exact(vf, tiny, thr):
+    """Search-time specificity threshold (f2): labels below max(T, T') are scanned on both sides;
+    results and per-item counters identical for single and greedy-AND queries."""
+    from workload import gen
+    w, go, gi = tiny
+    g, o = _pair(vf, w.X, w, go, gi)
+    ids, d = g.search(w.Q, w.q_off, w.q_lab, k=10, itopk=32, scan_threshold=thr)
+    oi, od, octr = o.search(w.Q, w.q_off, w.q_lab, k=10, itopk=32, scan_threshold=thr, counters=True)
+    assert (ids == oi).all() and (d == od.astype(np.float32)).all()
+    _items_match(g, octr)
+    qoff, qlab = gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=len(w.Q), mode="and2")
+    ids, d = g.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", scan_threshold=thr)
+    oi, od = o.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", scan_threshold=thr)
+    assert (ids == oi).all() and (d == od.astype(np.float32)).all()

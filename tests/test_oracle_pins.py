@@ -315,3 +315,29 @@ def test_f3_infinite_threshold_makes_greedy_and_exact(tiny, tiny_oracle):
     ids, d = tiny_oracle.search(Q, qoff, qlab, k=10, op="and", and_scan_threshold=2**30)
     gt, gd = tiny_oracle.exact_knn(Q, qoff, qlab, k=10, op="and")
     assert (ids == gt).all() and (d == gd).all()
+
+
+def test_scan_threshold_routing_f2():
+    """SURVEY §8(f) f2 (the T sweep, P:L339 / P:L766-L768): a search-time threshold T' routes
+    |C_l| < max(T, T') to the scan. Hand example at T = 2000: |C_A| = 5,000 is HS; T' = 5,000
+    keeps it on the graph (5000 < 5000 is false, P:L334's strict '<'), T' = 5,001 scans it;
+    T' below T cannot send the LS label |C_B| = 1,500 to a graph it does not have."""
+    off = np.array([0, 5000, 6500], np.int64)
+    ids = np.concatenate([np.arange(5000), np.arange(3000, 4500)]).astype(np.int32)
+    X = np.zeros((10000, 4), np.float32)
+    ix = oracle.Index(X, off, ids, 2000, 16)
+    qo, ql = np.array([0, 1, 2], np.int64), np.array([0, 1], np.int32)
+    for thr, pa in [(0, oracle.PATH_GRAPH), (1000, oracle.PATH_GRAPH), (5000, oracle.PATH_GRAPH),
+                    (5001, oracle.PATH_SCAN), (2**31 - 1, oracle.PATH_SCAN)]:
+        items, _ = ix.route(qo, ql, op="single", scan_threshold=thr)
+        assert [int(x) for x in items[:, 2]] == [pa, oracle.PATH_SCAN], (thr, items)
+
+
+def test_f2_infinite_threshold_equals_definition_1(tiny, tiny_oracle):
+    """T' = infinity serves every item by the exact scan: results are Definition 1,
+    i.e. the scan-only end of the paper's threshold sweep is exact kNN."""
+    w, _, _ = tiny
+    Q, qoff, qlab = w.Q[:300], w.q_off[:301], w.q_lab[:w.q_off[300]]
+    ids, d = tiny_oracle.search(Q, qoff, qlab, k=10, scan_threshold=2**31 - 1)
+    gt, gd = tiny_oracle.exact_knn(Q, qoff, qlab, k=10)
+    assert (ids == gt).all() and (d == gd).all()
