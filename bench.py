@@ -487,6 +487,16 @@ def main():
     dom = "graph" if g_ms >= s_ms else "scan"
     bytes_dom, ms_dom = (g_bytes, g_ms) if dom == "graph" else (s_bytes, s_ms)
     achieved = bytes_dom / (ms_dom / 1000.0) / 1e9 if ms_dom > 0 else 0.0
+    # measured DRAM traffic of that kernel at this operating point, from a committed ncu capture
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f).get(args.config)
+        if tj and tj["kernel"] == f"k_{dom}" and (tj["itopk"], tj["search_width"], tj["and_scan_threshold"],
+                                                  tj["scan_threshold"]) == (itopk, opnt[3], opnt[5], opnt[6]):
+            traffic = int(tj["bytes"])
+    except (OSError, ValueError, KeyError):
+        traffic = None
     line = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": tot / K, "higher_is_better": True, "scaling": "weak",
@@ -513,7 +523,8 @@ def main():
                    "ms": s[4]} for s in sweep],
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": int(bytes_dom),
+                     "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)" if traffic else None,
+                     "algorithmic_bytes_per_launch": int(bytes_dom),
                      "kernel_ms_per_launch": ms_dom},
         "phases_ms": {**{p: s0[f"mean_ms_{p}"] for p in ("route", "scan", "graph", "merge", "copy", "total")},
                       "steps_averaged": s0["n_profiled"]},

@@ -35,15 +35,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
               "-I" + CSRC]
     common += os.environ.get("VF_NVCC_EXTRA", "").split()      # e.g. -DVF_TC_PROF (diagnostics builds)
-    objs = []
-    for f in CU + CPP:
+    def compile_one(f):
         src = os.path.join(CSRC, f)
         obj = os.path.join(objdir, f + ".o")
         cmd = [NVCC] + ARCH + common + ["--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                                          "-c", src, "-o", obj]
         if f.endswith(".cpp"):
             cmd = [NVCC] + common + ["-x", "c++", "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return f, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # translation units compile in parallel (nvcc is single-threaded per file)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(CU + CPP), os.cpu_count() or 1)) as ex:
+        done = list(ex.map(compile_one, CU + CPP))
+    objs = []
+    for f, obj, r in done:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed for {f}")

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
     const int M = GL.itopk, H = GL.hash_slots, R = ix.R, k = a.k;
     const int chunks = ix.chunks, row_bytes = ix.row_bytes;
     const uint32_t hmask = (uint32_t)H - 1;
+    const int r_shift = (R & (R - 1)) == 0 ? __ffs(R) - 1 : -1;
     const int warp_slot = blockIdx.x * kWarpsPerGraphCta + wid;
     ull *gtab = a.gtab + (size_t)warp_slot * a.gtab_slots;
     const uint64_t gmask = (uint64_t)a.gtab_slots - 1;
@@ -219,12 +220,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
             if (M <= 32) {
                 // Top fits one key per lane: merge in registers (no shared-memory rank search)
                 ull Li = lane < ntop ? cur[lane] : KEY_INF;
-                if (ns == 1) {
-                    const ull kk = __shfl_sync(FULL, ck, __ffs(sm) - 1);
-                    const int pos = __popc(__ballot_sync(FULL, Li < kk));
-                    const ull up = __shfl_up_sync(FULL, Li, 1);
-                    if (lane > pos) Li = up;
-                    else if (lane == pos) Li = kk;
+                if (ns <= 4) {
+                    // few survivors (the common case once Top is full): insert one at a time
+                    // (ballot for the position, shift up) instead of a 32-key sort; the register
+                    // list stays sorted, and lanes >= M are never written back
+                    unsigned rem = sm;
+                    while (rem) {
+                        const ull kk = __shfl_sync(FULL, ck, __ffs(rem) - 1);
+                        rem &= rem - 1;
+                        const int pos = __popc(__ballot_sync(FULL, Li < kk));
+                        const ull up = __shfl_up_sync(FULL, Li, 1);
+                        if (lane > pos) Li = up;
+                        else if (lane == pos) Li = kk;
+                    }
                 } else {
                     // the 32 smallest of two sorted lists: min against the reversed candidates is a
                     // bitonic sequence, sorted by five compare-exchange steps
@@ -290,8 +298,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs 
                 const int l = cb + lane;
                 int32_t c = -1, cg = -1;
                 if (l < nch) {
-                    const int p = spar[l / R];
-                    const int2 e = __ldg(ix.G + (base + p) * (int64_t)R + (l % R));
+                    // R is a power of two in practice (16): shift instead of a division
+                    const int pi = r_shift >= 0 ? (l >> r_shift) : l / R;
+                    const int p = spar[pi];
+                    const int2 e = __ldg(ix.G + (base + p) * (int64_t)R + (l - pi * R));
                     c = e.x;
                     cg = e.y;
                     if (c < 0 || c >= S) c = -1;                     // reading #15
