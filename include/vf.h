@@ -199,7 +199,9 @@ vf_status vf_get_index_info(const vf_index *index, vf_index_info *info);
 
 /*
  * Per-phase device timing and work counters of the most recent vf_search on `stream` (timing
- * needs vf_set_profiling(index, 1)). Blocks until that search has finished. Times are CUDA-event
+ * needs vf_set_profiling(index, 1)). A small batch answered by the per-query path (one launch, one
+ * CTA per query; f1) reports its whole kernel as ms_graph, and its item records / V / E counters
+ * like the batched path. Blocks until that search has finished. Times are CUDA-event
  * milliseconds recorded on the search stream around each kernel.
  */
 typedef struct {
@@ -227,6 +229,35 @@ vf_status vf_get_last_stats(vf_index *index, void *cuda_stream, vf_search_stats 
  */
 vf_status vf_get_last_items(vf_index *index, void *cuda_stream, int64_t max_items, int32_t *rec,
                             int64_t *n_items);
+
+/*
+ * Persistent-kernel serving ("Persistent Kernel-based Search
+ * for Small Batch Queries", E13 P:L733-L738). vf_serve_start launches a kernel that stays resident
+ * (n_workers CTAs, <= 0: one per free SM slot) and a job ring of `capacity` slots in pinned,
+ * device-mapped host memory. Each query is answered by one CTA with the same routing, scan, beam
+ * search and merge as vf_search, so results are identical to vf_search with the same parameters
+ * (params: k <= 32; itopk, search_width, n_init, max_iterations, seed, op, recall_mode, exact,
+ * and_scan_threshold, scan_threshold as for vf_search; n_query_labels ignored).
+ *   vf_serve_submit  copies one query (dim elements of the index's element type, HOST memory) and
+ *                    its labels (HOST, 0..16 entries; semantics of `op`) into the next slot and
+ *                    publishes it; returns a ticket. Blocks only while the slot's previous job
+ *                    (ticket - capacity) is still running. Thread-safe.
+ *   vf_serve_wait    spins until the ticket is answered and copies its k ids / distances (HOST,
+ *                    caller-owned; layout as one row of vf_search's output). A ticket's results
+ *                    stay readable until `capacity` more queries have been submitted; a later wait
+ *                    returns VF_ERR_INVALID_ARG. VF_ERR_CUDA if the kernel died.
+ *   vf_serve_stop    stops the kernel once every submitted job is answered; frees the server.
+ * The resident kernel occupies the GPU's SMs: batched vf_search calls on the same device compete
+ * with it for SMs while it runs. The index must outlive the server.
+ */
+typedef struct vf_server vf_server;
+vf_status vf_serve_start(vf_index *index, const vf_search_params *params, int32_t capacity, int32_t n_workers,
+                         vf_server **out);
+vf_status vf_serve_submit(vf_server *server, const void *query, const int32_t *labels, int32_t n_labels,
+                          int64_t *ticket);
+vf_status vf_serve_wait(vf_server *server, int64_t ticket, int32_t *out_ids, float *out_dists);
+vf_status vf_serve_stop(vf_server *server);
+vf_status vf_serve_info(const vf_server *server, int32_t *n_workers, int64_t *submitted);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,7 @@ VF_RECALL_GREEDY, VF_RECALL_PARALLEL = 0, 1
 OPS = {"single": VF_SINGLE, "or": VF_OR, "and": VF_AND}
 MODES = {"greedy": VF_RECALL_GREEDY, "parallel": VF_RECALL_PARALLEL}
 EXPORTED = ("vf_build_index", "vf_search", "vf_free", "vf_last_error", "vf_get_index_info",
+            "vf_serve_start", "vf_serve_submit", "vf_serve_wait", "vf_serve_stop", "vf_serve_info",
             "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items", "vf_build_index_virtual_shards",
             "vf_partition_labels")
 
@@ -101,6 +102,16 @@ def lib():
         L.vf_get_last_stats.argtypes = [p, p, C.POINTER(SearchStats)]
         L.vf_get_last_items.restype = C.c_int
         L.vf_get_last_items.argtypes = [p, p, i64, p, C.POINTER(i64)]
+        L.vf_serve_start.restype = C.c_int
+        L.vf_serve_start.argtypes = [p, C.POINTER(SearchParams), i32, i32, C.POINTER(p)]
+        L.vf_serve_submit.restype = C.c_int
+        L.vf_serve_submit.argtypes = [p, p, p, i32, C.POINTER(i64)]
+        L.vf_serve_wait.restype = C.c_int
+        L.vf_serve_wait.argtypes = [p, i64, p, p]
+        L.vf_serve_stop.restype = C.c_int
+        L.vf_serve_stop.argtypes = [p]
+        L.vf_serve_info.restype = C.c_int
+        L.vf_serve_info.argtypes = [p, C.POINTER(i32), C.POINTER(i64)]
         L.vf_build_index_virtual_shards.restype = C.c_int
         L.vf_build_index_virtual_shards.argtypes = [C.POINTER(BuildDesc), i32, C.POINTER(p)]
         L.vf_partition_labels.restype = C.c_int
@@ -209,6 +220,18 @@ class Index:
         _check(lib().vf_search(self._h, _ptr(Q), n, _ptr(q_off), _ptr(q_lab), C.byref(p),
                                _ptr(out_ids), _ptr(out_dists), _stream_ptr(stream)))
 
+    def serve(self, k=10, itopk=64, op="single", recall_mode="greedy", exact=False, search_width=1, n_init=0,
+              max_iterations=0, seed=0x5EED1234, and_scan_threshold=0, scan_threshold=0, capacity=1024,
+              n_workers=0):
+        """vf_serve_start: a persistent serving kernel on this index (f1); see Server."""
+        p = SearchParams(int(k), int(itopk), int(search_width), int(n_init), int(max_iterations),
+                         int(seed) & 0xFFFFFFFF, OPS[op] if isinstance(op, str) else int(op),
+                         MODES[recall_mode] if isinstance(recall_mode, str) else int(recall_mode),
+                         1 if exact else 0, int(and_scan_threshold), int(scan_threshold), 0)
+        h = C.c_void_p()
+        _check(lib().vf_serve_start(self._h, C.byref(p), int(capacity), int(n_workers), C.byref(h)))
+        return Server(h, k, self)
+
     def search(self, Q, q_off, q_lab, k=10, **kw):
         """Host convenience wrapper: numpy in, numpy out (blocks)."""
         Q = np.ascontiguousarray(Q)
@@ -233,6 +256,50 @@ class Index:
         rec = np.empty((max(n.value, 1), 6), np.int32)
         _check(lib().vf_get_last_items(self._h, _stream_ptr(stream), n.value, _ptr(rec), C.byref(n)))
         return rec[:n.value]
+
+
+class Server:
+    """Persistent-kernel serving (vf_serve_*): submit(query, labels) -> ticket; wait(ticket) -> (ids,
+    dists). Host numpy in and out; one query per call (the single-batch mode of P:L733)."""
+
+    def __init__(self, h, k, index):
+        self._h, self.k, self._index = h, int(k), index
+
+    def submit(self, q, labels) -> int:
+        q = np.ascontiguousarray(q)
+        lab = np.ascontiguousarray(labels, np.int32).reshape(-1)
+        t = C.c_int64()
+        _check(lib().vf_serve_submit(self._h, _ptr(q), _ptr(lab) if lab.size else None, int(lab.size),
+                                     C.byref(t)))
+        return t.value
+
+    def wait(self, ticket, out_ids=None, out_dists=None):
+        ids = np.empty(self.k, np.int32) if out_ids is None else out_ids
+        d = np.empty(self.k, np.float32) if out_dists is None else out_dists
+        _check(lib().vf_serve_wait(self._h, int(ticket), _ptr(ids), _ptr(d)))
+        return ids, d
+
+    def info(self) -> dict:
+        n, s = C.c_int32(), C.c_int64()
+        _check(lib().vf_serve_info(self._h, C.byref(n), C.byref(s)))
+        return {"n_workers": n.value, "submitted": s.value}
+
+    def stop(self):
+        if self._h:
+            h, self._h = self._h, None
+            _check(lib().vf_serve_stop(h))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.stop()
+
+    def __del__(self):
+        try:
+            self.stop()
+        except Exception:
+            pass
 
 
 def partition_labels(sizes, world):

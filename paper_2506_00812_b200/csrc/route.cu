@@ -77,52 +77,9 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
         nraw = (int)(a.q_off[q + 1] - lo);
         int32_t *L = a.qlab + lo;   // the search's private copy of the labels, sorted in place
         if (lane == 0) {
-            // -- sort + dedup (reading #22)
-            for (int i = 1; i < nraw; i++) {
-                int32_t v = L[i];
-                int j = i - 1;
-                while (j >= 0 && L[j] > v) { L[j + 1] = L[j]; j--; }
-                L[j + 1] = v;
-            }
             int nl = 0;
-            for (int i = 0; i < nraw; i++)
-                if (nl == 0 || L[i] != L[nl - 1]) L[nl++] = L[i];
-            auto lsize = [&](int32_t l) -> int32_t {
-                return (l >= 0 && l < ix.n_labels) ? ix.dir[l].size : 0;   // reading #19
-            };
-            if (a.op == 0 || a.op == 1) {             // SINGLE / OR: one item per non-empty label
-                if (!(a.op == 0 && nl > 1))
-                    for (int t = 0; t < nl; t++) if (lsize(L[t]) > 0) chosen[nch++] = L[t];
-            } else {                                  // AND
-                bool any_empty = nl == 0;
-                for (int t = 0; t < nl; t++) any_empty |= lsize(L[t]) == 0;
-                if (!any_empty) {
-                    pred = nl > 1 ? META_PRED : 0;
-                    if (a.recall_mode == 0) {         // greedy: l* = argmin(|C_l|, l)
-                        int best = 0;
-                        for (int t = 1; t < nl; t++) if (lsize(L[t]) < lsize(L[best])) best = t;
-                        chosen[nch++] = L[best];
-                    } else {                          // parallel: every label
-                        for (int t = 0; t < nl; t++) chosen[nch++] = L[t];
-                    }
-                }
-            }
-            // selectivity-aware AND routing (f3, beyond the paper; include/vf.h): expected AND-set
-            // size of the greedy item under label independence, fp64, labels in ascending order
-            bool and_scan = false;
-            if (a.and_scan_thr > 0 && a.op == 2 && a.recall_mode == 0 && nch == 1 && nl > 1) {
-                double est = (double)lsize(chosen[0]);
-                for (int t = 0; t < nl; t++)
-                    if (L[t] != chosen[0]) est = __ddiv_rn(__dmul_rn(est, (double)lsize(L[t])), (double)ix.n_points);
-                and_scan = est < (double)a.and_scan_thr;
-            }
-            for (int t = 0; t < nch; t++) {           // routing equation
-                const int32_t s = lsize(chosen[t]);
-                cpath[t] = (a.exact || s < a.scan_thr || and_scan) ? PATH_SCAN : PATH_GRAPH;
-                // label sharding: an item whose label lives on another rank is shipped there
-                if (ix.owner && ix.owner[chosen[t]] != ix.rank) cpath[t] |= META_REMOTE;
-                ngraph += cpath[t] == PATH_GRAPH;
-            }
+            route_labels(a, L, nraw, &nl, chosen, cpath, &nch, &pred);
+            for (int t = 0; t < nch; t++) ngraph += cpath[t] == PATH_GRAPH;
             QueryInfo qi;
             qi.nl = nl; qi.n_items = nch; qi.qh = qh; qi.pad = 0;
             a.qinfo[q] = qi;

@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "host_internal.h"
+#include "small.h"
 
 namespace vf {
 int scan_qg(int row_bytes, int k);
@@ -444,6 +445,17 @@ extern "C" vf_status vf_set_profiling(vf_index *index, int32_t enable) {
 // ------------------------------------------------------------------ search (Alg. 2)
 namespace vf {
 
+// Visited-set geometry of one beam search: a shared-memory table within ~7 KB per warp and an exact
+// global overflow table large enough for every vertex the search can visit.
+void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slots, uint64_t *gslots) {
+    int hs = 1024;
+    const int64_t budget = 7168 - 16ll * itopk - 1024;
+    while (hs < 64 * itopk && hs < 8192 && (int64_t)hs * 2 * 4 <= budget) hs <<= 1;
+    const int64_t v_bound = (int64_t)n_init + (int64_t)max_iter * w * R + 32;
+    *hash_slots = hs;
+    *gslots = pow2ceil((uint64_t)(2 * v_bound + 64));
+}
+
 vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, const vf_search_params *p,
                       cudaStream_t s, Plan *out) {
     const DevIndex &D = ix->dev;
@@ -480,14 +492,9 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl.max_tiles = slots * mtpl;
     const int n_init = p->n_init > 0 ? p->n_init : R * w;
     const int max_iter = p->max_iterations > 0 ? p->max_iterations : 2 * ((p->itopk + w - 1) / w) + 16;
-    // visited sets: a shared-memory table within ~7 KB per warp, exact global overflow table
-    int hs = 1024;
-    {
-        const int64_t budget = 7168 - 16ll * p->itopk - 1024;
-        while (hs < 64 * p->itopk && hs < 8192 && (int64_t)hs * 2 * 4 <= budget) hs <<= 1;
-    }
-    const int64_t v_bound = (int64_t)n_init + (int64_t)max_iter * w * R + 32;
-    const uint64_t gslots = pow2ceil((uint64_t)(2 * v_bound + 64));
+    int hs = 0;
+    uint64_t gslots = 0;
+    beam_sizes(p->itopk, w, R, n_init, max_iter, &hs, &gslots);
 
     SearchArgs &a = pl.a;
     a.ix = D;
@@ -682,6 +689,18 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     return VF_OK;
 }
 
+// Small batches take the per-query path (f1, small.cu) unless VF_SMALL_BATCH=0; VF_SMALL_BATCH=<n>
+// sets the largest batch that takes it (default kSmallMaxBatch).
+static bool use_small_path(vf_index *ix, const vf_search_params *p, int64_t n) {
+    static const int limit = [] {
+        const char *e = getenv("VF_SMALL_BATCH");
+        return e ? atoi(e) : kSmallMaxBatch;
+    }();
+    if (n <= 0 || n > limit || ix->world > 1) return false;
+    const DevIndex &F = ix->enc8 ? ix->dev8 : ix->dev;
+    return small_supported(F, ix->dev, ix->enc8, p->k);
+}
+
 static vf_status check_params(vf_index *ix, const vf_search_params *p) {
     if (!p) return fail(VF_ERR_INVALID_ARG, "params is NULL");
     if (p->k < 1 || p->k > kMaxK) return fail(VF_ERR_INVALID_ARG, "k must be in [1, 256]");
@@ -797,7 +816,9 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     if (!q_dev) VF_CUDA(cudaMemcpyAsync(sc->raw.p, queries, (size_t)n * raw_bytes, cudaMemcpyHostToDevice, s));
     if (off_dev) a.q_off = qoff;
     else VF_CUDA(cudaMemcpyAsync(sc->qoff.p, qoff, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
-    if (n_slots > 0)
+    // f1 per-query path (small.cu): small batches are answered by one launch, one CTA per query
+    const bool small_path = use_small_path(ix, p, n);
+    if (n_slots > 0 && !(small_path && lab_dev))    // the per-query path reads device labels in place
         VF_CUDA(cudaMemcpyAsync(sc->qlab.p, qlab, (size_t)n_slots * 4,
                                 lab_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     a.Qraw = q_dev ? reinterpret_cast<const uint8_t *>(queries) : sc->raw.as<uint8_t>();
@@ -805,10 +826,26 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     a.out_dists = out_dev ? out_dists : sc->out_dists.as<float>();
 
     int launches = 0;
-    st = run_local(ix, sc, pl, s, nullptr, 0, 0, &launches);
-    if (st != VF_OK) return st;
-    const bool need_merge = p->op == VF_OR || (p->op == VF_AND && p->recall_mode == VF_RECALL_PARALLEL);
-    if (need_merge) launches += launch_merge(a, s);
+    if (small_path) {
+        SearchArgs f = a;
+        if (ix->enc8) f.ix = ix->dev8;
+        if (lab_dev) f.qlab = const_cast<int32_t *>(qlab);
+        VF_CUDA(cudaMemsetAsync(sc->ctr.p, 0, sizeof(Counters), s));
+        if (prof) {
+            VF_CUDA(cudaEventRecord(sc->ev[1], s));
+            VF_CUDA(cudaEventRecord(sc->ev[2], s));
+            VF_CUDA(cudaEventRecord(sc->ev[3], s));
+        }
+        const int l = launch_small(f, D, ix->enc8, raw_bytes, s);
+        if (l < 0) return fail(VF_ERR_INTERNAL, "per-query kernel dispatch failed");
+        launches += l;
+        if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));
+    } else {
+        st = run_local(ix, sc, pl, s, nullptr, 0, 0, &launches);
+        if (st != VF_OK) return st;
+        const bool need_merge = p->op == VF_OR || (p->op == VF_AND && p->recall_mode == VF_RECALL_PARALLEL);
+        if (need_merge) launches += launch_merge(a, s);
+    }
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[5], s));
     VF_CUDA(cudaGetLastError());
     if (!out_dev) {
