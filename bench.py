@@ -442,6 +442,34 @@ def main():
                 res[mode] = {"p50_ms": 1e3 * float(np.percentile(ts, 50)),
                              "p99_ms": 1e3 * float(np.percentile(ts, 99))}
             latency[f"batch{bsz}"] = res
+        # f1: the persistent serving kernel (vf_serve_*) -- single-query latency (one job
+        # in flight, host query in, host result out) and single-batch-mode throughput (every query
+        # its own job, up to 1024 in flight), the two E13 measurements
+        try:
+            labs = [np.ascontiguousarray(w.q_lab[w.q_off[i]:w.q_off[i + 1]]) for i in range(min(n, 20000))]
+            Qn = np.ascontiguousarray(w.Q)
+            with ix.serve(k=k, itopk=itopk, search_width=w_, op=op, and_scan_threshold=as_, scan_threshold=st_,
+                          capacity=4096) as sv:
+                oi_, od_ = np.empty(k, np.int32), np.empty(k, np.float32)
+                ts = []
+                for it_ in range(args.lat_calls + 50):
+                    i = it_ % len(labs)
+                    t0 = time.perf_counter()
+                    sv.wait(sv.submit(Qn[i], labs[i]), oi_, od_)
+                    if it_ >= 50:
+                        ts.append(time.perf_counter() - t0)
+                # the whole batch, each query its own job, from a C client loop (vf_serve_run)
+                sv.run(Qn[:1024], w.q_off[:1025], w.q_lab[:w.q_off[1024]], max_in_flight=1024)
+                m_q = n
+                t0 = time.perf_counter()
+                sv.run(Qn, w.q_off, w.q_lab, max_in_flight=1024)
+                el = time.perf_counter() - t0
+                latency["serve"] = {"p50_ms": 1e3 * float(np.percentile(ts, 50)),
+                                    "p99_ms": 1e3 * float(np.percentile(ts, 99)),
+                                    "single_batch_qps": m_q / el, "in_flight": 1024,
+                                    "workers": sv.info()["n_workers"]}
+        except Exception as e:   # reported, not fatal: the batched numbers stand on their own
+            latency["serve"] = {"error": str(e)}
         log(f"latency: {latency}")
 
     # -- CPU baseline: the oracle on this host's cores, bounded sample, rank 0 only

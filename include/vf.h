@@ -257,6 +257,11 @@ vf_status vf_serve_submit(vf_server *server, const void *query, const int32_t *l
                           int64_t *ticket);
 vf_status vf_serve_wait(vf_server *server, int64_t ticket, int32_t *out_ids, float *out_dists);
 vf_status vf_serve_stop(vf_server *server);
+/* A client loop in C (single-batch mode): submits the n queries of a host batch as n
+ * separate jobs, at most max_in_flight (<= capacity) outstanding, and waits for each in order;
+ * results land in out_ids / out_dists (host, n*k). Same answers as n vf_serve_submit/wait pairs. */
+vf_status vf_serve_run(vf_server *server, int64_t n, const void *queries, const int64_t *qlabel_offsets,
+                       const int32_t *qlabels, int32_t max_in_flight, int32_t *out_ids, float *out_dists);
 vf_status vf_serve_info(const vf_server *server, int32_t *n_workers, int64_t *submitted);
 
 #ifdef __cplusplus

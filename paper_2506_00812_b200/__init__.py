@@ -23,6 +23,7 @@ OPS = {"single": VF_SINGLE, "or": VF_OR, "and": VF_AND}
 MODES = {"greedy": VF_RECALL_GREEDY, "parallel": VF_RECALL_PARALLEL}
 EXPORTED = ("vf_build_index", "vf_search", "vf_free", "vf_last_error", "vf_get_index_info",
             "vf_serve_start", "vf_serve_submit", "vf_serve_wait", "vf_serve_stop", "vf_serve_info",
+            "vf_serve_run",
             "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items", "vf_build_index_virtual_shards",
             "vf_partition_labels")
 
@@ -110,6 +111,8 @@ def lib():
         L.vf_serve_wait.argtypes = [p, i64, p, p]
         L.vf_serve_stop.restype = C.c_int
         L.vf_serve_stop.argtypes = [p]
+        L.vf_serve_run.restype = C.c_int
+        L.vf_serve_run.argtypes = [p, i64, p, p, p, i32, p, p]
         L.vf_serve_info.restype = C.c_int
         L.vf_serve_info.argtypes = [p, C.POINTER(i32), C.POINTER(i64)]
         L.vf_build_index_virtual_shards.restype = C.c_int
@@ -277,6 +280,20 @@ class Server:
         ids = np.empty(self.k, np.int32) if out_ids is None else out_ids
         d = np.empty(self.k, np.float32) if out_dists is None else out_dists
         _check(lib().vf_serve_wait(self._h, int(ticket), _ptr(ids), _ptr(d)))
+        return ids, d
+
+    def run(self, Q, q_off, q_lab, max_in_flight=1024):
+        """vf_serve_run: every query of a host batch as its own job (single-batch mode), in C."""
+        Q = np.ascontiguousarray(Q)
+        q_off = np.ascontiguousarray(q_off, np.int64)
+        q_lab = np.ascontiguousarray(q_lab, np.int32)
+        if q_lab.size == 0:
+            q_lab = np.zeros(1, np.int32)
+        n = len(q_off) - 1
+        ids = np.empty((n, self.k), np.int32)
+        d = np.empty((n, self.k), np.float32)
+        _check(lib().vf_serve_run(self._h, n, _ptr(Q), _ptr(q_off), _ptr(q_lab), int(max_in_flight), _ptr(ids),
+                                  _ptr(d)))
         return ids, d
 
     def info(self) -> dict:

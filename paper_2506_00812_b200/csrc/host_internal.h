@@ -61,6 +61,8 @@ struct Scratch {
         item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
     // label sharding: item records out / in, returned results, slots of the sent items
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
+    // per-query path (f1): per-CTA item lists of a query split over several CTAs, completion counters
+    DevBuf small_part, small_cnt;
     size_t gtab_slots = 0, gtab_warps = 0;
     // profiled searches record their phase events into a ring: ev points at the current set, so
     // the mean over every search since profiling was enabled (<= kProfRing of them) is readable

@@ -91,7 +91,7 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
     a.q8_row_bytes = ix->enc8 ? ix->dev8.row_bytes : 0;
     auto bail = [&](vf_status st) { free_server(sv); return st; };
 
-    int n = serve_max_ctas(a, ix->dev, sv->two_views);
+    int n = serve_max_ctas(a, ix->dev, sv->two_views) - 1;         // one slot for the dispatcher CTA
     if (n <= 0)
         return bail(fail(VF_ERR_INTERNAL, "serving kernel does not fit (" +
                                               std::string(n < 0 ? cudaGetErrorString((cudaError_t)-n) : "0 CTAs/SM") + ")"));
@@ -103,7 +103,7 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
         (e = cudaMemset(sv->gtab.p, 0, warps * gslots * 8 + warps * 4)) != cudaSuccess ||
         (e = sv->ctr.ensure(sizeof(Counters))) != cudaSuccess ||
         (e = cudaMemset(sv->ctr.p, 0, sizeof(Counters))) != cudaSuccess ||
-        (e = sv->next.ensure(8)) != cudaSuccess || (e = cudaMemset(sv->next.p, 0, 8)) != cudaSuccess)
+        (e = sv->next.ensure(64)) != cudaSuccess || (e = cudaMemset(sv->next.p, 0, 64)) != cudaSuccess)
         return bail(fail(VF_ERR_OUT_OF_MEMORY, std::string("serve buffers: ") + cudaGetErrorString(e)));
     a.gtab = sv->gtab.as<unsigned long long>();
     a.n_warp_slots = (int32_t)warps;
@@ -149,6 +149,8 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
     r.head = reinterpret_cast<const long long *>(dev + o_head);
     r.stop = reinterpret_cast<const int32_t *>(dev + o_stop);
     r.next = sv->next.as<unsigned long long>();
+    r.dev_head = reinterpret_cast<long long *>(sv->next.as<uint8_t>() + 16);
+    r.dev_stop = reinterpret_cast<int32_t *>(sv->next.as<uint8_t>() + 32);
 
     if ((e = cudaStreamCreateWithFlags(&sv->stream, cudaStreamNonBlocking)) != cudaSuccess)
         return bail(fail(VF_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e)));
@@ -205,6 +207,33 @@ extern "C" vf_status vf_serve_wait(vf_server *sv, int64_t ticket, int32_t *out_i
     std::memcpy(out_ids, sv->hids + slot * sv->k, (size_t)sv->k * 4);
     std::memcpy(out_dists, sv->hd + slot * sv->k, (size_t)sv->k * 4);
     if (*dn != ticket + 1) return fail(VF_ERR_INVALID_ARG, "ticket's results were overwritten (capacity exceeded)");
+    return VF_OK;
+}
+
+extern "C" vf_status vf_serve_run(vf_server *sv, int64_t n, const void *queries, const int64_t *qlabel_offsets,
+                                  const int32_t *qlabels, int32_t max_in_flight, int32_t *out_ids, float *out_dists) {
+    if (!sv || n < 0 || (n > 0 && (!queries || !qlabel_offsets || !out_ids || !out_dists)))
+        return fail(VF_ERR_INVALID_ARG, "NULL argument");
+    if (max_in_flight < 1 || max_in_flight > sv->cap) return fail(VF_ERR_INVALID_ARG, "max_in_flight must be in [1, capacity]");
+    const uint8_t *q = static_cast<const uint8_t *>(queries);
+    int64_t first = -1, waited = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (i - waited == max_in_flight) {
+            vf_status st = vf_serve_wait(sv, first + waited, out_ids + waited * sv->k, out_dists + waited * sv->k);
+            if (st != VF_OK) return st;
+            waited++;
+        }
+        int64_t t = 0;
+        const int64_t lo = qlabel_offsets[i];
+        vf_status st = vf_serve_submit(sv, q + i * sv->raw_bytes, qlabels + lo, (int32_t)(qlabel_offsets[i + 1] - lo), &t);
+        if (st != VF_OK) return st;
+        if (first < 0) first = t;
+        else if (t != first + i) return fail(VF_ERR_INVALID_ARG, "vf_serve_run needs the server to itself");
+    }
+    for (; waited < n; waited++) {
+        vf_status st = vf_serve_wait(sv, first + waited, out_ids + waited * sv->k, out_dists + waited * sv->k);
+        if (st != VF_OK) return st;
+    }
     return VF_OK;
 }
 

@@ -100,15 +100,17 @@ __device__ __forceinline__ ull merge_warp_lists(const ull *mrg, int k, int lane)
 template <int DT, int TEAM, int CPL>
 __device__ void small_scan_item(const SearchArgs &a, const DevIndex &v, const SmallLayout &L, const SmallSmem &s,
                                 const uint8_t *qrow, int32_t label, bool has_pred, int np, ull *out,
-                                uint32_t &bar_phase) {
+                                uint32_t &bar_phase, int part, int nparts) {
     typedef Acc<DT> A;
     constexpr int RP = 32 / TEAM;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int team = lane / TEAM, tl = lane % TEAM;
     const int k = a.k, chunks = v.chunks, rb = v.row_bytes;
     const LabelDir d = v.dir[label];
-    const int32_t S = d.size;
-    const bool hs = S >= v.T;
+    const bool hs = d.size >= v.T;
+    // this CTA's slice of the list (a small batch splits each scan item over nparts CTAs)
+    const int32_t rlo = (int32_t)((int64_t)d.size * part / nparts);
+    const int32_t S = (int32_t)((int64_t)d.size * (part + 1) / nparts) - rlo;
     uint4 qreg[CPL];
     const uint4 *q4 = reinterpret_cast<const uint4 *>(qrow);
 #pragma unroll
@@ -135,7 +137,7 @@ __device__ void small_scan_item(const SearchArgs &a, const DevIndex &v, const Sm
     const int32_t *P = s.lab;
     if (!hs) {
         // contiguous rows: TMA bulk stages of L.stage_rows rows
-        const uint8_t *src = v.Xls + d.base * (int64_t)rb;
+        const uint8_t *src = v.Xls + (d.base + rlo) * (int64_t)rb;
         const int SR = L.stage_rows, NS = L.n_stages;
         const int nst = (S + SR - 1) / SR;
         if (threadIdx.x == 0) {
@@ -158,8 +160,8 @@ __device__ void small_scan_item(const SearchArgs &a, const DevIndex &v, const Sm
                 const int r = rr + team;
                 const bool live = r < nr;
                 bool ok = live;
-                if (ok && has_pred) ok = verify_pred(v, __ldg(v.M_ls + d.base + r0 + r), P, np, label);
-                offer(r0 + r, reinterpret_cast<const uint4 *>(stg + (size_t)(live ? r : 0) * rb), ok);
+                if (ok && has_pred) ok = verify_pred(v, __ldg(v.M_ls + d.base + rlo + r0 + r), P, np, label);
+                offer(rlo + r0 + r, reinterpret_cast<const uint4 *>(stg + (size_t)(live ? r : 0) * rb), ok);
             }
             __syncthreads();                                   // stage consumed by every warp
             bar_phase ^= 1u << buf;                            // every thread tracks the parity
@@ -175,7 +177,7 @@ __device__ void small_scan_item(const SearchArgs &a, const DevIndex &v, const Sm
         for (int rr = wid * RP; rr < S; rr += kSmallWarps * RP) {
             const int r = rr + team;
             const bool live = r < S;
-            int32_t gid = live ? __ldg(v.M_hs + d.base + r) : 0;
+            int32_t gid = live ? __ldg(v.M_hs + d.base + rlo + r) : 0;
             bool ok = live;
             if (ok && has_pred) ok = verify_pred(v, gid, P, np, label);
             offer(gid, reinterpret_cast<const uint4 *>(v.X + (int64_t)(ok ? gid : 0) * rb), ok);
@@ -189,7 +191,7 @@ __device__ void small_scan_item(const SearchArgs &a, const DevIndex &v, const Sm
             m = (m & 0xFFFFFFFF00000000ull) | (uint32_t)__ldg(v.M_ls + d.base + (int32_t)(uint32_t)m);
         if (lane < k) out[lane] = m;
     }
-    if (threadIdx.x == 0) atomicAdd(&a.ctr->scan_rows, (ull)S);
+    if (threadIdx.x == 0 && S > 0) atomicAdd(&a.ctr->scan_rows, (ull)S);
     __syncthreads();
 }
 
@@ -199,19 +201,22 @@ __device__ void small_scan_item(const SearchArgs &a, const DevIndex &v, const Sm
 template <int DT, int TEAM, int CPL>
 __device__ void small_items(const SearchArgs &a, const DevIndex &v, const SmallLayout &L, const SmallSmem &s,
                             const uint8_t *qrow, ull *gtab_base, uint32_t *epochs, int warp_slot0,
-                            int32_t item_slot0, int32_t qid, uint32_t &bar_phase) {
+                            int32_t item_slot0, int32_t qid, uint32_t &bar_phase, int part, int nparts) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nl = s.misc[0], nch = s.misc[1];
     const bool has_pred = s.misc[3] != 0;
     const uint32_t qh = (uint32_t)s.misc[4];
+    for (int i = threadIdx.x; i < nch * kSmallMaxK; i += blockDim.x) s.res[i] = KEY_INF;
+    __syncthreads();
     for (int t = 0; t < nch; t++)
         if ((s.items[64 + t] & 3) == PATH_SCAN)
             small_scan_item<DT, TEAM, CPL>(a, v, L, s, qrow, s.items[t], has_pred, nl, s.res + t * kSmallMaxK,
-                                           bar_phase);
+                                           bar_phase, part, nparts);
     int g = 0;
     for (int t = 0; t < nch; t++) {
         if ((s.items[64 + t] & 3) != PATH_GRAPH) continue;
-        if (g++ % kSmallWarps != wid) continue;
+        const int gw = g++ % (kSmallWarps * nparts);      // graph items round robin over the warps
+        if (gw != part * kSmallWarps + wid) continue;       // of every CTA of the query
         const int32_t label = s.items[t];
         const LabelDir d = v.dir[label];
         BeamItem bi;
@@ -373,17 +378,44 @@ template <int DTF, int TF, int CF, int TS, int CS>
 __device__ void small_query(const SearchArgs &a, const DevIndex &native, const SmallLayout &L, uint8_t *smem,
                             const uint8_t *raw, int raw_bytes, const int32_t *lab, int nraw, int32_t qid,
                             int32_t item_slot0, int32_t *out_ids, float *out_d, int warp_slot0, uint32_t *epochs,
-                            uint32_t &bar_phase) {
+                            uint32_t &bar_phase, int part = 0, int nparts = 1, ull *partials = nullptr,
+                            int32_t *done_ctr = nullptr) {
     const SmallSmem s = small_smem(smem, L);
     const bool have_fast = TS > 0;   // a u8 row store in front of a fp32 index
     small_prepare(a, native, s, raw, raw_bytes, lab, nraw, have_fast);
     if (!have_fast || s.misc[2]) {
         small_items<DTF, TF, CF>(a, a.ix, L, s, have_fast ? s.qf : s.qs, a.gtab, epochs, warp_slot0, item_slot0,
-                                 qid, bar_phase);
+                                 qid, bar_phase, part, nparts);
     } else {
         // every index array of the fp32 view is read through `native`; `a` only supplies parameters
         small_items<1, (TS > 0 ? TS : 1), (CS > 0 ? CS : 1)>(a, native, L, s, s.qs, a.gtab, epochs, warp_slot0,
-                                                             item_slot0, qid, bar_phase);
+                                                             item_slot0, qid, bar_phase, part, nparts);
+    }
+    if (nparts > 1) {
+        // publish this CTA's per-item lists; the last CTA of the query merges all of them
+        const int nch = s.misc[1];
+        ull *mine = partials + (size_t)part * kMaxQueryLabels * kSmallMaxK;
+        for (int i = threadIdx.x; i < nch * kSmallMaxK; i += blockDim.x) mine[i] = s.res[i];
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s.misc[12] = atomicAdd(done_ctr, 1) == nparts - 1;
+        __syncthreads();
+        if (!s.misc[12]) return;                      // not the last: this CTA is done
+        __threadfence();
+        if ((threadIdx.x >> 5) == 0) {
+            const int lane = threadIdx.x & 31;
+            for (int t = 0; t < nch; t++) {
+                ull Li = KEY_INF;
+                for (int c = 0; c < nparts; c++) {
+                    const ull key = lane < a.k ? __ldcg(partials + ((size_t)c * kMaxQueryLabels + t) * kSmallMaxK + lane)
+                                               : KEY_INF;
+                    Li = warp_merge_topk(Li, key, a.k, lane);   // slices hold distinct rows
+                }
+                s.res[t * kSmallMaxK + lane] = Li;
+            }
+            if (lane == 0) *done_ctr = 0;                 // ready for the next search
+        }
+        __syncthreads();
     }
     if ((threadIdx.x >> 5) == 0) {
         const ull key = small_merge(s, a.k, threadIdx.x & 31);
@@ -403,9 +435,11 @@ __device__ __forceinline__ void small_init_bars(const SmallSmem &s, int n_stages
 // ---------------------------------------------------------------- k_small: one CTA per query
 template <int DTF, int TF, int CF, int TS, int CS>
 __global__ void __launch_bounds__(32 * kSmallWarps) k_small(SearchArgs a, DevIndex native, SmallLayout L,
-                                                            int raw_bytes, uint32_t *epochs) {
+                                                            int raw_bytes, uint32_t *epochs, int nparts,
+                                                            ull *partials, int32_t *done_ctr) {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int64_t q = blockIdx.x;
+    const int64_t q = blockIdx.x / nparts;
+    const int part = (int)(blockIdx.x % nparts);
     if (q >= a.n_q) return;
     const SmallSmem s = small_smem(smem, L);
     small_init_bars(s, L.n_stages);
@@ -414,18 +448,43 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_small(SearchArgs a, DevInd
     const int nraw = (int)(a.q_off[q + 1] - lo);
     small_query<DTF, TF, CF, TS, CS>(a, native, L, smem, a.Qraw + q * (int64_t)raw_bytes, raw_bytes, a.qlab + lo,
                                      nraw, (int32_t)q, (int32_t)lo, a.out_ids + q * a.k, a.out_dists + q * a.k,
-                                     (int)blockIdx.x * kSmallWarps, epochs, bar_phase);
+                                     (int)blockIdx.x * kSmallWarps, epochs, bar_phase, part, nparts,
+                                     partials + (size_t)q * nparts * kMaxQueryLabels * kSmallMaxK, done_ctr + q);
 }
 
 // ---------------------------------------------------------------- k_serve: the persistent kernel
 // Job j lives in slot j % cap of the host-mapped ring. The host writes the slot's query row and
-// labels, then publishes head = j + 1 (release). A CTA claims j from the device job counter, waits
-// for head > j (or stop), answers the query, writes ids / dists into the slot and publishes
-// done[slot] = j + 1 after a system-scope fence.
+// labels, then publishes head = j + 1 (release). The last CTA is the dispatcher: it alone polls the
+// host-mapped head / stop words over PCIe and mirrors them into device memory. Every other CTA
+// claims j from the device job counter, waits on the device mirror for head > j (or stop), answers
+// the query, writes ids / dists into the slot and publishes done[slot] = j + 1 after a system-scope
+// fence.
 template <int DTF, int TF, int CF, int TS, int CS>
 __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevIndex native, SmallLayout L,
                                                             int raw_bytes, uint32_t *epochs, ServeRing ring) {
     extern __shared__ __align__(128) uint8_t smem[];
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            long long last = -1;
+            for (;;) {
+                const int32_t st = *(volatile const int32_t *)ring.stop;
+                __threadfence_system();
+                const long long h = *(volatile const long long *)ring.head;
+                if (h != last) {
+                    *(volatile long long *)ring.dev_head = h;
+                    __threadfence();
+                    last = h;
+                }
+                if (st) {
+                    *(volatile int32_t *)ring.dev_stop = 1;
+                    __threadfence();
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+        return;
+    }
     const SmallSmem s = small_smem(smem, L);
     small_init_bars(s, L.n_stages);
     uint32_t bar_phase = 0;
@@ -433,12 +492,17 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
     for (;;) {                                                      // size may use all 227 KB
         if (threadIdx.x == 0) {
             long long j = (long long)atomicAdd(ring.next, 1ull);
-            // wait until the host has published job j, or stop
+            // wait until job j is published (device mirror of the host head), or stop
             for (;;) {
-                const long long h = *(volatile long long *)ring.head;
+                const long long h = *(volatile long long *)ring.dev_head;
                 if (h > j) break;
-                if (*(volatile int32_t *)ring.stop) { j = -1; break; }
-                __nanosleep(256);
+                if (*(volatile int32_t *)ring.dev_stop) {
+                    __threadfence();
+                    if (*(volatile long long *)ring.dev_head > j) break;
+                    j = -1;
+                    break;
+                }
+                __nanosleep(32);
             }
             *s_job = j;
         }
@@ -459,7 +523,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
         __syncthreads();
         small_query<DTF, TF, CF, TS, CS>(a, native, L, smem, rawbuf, raw_bytes, labbuf, nraw, -1, -1,
                                          ring.out_ids + (int64_t)slot * a.k, ring.out_dists + (int64_t)slot * a.k,
-                                         (int)blockIdx.x * kSmallWarps, epochs, bar_phase);
+                                         (int)(blockIdx.x - 1) * kSmallWarps, epochs, bar_phase);
         __threadfence_system();
         if (threadIdx.x == 0) *(volatile long long *)(ring.done + slot) = j + 1;
         __syncthreads();
@@ -467,7 +531,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
 }
 
 // ---------------------------------------------------------------- dispatch
-typedef void (*small_fn)(SearchArgs, DevIndex, SmallLayout, int, uint32_t *);
+typedef void (*small_fn)(SearchArgs, DevIndex, SmallLayout, int, uint32_t *, int, ull *, int32_t *);
 typedef void (*serve_fn)(SearchArgs, DevIndex, SmallLayout, int, uint32_t *, ServeRing);
 
 struct SmallPick { small_fn f; serve_fn g; };
@@ -509,13 +573,15 @@ static void set_smem_attr(const void *f) {
     if (nd < 32) done[nd++] = f;
 }
 
-int launch_small(const SearchArgs &a, const DevIndex &native, bool two_views, int raw_bytes, cudaStream_t s) {
+int launch_small(const SearchArgs &a, const DevIndex &native, bool two_views, int raw_bytes, int nparts,
+                 unsigned long long *partials, int32_t *done_ctr, cudaStream_t s) {
     const SmallPick p = small_kernel(a.ix, native, two_views);
     if (!p.f || a.n_q <= 0) return a.n_q <= 0 ? 0 : -1;
     const SmallLayout L = small_layout(a.itopk, a.hash_slots, native.row_bytes, two_views ? a.ix.row_bytes : 16, a.k);
     set_smem_attr((const void *)p.f);
     uint32_t *epochs = reinterpret_cast<uint32_t *>(a.gtab + (size_t)a.n_warp_slots * a.gtab_slots);
-    p.f<<<(unsigned)a.n_q, 32 * kSmallWarps, L.bytes, s>>>(a, native, L, raw_bytes, epochs);
+    p.f<<<(unsigned)(a.n_q * nparts), 32 * kSmallWarps, L.bytes, s>>>(a, native, L, raw_bytes, epochs, nparts,
+                                                                      partials, done_ctr);
     return 1;
 }
 
@@ -526,7 +592,7 @@ int launch_serve(const SearchArgs &a, const DevIndex &native, bool two_views, in
     const SmallLayout L = small_layout(a.itopk, a.hash_slots, native.row_bytes, two_views ? a.ix.row_bytes : 16, a.k);
     set_smem_attr((const void *)p.g);
     uint32_t *epochs = reinterpret_cast<uint32_t *>(a.gtab + (size_t)a.n_warp_slots * a.gtab_slots);
-    p.g<<<n_ctas, 32 * kSmallWarps, L.bytes, s>>>(a, native, L, raw_bytes, epochs, ring);
+    p.g<<<n_ctas + 1, 32 * kSmallWarps, L.bytes, s>>>(a, native, L, raw_bytes, epochs, ring);   // + dispatcher
     return 1;
 }
 

@@ -37,10 +37,14 @@ struct ServeRing {
     const long long *head;              // jobs published by the host
     const int32_t *stop;                // 1: exit when no published job is pending
     unsigned long long *next;           // device job counter
+    long long *dev_head;                // device mirror of head (written by the dispatcher CTA)
+    int32_t *dev_stop;                  // device mirror of stop
 };
 
 bool small_supported(const DevIndex &fast, const DevIndex &native, bool two_views, int k);
-int launch_small(const SearchArgs &a, const DevIndex &native, bool two_views, int raw_bytes, cudaStream_t s);
+// nparts CTAs per query (grid n * nparts); partials: [n][nparts][64][32] keys, done_ctr: [n] zeroed
+int launch_small(const SearchArgs &a, const DevIndex &native, bool two_views, int raw_bytes, int nparts,
+                 unsigned long long *partials, int32_t *done_ctr, cudaStream_t s);
 int launch_serve(const SearchArgs &a, const DevIndex &native, bool two_views, int raw_bytes, int n_ctas,
                  const ServeRing &ring, cudaStream_t s);
 int serve_max_ctas(const SearchArgs &a, const DevIndex &native, bool two_views);

@@ -836,7 +836,15 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
             VF_CUDA(cudaEventRecord(sc->ev[2], s));
             VF_CUDA(cudaEventRecord(sc->ev[3], s));
         }
-        const int l = launch_small(f, D, ix->enc8, raw_bytes, s);
+        // a small batch spreads each query over several CTAs (scan items split by rows, graph items
+        // round robin over the CTAs' warps) so that one query can use several SMs
+        const int nparts = (int)std::max<int64_t>(1, std::min<int64_t>(8, 148 / n));
+        bool fresh = false;
+        VF_CUDA(sc->small_part.ensure((size_t)n * nparts * kMaxQueryLabels * kSmallMaxK * 8));
+        VF_CUDA(sc->small_cnt.ensure((size_t)std::max<int64_t>(n, kSmallMaxBatch) * 4 + 256, &fresh));
+        if (fresh) VF_CUDA(cudaMemsetAsync(sc->small_cnt.p, 0, sc->small_cnt.n, s));
+        const int l = launch_small(f, D, ix->enc8, raw_bytes, nparts, sc->small_part.as<unsigned long long>(),
+                                   sc->small_cnt.as<int32_t>(), s);
         if (l < 0) return fail(VF_ERR_INTERNAL, "per-query kernel dispatch failed");
         launches += l;
         if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));

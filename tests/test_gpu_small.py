@@ -219,3 +219,13 @@ def test_serve_rejects_bad_arguments(vf, tiny):
         t = sv.submit(w.Q[0], w.q_lab[:1])
         ids, _ = sv.wait(t)
         assert ids.shape == (5,)
+
+
+def test_serve_run_single_batch_mode(vf, tiny):
+    """vf_serve_run: a host batch submitted as one job per query (C client loop) equals vf_search."""
+    w, go, gi = tiny
+    g = vf.Index(w.X, w.post_off, w.post_ids, w.cfg.threshold_T, w.cfg.degree_R, go, gi)
+    a, ad = g.search(w.Q, w.q_off, w.q_lab, k=10, itopk=48)
+    with g.serve(k=10, itopk=48, capacity=256) as sv:
+        b, bd = sv.run(w.Q, w.q_off, w.q_lab, max_in_flight=200)
+    assert (a == b).all() and (ad == bd).all()
