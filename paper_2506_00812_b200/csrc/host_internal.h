@@ -63,6 +63,9 @@ struct Scratch {
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
     // per-query path (f1): per-CTA item lists of a query split over several CTAs, completion counters
     DevBuf small_part, small_cnt;
+    // scan / graph overlap: the graph kernels run on a side stream forked after routing
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     size_t gtab_slots = 0, gtab_warps = 0;
     // profiled searches record their phase events into a ring: ev points at the current set, so
     // the mean over every search since profiling was enabled (<= kProfRing of them) is readable
@@ -73,6 +76,8 @@ struct Scratch {
     int64_t prof_n = 0, prof_first = 0;
     bool ev_ok = false;
     bool profiled = false;
+    bool overlapped = false;        // last search ran scan and graph concurrently (phases overlap)
+    bool evov[kProfRing] = {};      // per profiled search: graph phase = ev[2] -> ev[7] (side stream)
     SearchArgs last{};
     int64_t last_slots = 0;
     int last_launches = 0;
@@ -81,6 +86,9 @@ struct Scratch {
         if (ev_ok)
             for (auto &set : evs)
                 for (auto &e : set) cudaEventDestroy(e);
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
     }
 };
 

@@ -993,7 +993,8 @@ bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *
     return ok;
 }
 
-int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x) {
+int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x,
+                   int ctas_per_sm) {
     if (max_tiles_bound <= 0) return 0;
     const TcLayout SL = tc_layout(a.ix.row_bytes, a.k);
     if (SL.nst < 2) return -1;
@@ -1006,7 +1007,7 @@ int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, con
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cached_dev[a.ix.dtype] = dev;
     }
-    int grid = cached_nsm * SL.ctas;
+    int grid = cached_nsm * (ctas_per_sm > 0 && ctas_per_sm < SL.ctas ? ctas_per_sm : SL.ctas);
     if (grid > max_tiles_bound) grid = max_tiles_bound;
     f<<<grid, kTcThreads, SL.total, s>>>(a, SL, *reinterpret_cast<const CUtensorMap *>(tm_ls),
                                          *reinterpret_cast<const CUtensorMap *>(tm_x));

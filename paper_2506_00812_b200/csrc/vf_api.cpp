@@ -648,6 +648,24 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     if (pl.filter) nl += launch_hs_filter(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
+    // scan and graph items are independent (Alg. 2 L418 / L428): the graph kernels run on a side
+    // stream concurrently with the scan; graph CTAs take whatever each SM has left and pull items
+    // dynamically. VF_OVERLAP=0 serialises them (A/B knobs: VF_TC_CTAS, VF_GRAPH_FIRST,
+    // VF_GRAPH_PER_SM; scripts/ab_overlap.sh).
+    static const int overlap_env = [] { const char *e = getenv("VF_OVERLAP"); return e ? atoi(e) : 1; }();
+    static const int tc_ctas_env = [] { const char *e = getenv("VF_TC_CTAS"); return e ? atoi(e) : 2; }();
+    const bool overlap = overlap_env != 0 && pl.tc;
+    cudaStream_t gs = s;
+    if (overlap) {
+        if (!sc->side) {
+            VF_CUDA(cudaStreamCreateWithFlags(&sc->side, cudaStreamNonBlocking));
+            VF_CUDA(cudaEventCreateWithFlags(&sc->ev_fork, cudaEventDisableTiming));
+            VF_CUDA(cudaEventCreateWithFlags(&sc->ev_join, cudaEventDisableTiming));
+        }
+        VF_CUDA(cudaEventRecord(sc->ev_fork, s));
+        VF_CUDA(cudaStreamWaitEvent(sc->side, sc->ev_fork, 0));
+        gs = sc->side;
+    }
     // Fast kernels gated on "no query outside the exact range" (gate 1), the fp32 FFMA kernels on
     // the opposite (gate 2); without a range check only the fast set runs (gate 0).
     SearchArgs fast = a, slow = a;
@@ -658,31 +676,57 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     }
     fast.gate = pl.checked ? 1 : 0;
     slow.gate = 2;
-    int sl = pl.tc ? launch_scan_tc(fast, s, tb, ix->tm_ls, ix->tm_x) : launch_scan(fast, s, tb);
-    if (sl >= 0 && pl.wsplit) {
-        const int s3 = launch_scan_warp(fast, s, tb);
-        sl = s3 < 0 ? s3 : sl + s3;
+    static const int graph_first_env = [] { const char *e = getenv("VF_GRAPH_FIRST"); return e ? atoi(e) : 0; }();
+    static const int graph_per_sm_env = [] { const char *e = getenv("VF_GRAPH_PER_SM"); return e ? atoi(e) : 0; }();
+    auto launch_scans = [&]() -> int {
+        int sl = pl.tc ? launch_scan_tc(fast, s, tb, ix->tm_ls, ix->tm_x, overlap ? tc_ctas_env : 0)
+                       : launch_scan(fast, s, tb);
+        if (sl >= 0 && pl.wsplit) {
+            const int s3 = launch_scan_warp(fast, s, tb);
+            sl = s3 < 0 ? s3 : sl + s3;
+        }
+        if (sl >= 0 && pl.checked) {
+            const int s2 = launch_scan(slow, s, tb);
+            sl = s2 < 0 ? s2 : sl + s2;
+        }
+        return sl;
+    };
+    auto launch_graphs = [&]() -> int {
+        const int gb = (int)std::min<int64_t>(pl.n_slots, INT32_MAX);
+        auto cap = [&](int ctas) { return overlap && graph_per_sm_env > 0 ? std::min(ctas, graph_per_sm_env * 148) : ctas; };
+        int gl;
+        if (ix->enc8) {
+            gl = launch_graph(fast, gs, gb, cap(pl.graph_ctas8));
+            const int g2 = gl < 0 ? 0 : launch_graph(slow, gs, gb, cap(pl.graph_ctas));
+            gl = g2 < 0 ? g2 : gl + g2;
+        } else {
+            SearchArgs ga = a;
+            ga.gate = 0;
+            gl = launch_graph(ga, gs, gb, cap(pl.graph_ctas));
+        }
+        return gl;
+    };
+    int gl = 0;
+    if (overlap && graph_first_env) {
+        gl = launch_graphs();
+        if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
     }
-    if (sl >= 0 && pl.checked) {
-        const int s2 = launch_scan(slow, s, tb);
-        sl = s2 < 0 ? s2 : sl + s2;
-    }
+    const int sl = launch_scans();
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));
-    const int gb = (int)std::min<int64_t>(pl.n_slots, INT32_MAX);
-    int gl;
-    if (ix->enc8) {
-        gl = launch_graph(fast, s, gb, pl.graph_ctas8);
-        const int g2 = gl < 0 ? 0 : launch_graph(slow, s, gb, pl.graph_ctas);
-        gl = g2 < 0 ? g2 : gl + g2;
-    } else {
-        SearchArgs ga = a;
-        ga.gate = 0;
-        gl = launch_graph(ga, s, gb, pl.graph_ctas);
+    if (!(overlap && graph_first_env)) {
+        gl = launch_graphs();
+        if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
     }
-    if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
     nl += gl;
+    if (overlap) {
+        if (prof) VF_CUDA(cudaEventRecord(sc->ev[7], gs));     // graph phase end (side stream)
+        VF_CUDA(cudaEventRecord(sc->ev_join, gs));
+        VF_CUDA(cudaStreamWaitEvent(s, sc->ev_join, 0));
+    }
+    sc->overlapped = overlap;
+    if (prof) sc->evov[sc->prof_n % Scratch::kProfRing] = overlap;
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[4], s));
     VF_CUDA(cudaGetLastError());
     *launches += nl;
@@ -896,11 +940,12 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->graph_V_max = (int64_t)c.graph_V_max;
     st->kernel_launches = sc->last_launches;
     st->row_bytes = ix->enc8 && !c.exact_fallback ? ix->dev8.row_bytes : ix->dev.row_bytes;   // rows the kernels read
-    auto phases = [](cudaEvent_t *e, double *out) {
+    // with scan / graph overlap the graph phase runs from the fork (ev[2]) to its own end (ev[7])
+    auto phases = [](cudaEvent_t *e, bool ov, double *out) {
         float t;
         cudaEventElapsedTime(&t, e[1], e[2]); out[0] = t;
         cudaEventElapsedTime(&t, e[2], e[3]); out[1] = t;
-        cudaEventElapsedTime(&t, e[3], e[4]); out[2] = t;
+        cudaEventElapsedTime(&t, ov ? e[2] : e[3], ov ? e[7] : e[4]); out[2] = t;
         cudaEventElapsedTime(&t, e[4], e[5]); out[3] = t;
         float c0, c1;
         cudaEventElapsedTime(&c0, e[0], e[1]);
@@ -910,13 +955,13 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     };
     if (sc->profiled && sc->prof_n > 0) {
         double v[6];
-        phases(sc->evs[(sc->prof_n - 1) % Scratch::kProfRing], v);
+        phases(sc->evs[(sc->prof_n - 1) % Scratch::kProfRing], sc->evov[(sc->prof_n - 1) % Scratch::kProfRing], v);
         st->ms_route = v[0]; st->ms_scan = v[1]; st->ms_graph = v[2];
         st->ms_merge = v[3]; st->ms_copy = v[4]; st->ms_total = v[5];
         const int64_t lo = std::max(sc->prof_first, sc->prof_n - Scratch::kProfRing);
         double sum[6] = {0, 0, 0, 0, 0, 0};
         for (int64_t i = lo; i < sc->prof_n; i++) {
-            phases(sc->evs[i % Scratch::kProfRing], v);
+            phases(sc->evs[i % Scratch::kProfRing], sc->evov[i % Scratch::kProfRing], v);
             for (int j = 0; j < 6; j++) sum[j] += v[j];
         }
         const int64_t m = sc->prof_n - lo;

@@ -211,7 +211,9 @@ int launch_scan_warp(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);
 // a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
 int scan_tc_qg(int row_bytes, int k);
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x);
-int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x);
+// ctas_per_sm: 0 = the layout's own choice (2 when it fits), 1 = leave room for a concurrent kernel
+int launch_scan_tc(const SearchArgs &a, cudaStream_t s, int max_tiles_bound, const void *tm_ls, const void *tm_x,
+                   int ctas_per_sm = 0);
 void launch_row_norms(int dtype, const uint8_t *X, int row_bytes, const int32_t *ids, int64_t n, uint32_t *out,
                       cudaStream_t s);
 float tf32_exact_vmax(int dim);
