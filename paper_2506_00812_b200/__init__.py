@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvecflow.so")
+LIB_PATH = os.environ.get("VF_LIB") or os.path.join(_HERE, "libvecflow.so")   # VF_LIB: A/B builds
 
 VF_OK, VF_ERR_INVALID_ARG, VF_ERR_OUT_OF_MEMORY, VF_ERR_CUDA, VF_ERR_NCCL, VF_ERR_INTERNAL = range(6)
 VF_U8, VF_F32 = 0, 1

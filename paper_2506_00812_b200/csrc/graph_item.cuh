@@ -19,6 +19,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef VF_PREFETCH_ADJ
+#define VF_PREFETCH_ADJ 1
+#endif
+
 namespace vf {
 
 struct GraphLayout {
@@ -225,6 +229,12 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
         const unsigned sm = __ballot_sync(FULL, ck != KEY_INF);
         const int ns = __popc(sm);
         if (ns == 0) return;
+#if VF_PREFETCH_ADJ
+        // a child entering Top is a future parent: start its adjacency row on its way to L2 now, so
+        // the expansion's dependent load hits L2 instead of DRAM
+        if (ck != KEY_INF)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ix.G + (base + (int64_t)((uint32_t)ck >> 1)) * R));
+#endif
         if (M <= 32) {
             // Top fits one key per lane: merge in registers (no shared-memory rank search)
             ull Li = lane < ntop ? cur[lane] : KEY_INF;
