@@ -464,7 +464,8 @@ def main():
                 t0 = time.perf_counter()
                 sv.run(Qn, w.q_off, w.q_lab, max_in_flight=1024)
                 el = time.perf_counter() - t0
-                latency["serve"] = {"p50_ms": 1e3 * float(np.percentile(ts, 50)),
+                latency["serve"] = {"device_means_us": sv.stats(),
+                                    "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                                     "p99_ms": 1e3 * float(np.percentile(ts, 99)),
                                     "single_batch_qps": m_q / el, "in_flight": 1024,
                                     "workers": sv.info()["n_workers"]}

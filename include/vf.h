@@ -263,6 +263,10 @@ vf_status vf_serve_stop(vf_server *server);
 vf_status vf_serve_run(vf_server *server, int64_t n, const void *queries, const int64_t *qlabel_offsets,
                        const int32_t *qlabels, int32_t max_in_flight, int32_t *out_ids, float *out_dists);
 vf_status vf_serve_info(const vf_server *server, int32_t *n_workers, int64_t *submitted);
+/* Mean per answered job part (device globaltimer): time a worker CTA waited for its job to be
+ * published, copied the slot from host memory, and searched + published; parts answered. */
+vf_status vf_serve_stats(vf_server *server, double *wait_us, double *copy_us, double *search_us,
+                         int64_t *parts_done);
 
 #ifdef __cplusplus
 }

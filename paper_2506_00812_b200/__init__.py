@@ -23,7 +23,7 @@ OPS = {"single": VF_SINGLE, "or": VF_OR, "and": VF_AND}
 MODES = {"greedy": VF_RECALL_GREEDY, "parallel": VF_RECALL_PARALLEL}
 EXPORTED = ("vf_build_index", "vf_search", "vf_free", "vf_last_error", "vf_get_index_info",
             "vf_serve_start", "vf_serve_submit", "vf_serve_wait", "vf_serve_stop", "vf_serve_info",
-            "vf_serve_run",
+            "vf_serve_run", "vf_serve_stats",
             "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items", "vf_build_index_virtual_shards",
             "vf_partition_labels")
 
@@ -113,6 +113,9 @@ def lib():
         L.vf_serve_stop.argtypes = [p]
         L.vf_serve_run.restype = C.c_int
         L.vf_serve_run.argtypes = [p, i64, p, p, p, i32, p, p]
+        L.vf_serve_stats.restype = C.c_int
+        L.vf_serve_stats.argtypes = [p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(i64)]
         L.vf_serve_info.restype = C.c_int
         L.vf_serve_info.argtypes = [p, C.POINTER(i32), C.POINTER(i64)]
         L.vf_build_index_virtual_shards.restype = C.c_int
@@ -295,6 +298,11 @@ class Server:
         _check(lib().vf_serve_run(self._h, n, _ptr(Q), _ptr(q_off), _ptr(q_lab), int(max_in_flight), _ptr(ids),
                                   _ptr(d)))
         return ids, d
+
+    def stats(self) -> dict:
+        w, c, s, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+        _check(lib().vf_serve_stats(self._h, C.byref(w), C.byref(c), C.byref(s), C.byref(n)))
+        return {"wait_us": w.value, "copy_us": c.value, "search_us": s.value, "parts": n.value}
 
     def info(self) -> dict:
         n, s = C.c_int32(), C.c_int64()

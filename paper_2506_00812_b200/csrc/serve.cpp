@@ -5,6 +5,7 @@
 // the slot's done word. The device side is k_serve (small.cu), the same per-query body as k_small.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <immintrin.h>
 #include <mutex>
@@ -26,7 +27,8 @@ struct vf_server {
     float *hd = nullptr;
     long long *hdone = nullptr, *hhead = nullptr;
     vf::ServeRing ring{};
-    vf::DevBuf next, gtab, ctr;
+    vf::DevBuf next, gtab, ctr, partials, part_done, dring;
+    int nparts = 1;
     cudaStream_t stream = nullptr;
     int64_t submitted = 0;
     std::mutex mu;
@@ -103,8 +105,18 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
         (e = cudaMemset(sv->gtab.p, 0, warps * gslots * 8 + warps * 4)) != cudaSuccess ||
         (e = sv->ctr.ensure(sizeof(Counters))) != cudaSuccess ||
         (e = cudaMemset(sv->ctr.p, 0, sizeof(Counters))) != cudaSuccess ||
-        (e = sv->next.ensure(64)) != cudaSuccess || (e = cudaMemset(sv->next.p, 0, 64)) != cudaSuccess)
+        (e = sv->next.ensure(128)) != cudaSuccess || (e = cudaMemset(sv->next.p, 0, 128)) != cudaSuccess)
         return bail(fail(VF_ERR_OUT_OF_MEMORY, std::string("serve buffers: ") + cudaGetErrorString(e)));
+    // a job is answered by nparts CTAs together (VF_SERVE_PARTS, default 2): scan items split by
+    // rows, graph items spread over the CTAs' warps, the last CTA merges and publishes
+    {
+        const char *e = getenv("VF_SERVE_PARTS");
+        sv->nparts = std::max(1, std::min(8, e ? atoi(e) : 2));   // see DESIGN.md §6 (k_serve)
+    }
+    const size_t pbytes = (size_t)capacity * sv->nparts * kServeLabels * kSmallMaxK * 8;
+    if ((e = sv->partials.ensure(pbytes)) != cudaSuccess || (e = sv->part_done.ensure((size_t)capacity * 4)) != cudaSuccess ||
+        (e = cudaMemset(sv->part_done.p, 0, (size_t)capacity * 4)) != cudaSuccess)
+        return bail(fail(VF_ERR_OUT_OF_MEMORY, std::string("serve partials: ") + cudaGetErrorString(e)));
     a.gtab = sv->gtab.as<unsigned long long>();
     a.n_warp_slots = (int32_t)warps;
     a.ctr = sv->ctr.as<Counters>();
@@ -149,6 +161,18 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
     r.head = reinterpret_cast<const long long *>(dev + o_head);
     r.stop = reinterpret_cast<const int32_t *>(dev + o_stop);
     r.next = sv->next.as<unsigned long long>();
+    {
+        const size_t dq = (size_t)capacity * sv->raw_stride, dl = (size_t)capacity * kServeLabels * 4;
+        if ((e = sv->dring.ensure(dq + dl + (size_t)capacity * 4)) != cudaSuccess)
+            return bail(fail(VF_ERR_OUT_OF_MEMORY, std::string("serve ring: ") + cudaGetErrorString(e)));
+        r.dq = sv->dring.as<uint8_t>();
+        r.dlab = reinterpret_cast<int32_t *>(sv->dring.as<uint8_t>() + dq);
+        r.dnlab = reinterpret_cast<int32_t *>(sv->dring.as<uint8_t>() + dq + dl);
+    }
+    r.nparts = sv->nparts;
+    r.stats = reinterpret_cast<unsigned long long *>(sv->next.as<uint8_t>() + 64);
+    r.partials = sv->partials.as<unsigned long long>();
+    r.part_done = sv->part_done.as<int32_t>();
     r.dev_head = reinterpret_cast<long long *>(sv->next.as<uint8_t>() + 16);
     r.dev_stop = reinterpret_cast<int32_t *>(sv->next.as<uint8_t>() + 32);
 
@@ -250,6 +274,25 @@ extern "C" vf_status vf_serve_stop(vf_server *sv) {
     }
     free_server(sv);
     return st;
+}
+
+extern "C" vf_status vf_serve_stats(vf_server *sv, double *wait_us, double *copy_us, double *search_us,
+                                    int64_t *parts_done) {
+    if (!sv) return fail(VF_ERR_INVALID_ARG, "NULL server");
+    unsigned long long h[4] = {0, 0, 0, 0};
+    // a copy on a side stream: the serving stream never completes while the kernel runs
+    cudaStream_t st;
+    VF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaError_t e = cudaMemcpyAsync(h, sv->ring.stats, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (e != cudaSuccess) return fail(VF_ERR_CUDA, std::string("serve stats: ") + cudaGetErrorString(e));
+    const double n = h[3] ? (double)h[3] : 1.0;
+    if (wait_us) *wait_us = h[0] / n / 1e3;
+    if (copy_us) *copy_us = h[1] / n / 1e3;
+    if (search_us) *search_us = h[2] / n / 1e3;
+    if (parts_done) *parts_done = (int64_t)h[3];
+    return VF_OK;
 }
 
 extern "C" vf_status vf_serve_info(const vf_server *sv, int32_t *n_workers, int64_t *submitted) {

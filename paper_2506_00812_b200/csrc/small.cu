@@ -12,6 +12,10 @@
 #include "graph_item.cuh"
 #include "small.h"
 
+#ifndef VF_SERVE_SYSLD
+#define VF_SERVE_SYSLD 0
+#endif
+
 namespace vf {
 
 // ---------------------------------------------------------------- shared-memory layout
@@ -374,12 +378,14 @@ __device__ __forceinline__ void small_finish(const SearchArgs &a, const SmallSme
 }
 
 // One whole query by the CTA: prepare, items on the fast or native view, merge, output.
+// Returns true in the CTA that wrote the query's results (with nparts > 1: the last to finish).
+// partials: [nparts][pstride][kSmallMaxK] keys (pstride >= the query's item count).
 template <int DTF, int TF, int CF, int TS, int CS>
-__device__ void small_query(const SearchArgs &a, const DevIndex &native, const SmallLayout &L, uint8_t *smem,
+__device__ bool small_query(const SearchArgs &a, const DevIndex &native, const SmallLayout &L, uint8_t *smem,
                             const uint8_t *raw, int raw_bytes, const int32_t *lab, int nraw, int32_t qid,
                             int32_t item_slot0, int32_t *out_ids, float *out_d, int warp_slot0, uint32_t *epochs,
                             uint32_t &bar_phase, int part = 0, int nparts = 1, ull *partials = nullptr,
-                            int32_t *done_ctr = nullptr) {
+                            int32_t *done_ctr = nullptr, int pstride = kMaxQueryLabels) {
     const SmallSmem s = small_smem(smem, L);
     const bool have_fast = TS > 0;   // a u8 row store in front of a fp32 index
     small_prepare(a, native, s, raw, raw_bytes, lab, nraw, have_fast);
@@ -394,20 +400,20 @@ __device__ void small_query(const SearchArgs &a, const DevIndex &native, const S
     if (nparts > 1) {
         // publish this CTA's per-item lists; the last CTA of the query merges all of them
         const int nch = s.misc[1];
-        ull *mine = partials + (size_t)part * kMaxQueryLabels * kSmallMaxK;
+        ull *mine = partials + (size_t)part * pstride * kSmallMaxK;
         for (int i = threadIdx.x; i < nch * kSmallMaxK; i += blockDim.x) mine[i] = s.res[i];
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) s.misc[12] = atomicAdd(done_ctr, 1) == nparts - 1;
         __syncthreads();
-        if (!s.misc[12]) return;                      // not the last: this CTA is done
+        if (!s.misc[12]) return false;                // not the last: this CTA is done
         __threadfence();
         if ((threadIdx.x >> 5) == 0) {
             const int lane = threadIdx.x & 31;
             for (int t = 0; t < nch; t++) {
                 ull Li = KEY_INF;
                 for (int c = 0; c < nparts; c++) {
-                    const ull key = lane < a.k ? __ldcg(partials + ((size_t)c * kMaxQueryLabels + t) * kSmallMaxK + lane)
+                    const ull key = lane < a.k ? __ldcg(partials + ((size_t)c * pstride + t) * kSmallMaxK + lane)
                                                : KEY_INF;
                     Li = warp_merge_topk(Li, key, a.k, lane);   // slices hold distinct rows
                 }
@@ -422,6 +428,7 @@ __device__ void small_query(const SearchArgs &a, const DevIndex &native, const S
         small_finish(a, s, key, qid, item_slot0, nraw, out_ids, out_d);
     }
     __syncthreads();
+    return true;
 }
 
 __device__ __forceinline__ void small_init_bars(const SmallSmem &s, int n_stages) {
@@ -464,24 +471,72 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
                                                             int raw_bytes, uint32_t *epochs, ServeRing ring) {
     extern __shared__ __align__(128) uint8_t smem[];
     if (blockIdx.x == 0) {
-        if (threadIdx.x == 0) {
-            long long last = -1;
-            for (;;) {
-                const int32_t st = *(volatile const int32_t *)ring.stop;
-                __threadfence_system();
-                const long long h = *(volatile const long long *)ring.head;
-                if (h != last) {
-                    *(volatile long long *)ring.dev_head = h;
-                    __threadfence();
-                    last = h;
+        // dispatcher: the only CTA that reads the host ring. New jobs are copied in bulk (all 128
+        // threads, 16-byte loads, a job's slot per 40 threads) into the device-memory ring, then
+        // published through the device head; workers never touch PCIe for their inputs.
+        long long *sh = reinterpret_cast<long long *>(smem);
+        long long copied = 0;
+        const int qv = ring.raw_stride / 16;             // 16-byte words of a query slot
+        const int per_job = qv + kServeLabels / 4 + 1;   // + labels (4 x 16 B) + the count
+        for (;;) {
+            if (threadIdx.x == 0) {
+                long long h;
+                int32_t st;
+                for (;;) {
+                    st = *(volatile const int32_t *)ring.stop;
+                    __threadfence_system();
+                    h = *(volatile const long long *)ring.head;
+                    if (h != copied || st) break;
+                    __nanosleep(64);
                 }
-                if (st) {
-                    *(volatile int32_t *)ring.dev_stop = 1;
-                    __threadfence();
-                    break;
-                }
-                __nanosleep(64);
+                sh[0] = h;
+                sh[1] = st;
             }
+            __syncthreads();
+            const long long h = sh[0];
+            const bool st = sh[1] != 0;
+            const long long n_new = h - copied;
+            // 4 PCIe reads in flight per thread before their stores (latency-bound otherwise)
+            constexpr int U = 4;
+            const long long total = n_new * per_job;
+            for (long long e0 = threadIdx.x; e0 < total; e0 += (long long)U * blockDim.x) {
+                uint4 v[U];
+                uint4 *dst[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const long long e = e0 + (long long)u * blockDim.x;
+                    dst[u] = nullptr;
+                    if (e >= total) continue;
+                    const long long j = copied + e / per_job;
+                    const int w = (int)(e % per_job);
+                    const int64_t slot = j % ring.cap;
+                    if (w < qv) {
+                        v[u] = __ldcv(reinterpret_cast<const uint4 *>(ring.queries + slot * ring.raw_stride) + w);
+                        dst[u] = reinterpret_cast<uint4 *>(ring.dq + slot * ring.raw_stride) + w;
+                    } else if (w < per_job - 1) {
+                        const int l = w - qv;
+                        v[u] = __ldcv(reinterpret_cast<const uint4 *>(ring.labels + slot * kServeLabels) + l);
+                        dst[u] = reinterpret_cast<uint4 *>(ring.dlab + slot * kServeLabels) + l;
+                    } else {
+                        v[u].x = (uint32_t)__ldcv(ring.nlab + slot);
+                        ring.dnlab[slot] = (int32_t)v[u].x;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (dst[u]) *dst[u] = v[u];
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                copied = h;
+                *(volatile long long *)ring.dev_head = h;
+                if (st) *(volatile int32_t *)ring.dev_stop = 1;
+                __threadfence();
+            }
+            if (threadIdx.x != 0) copied = h;
+            if (st) break;
+            __syncthreads();
         }
         return;
     }
@@ -489,9 +544,15 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
     small_init_bars(s, L.n_stages);
     uint32_t bar_phase = 0;
     long long *s_job = reinterpret_cast<long long *>(s.misc + 8);   // no static smem: the dynamic
+    auto now = [] { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
     for (;;) {                                                      // size may use all 227 KB
+        unsigned long long t0 = 0, t1 = 0, t2 = 0;
         if (threadIdx.x == 0) {
-            long long j = (long long)atomicAdd(ring.next, 1ull);
+            t0 = now();
+            // claim c = (job j, part c % nparts): a job is answered by nparts CTAs together
+            const long long c = (long long)atomicAdd(ring.next, 1ull);
+            long long j = c / ring.nparts;
+            s.misc[13] = (int32_t)(c % ring.nparts);
             // wait until job j is published (device mirror of the host head), or stop
             for (;;) {
                 const long long h = *(volatile long long *)ring.dev_head;
@@ -508,24 +569,62 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
         }
         __syncthreads();
         const long long j = *s_job;
+        const int part = s.misc[13];
         if (j < 0) break;
-        __threadfence_system();
+        if (threadIdx.x == 0) t1 = now();
         const int slot = (int)(j % ring.cap);
-        // the slot may have held an earlier job: read it past every cache (ld.cv) into shared memory
+        // the job's query and labels into shared memory
         uint8_t *rawbuf = s.stage;
         int32_t *labbuf = reinterpret_cast<int32_t *>(s.stage + ring.raw_stride);
         const uint4 *src = reinterpret_cast<const uint4 *>(ring.queries + (int64_t)slot * ring.raw_stride);
+#if VF_SERVE_SYSLD == 2
+        // system-scope relaxed loads: coherent with the host's stores, vectorised
+        for (int i = threadIdx.x; i < ring.raw_stride / 16; i += blockDim.x) {
+            uint4 v;
+            asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i));
+            reinterpret_cast<uint4 *>(rawbuf)[i] = v;
+        }
+        for (int i = threadIdx.x; i < kServeLabels; i += blockDim.x) {
+            int32_t v;
+            asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(ring.labels + (int64_t)slot * kServeLabels + i));
+            labbuf[i] = v;
+        }
+        int32_t nl_raw;
+        asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(nl_raw) : "l"(ring.nlab + slot));
+        const int nraw = min(nl_raw, kServeLabels);
+#else
+        // the dispatcher copied the slot into device memory: read it from L2 (ld.cg; an earlier job
+        // in this slot may still sit in this SM's L1)
+        const uint4 *dsrc = reinterpret_cast<const uint4 *>(ring.dq + (int64_t)slot * ring.raw_stride);
         for (int i = threadIdx.x; i < ring.raw_stride / 16; i += blockDim.x)
-            reinterpret_cast<uint4 *>(rawbuf)[i] = __ldcv(src + i);
+            reinterpret_cast<uint4 *>(rawbuf)[i] = __ldcg(dsrc + i);
         for (int i = threadIdx.x; i < kServeLabels; i += blockDim.x)
-            labbuf[i] = __ldcv(ring.labels + (int64_t)slot * kServeLabels + i);
-        const int nraw = min(__ldcv(ring.nlab + slot), kServeLabels);
+            labbuf[i] = __ldcg(ring.dlab + (int64_t)slot * kServeLabels + i);
+        const int nraw = min(__ldcg(ring.dnlab + slot), kServeLabels);
+        (void)src;
+#endif
         __syncthreads();
-        small_query<DTF, TF, CF, TS, CS>(a, native, L, smem, rawbuf, raw_bytes, labbuf, nraw, -1, -1,
-                                         ring.out_ids + (int64_t)slot * a.k, ring.out_dists + (int64_t)slot * a.k,
-                                         (int)(blockIdx.x - 1) * kSmallWarps, epochs, bar_phase);
-        __threadfence_system();
-        if (threadIdx.x == 0) *(volatile long long *)(ring.done + slot) = j + 1;
+        if (threadIdx.x == 0) t2 = now();
+        const bool wrote = small_query<DTF, TF, CF, TS, CS>(
+            a, native, L, smem, rawbuf, raw_bytes, labbuf, nraw, -1, -1, ring.out_ids + (int64_t)slot * a.k,
+            ring.out_dists + (int64_t)slot * a.k, (int)(blockIdx.x - 1) * kSmallWarps, epochs, bar_phase, part,
+            ring.nparts, ring.partials + (size_t)slot * ring.nparts * kServeLabels * kSmallMaxK,
+            ring.part_done + slot, kServeLabels);
+        // only warp 0 wrote results into the slot: its lanes make them visible to the host, then the
+        // done word publishes the job
+        if (wrote && threadIdx.x < 32) {
+            __threadfence_system();
+            __syncwarp();
+            if (threadIdx.x == 0) *(volatile long long *)(ring.done + slot) = j + 1;
+        }
+        if (threadIdx.x == 0 && ring.stats) {       // [0] wait for the job, [1] slot copy, [2] search, [3] parts
+            const unsigned long long t3 = now();
+            atomicAdd(ring.stats + 0, t1 - t0);
+            atomicAdd(ring.stats + 1, t2 - t1);
+            atomicAdd(ring.stats + 2, t3 - t2);
+            atomicAdd(ring.stats + 3, 1ull);
+        }
         __syncthreads();
     }
 }

@@ -39,6 +39,12 @@ struct ServeRing {
     unsigned long long *next;           // device job counter
     long long *dev_head;                // device mirror of head (written by the dispatcher CTA)
     int32_t *dev_stop;                  // device mirror of stop
+    int32_t nparts;                     // CTAs answering one job together (scan rows split, graph items spread)
+    unsigned long long *partials;       // [cap][nparts][kServeLabels][kSmallMaxK] per-CTA item lists
+    int32_t *part_done;                 // [cap] parts finished (reset by the merging CTA)
+    unsigned long long *stats;          // [4] ns waiting for jobs, copying slots, searching; parts done
+    uint8_t *dq;                        // device copies of the slots (written by the dispatcher CTA)
+    int32_t *dlab, *dnlab;
 };
 
 bool small_supported(const DevIndex &fast, const DevIndex &native, bool two_views, int k);
