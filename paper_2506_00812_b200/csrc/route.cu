@@ -76,6 +76,9 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
         lo = a.q_off[q];
         nraw = (int)(a.q_off[q + 1] - lo);
         int32_t *L = a.qlab + lo;   // the search's private copy of the labels, sorted in place
+        if (a.qlab_in)              // fused copy of the caller's device labels (no separate memcpy)
+            for (int t = lane; t < nraw; t += 32) L[t] = a.qlab_in[lo + t];
+        __syncwarp();
         if (lane == 0) {
             int nl = 0;
             route_labels(a, L, nraw, &nl, chosen, cpath, &nch, &pred);

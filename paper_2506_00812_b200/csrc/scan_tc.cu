@@ -30,6 +30,7 @@
 //           Multi-tile segments are finished as in k_scan.
 #include <cuda.h>
 #include <cstdio>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace vf {
@@ -970,7 +971,10 @@ static encode_tiled_fn get_encoder() {
 }
 
 // 2-D byte tensor [n_rows][row_bytes] with a box of `box_rows` rows x cw bytes, swizzled to cw.
-static bool encode_rows(CUtensorMap *m, const void *base, int row_bytes, int64_t n_rows, int cw, int box_rows) {
+// promote: L2 fill size for the map's loads -- 256 B for contiguous row tiles (X_LS), none for
+// row gathers (X via tile::gather4: a 192-B row promoted to 256-B blocks would fetch up to 512 B)
+static bool encode_rows(CUtensorMap *m, const void *base, int row_bytes, int64_t n_rows, int cw, int box_rows,
+                        bool promote) {
     encode_tiled_fn enc = get_encoder();
     if (!enc || n_rows <= 0) return false;
     cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)n_rows};
@@ -980,16 +984,18 @@ static bool encode_rows(CUtensorMap *m, const void *base, int row_bytes, int64_t
     const CUtensorMapSwizzle sw = cw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : cw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+               promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Encode the two maps the tensor-core scan reads (X_LS tiles, X rows); false if unsupported.
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x) {
     const int cw = ix.row_bytes % 128 == 0 ? 128 : ix.row_bytes % 64 == 0 ? 64 : 32;
-    bool ok = encode_rows(reinterpret_cast<CUtensorMap *>(tm_x), ix.X, ix.row_bytes, ix.n_points, cw, 1);
+    static const bool gpromote = [] { const char *e = getenv("VF_GATHER_PROMOTE"); return e && atoi(e) == 1; }();
+    bool ok = encode_rows(reinterpret_cast<CUtensorMap *>(tm_x), ix.X, ix.row_bytes, ix.n_points, cw, 1, gpromote);
     ok = ok && encode_rows(reinterpret_cast<CUtensorMap *>(tm_ls), ix.Xls, ix.row_bytes,
-                           ls_rows_pad > 0 ? ls_rows_pad : 1, cw, kTcRows);
+                           ls_rows_pad > 0 ? ls_rows_pad : 1, cw, kTcRows, true);
     return ok;
 }
 

@@ -614,6 +614,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.Qp = sc->Qp.as<uint8_t>();
     a.q_off = sc->qoff.as<int64_t>();
     a.qlab = sc->qlab.as<int32_t>();
+    a.qlab_in = nullptr;
     a.qinfo = sc->qinfo.as<QueryInfo>();
     a.items = sc->items.as<Item>();
     a.item_ctr = sc->item_ctr.as<int32_t>();
@@ -862,9 +863,13 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     else VF_CUDA(cudaMemcpyAsync(sc->qoff.p, qoff, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
     // f1 per-query path (small.cu): small batches are answered by one launch, one CTA per query
     const bool small_path = use_small_path(ix, p, n);
-    if (n_slots > 0 && !(small_path && lab_dev))    // the per-query path reads device labels in place
-        VF_CUDA(cudaMemcpyAsync(sc->qlab.p, qlab, (size_t)n_slots * 4,
-                                lab_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    // host labels are copied in; device labels are read in place by the per-query path and copied
+    // by k_prepare itself on the batched path (no separate device-to-device copy)
+    a.qlab_in = nullptr;
+    if (n_slots > 0 && !lab_dev)
+        VF_CUDA(cudaMemcpyAsync(sc->qlab.p, qlab, (size_t)n_slots * 4, cudaMemcpyHostToDevice, s));
+    else if (n_slots > 0 && !small_path)
+        a.qlab_in = qlab;
     a.Qraw = q_dev ? reinterpret_cast<const uint8_t *>(queries) : sc->raw.as<uint8_t>();
     a.out_ids = out_dev ? out_ids : sc->out_ids.as<int32_t>();
     a.out_dists = out_dev ? out_dists : sc->out_dists.as<float>();

@@ -150,6 +150,7 @@ struct SearchArgs {
     const uint8_t *Qp;        // [n_q][row_bytes] padded queries
     const int64_t *q_off;     // [n_q+1]
     int32_t *qlab;            // sorted/dedup labels per query (CSR with q_off)
+    const int32_t *qlab_in;   // caller's device labels copied into qlab by k_prepare (nullptr: already there)
     QueryInfo *qinfo;
     Item *items;              // [q_off[n_q]] slots
     int32_t *item_ctr;        // [slots][3] V, E, iterations (graph items)
