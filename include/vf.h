@@ -186,7 +186,10 @@ typedef struct {
     int64_t bytes_map_hs;               /* M_HS: hs_rows * 4 */
     int64_t bytes_ls_vectors;           /* X_LS: ls_rows * row_bytes */
     int64_t bytes_map_ls;               /* M_LS: ls_rows * 4 */
-    int64_t bytes_predicate;            /* point -> labels table: (n_points+1)*8 + entries*4 */
+    int64_t bytes_predicate;            /* point -> labels table: (n_points+1)*8 + entries*4, plus the
+                                           membership bitmaps of the largest labels (n_bm * ceil(N/32) * 4
+                                           + n_labels * 2; VF_BITMAP_DENSITY at build: |C_l| >= N/density,
+                                           default 256, 0 = none) */
     int64_t bytes_directory;            /* per-label metadata */
     int64_t bytes_norms;                /* ||x||^2 per point and per X_LS row (tensor-core scan) */
     int64_t bytes_u8_store;             /* integer-valued fp32 in [0,255]: lossless u8 X and X_LS copies */

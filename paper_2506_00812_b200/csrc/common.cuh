@@ -67,8 +67,24 @@ __device__ __forceinline__ int64_t bsearch_lab(const int32_t *__restrict__ lab, 
     return -1;
 }
 
+__device__ __forceinline__ bool has_label_bit(const DevIndex &ix, int slot, int32_t gid) {
+    return (__ldg(ix.lbits + (int64_t)slot * ix.lbit_words + (gid >> 5)) >> (gid & 31)) & 1u;
+}
+
 __device__ __forceinline__ bool verify_pred(const DevIndex &ix, int32_t gid, const int32_t *P, int np,
                                             int32_t excl) {
+    // fast path: every label to check has a membership bitmap -> one bit per label, no search
+    if (ix.lbit_slot) {
+        bool all = true, ok = true;
+        for (int t = 0; t < np && all; t++) {
+            const int32_t l = P[t];
+            if (l == excl) continue;
+            const int sl = (l >= 0 && l < ix.n_labels) ? ix.lbit_slot[l] : -1;
+            if (sl < 0) all = false;
+            else ok = ok && has_label_bit(ix, sl, gid);
+        }
+        if (all) return ok;
+    }
     int i0 = 0, i1 = np - 1;
     if (i0 <= i1 && P[i0] == excl) i0++;
     if (i0 <= i1 && P[i1] == excl) i1--;

@@ -268,6 +268,36 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
             __syncwarp();
             return;
         }
+        if (M <= 64 && ns <= 8) {
+            // Top of 33..64 keys as two register halves (lane i holds entries i and 32 + i): few
+            // survivors are inserted one at a time -- position by two ballots, shift up across the
+            // halves (A's last entry moves to B's first); entries >= M are never written back
+            ull A = lane < ntop ? cur[lane] : KEY_INF;
+            ull B = 32 + lane < ntop ? cur[32 + lane] : KEY_INF;
+            unsigned rem = sm;
+            while (rem) {
+                const ull kk = __shfl_sync(FULL, ck, __ffs(rem) - 1);
+                rem &= rem - 1;
+                const int pos = __popc(__ballot_sync(FULL, A < kk)) + __popc(__ballot_sync(FULL, B < kk));
+                const ull carry = __shfl_sync(FULL, A, 31);
+                const ull upA = __shfl_up_sync(FULL, A, 1);
+                const ull upB = __shfl_up_sync(FULL, B, 1);
+                if (pos < 32) {
+                    B = lane == 0 ? carry : upB;
+                    if (lane > pos) A = upA;
+                    else if (lane == pos) A = kk;
+                } else {
+                    const int p2 = pos - 32;
+                    if (lane > p2) B = upB;
+                    else if (lane == p2) B = kk;
+                }
+            }
+            if (lane < M) cur[lane] = A;
+            if (32 + lane < M) cur[32 + lane] = B;
+            ntop = min(M, ntop + ns);
+            __syncwarp();
+            return;
+        }
         if (ns == 1) {
             ck = __shfl_sync(FULL, ck, __ffs(sm) - 1);
             if (lane == 0) cbuf[0] = ck;

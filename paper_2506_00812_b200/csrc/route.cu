@@ -233,6 +233,8 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
     __shared__ int s_tile, s_ok, s_n, s_np, s_bad, s_flush_off, s_nu;
     __shared__ int32_t s_u[kFiltUnion];           // union of the segment's other query labels, sorted
     __shared__ unsigned long long s_qm[kScanQG];  // per query: its labels' bits in s_u
+    __shared__ int16_t s_slot[kFiltUnion];        // membership bitmap of each s_u label
+    __shared__ int s_allbits;                     // every s_u label has a bitmap: no label-list reads
     const int ntiles = a.ctr->n_tiles;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&a.ctr->filter_next, 1);
@@ -274,9 +276,18 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
                     nu++;
                 }
             s_nu = nu;
+            int all = nu <= 64 && a.ix.lbit_slot != nullptr;
+            for (int j = 0; j < nu && all; j++) {
+                const int32_t l = s_u[j];
+                const int sl = (l >= 0 && l < a.ix.n_labels) ? a.ix.lbit_slot[l] : -1;
+                s_slot[j] = (int16_t)sl;
+                all = sl >= 0;
+            }
+            s_allbits = all;
         }
         __syncthreads();
         const int nu = s_nu;
+        const bool allbits = s_allbits != 0;
         if (nu <= 64 && threadIdx.x < tl.nq) {
             unsigned long long qm = 0;
             for (int i = 0; i < q_nl[threadIdx.x]; i++) {
@@ -297,6 +308,19 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
                 const int r = r0 + u * kFiltThreads + threadIdx.x;
                 gid[u] = r < tl.row_end ? __ldg(a.ix.M_hs + tl.base + r) : -1;
             }
+            if (allbits) {
+                // membership bitmaps: one bit read per (row, other label), independent loads
+#pragma unroll
+                for (int u = 0; u < kFiltRows; u++) {
+                    if (gid[u] < 0) continue;
+                    unsigned long long bits = 0;
+                    for (int j = 0; j < nu; j++)
+                        if (has_label_bit(a.ix, s_slot[j], gid[u])) bits |= 1ull << j;
+                    bool pass = false;
+                    for (int g = 0; g < tl.nq && !pass; g++) pass = (bits & s_qm[g]) == s_qm[g];
+                    if (pass) buf[atomicAdd(&s_n, 1)] = gid[u];
+                }
+            } else {
 #pragma unroll
             for (int u = 0; u < kFiltRows; u++) {
                 lo[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u]) : 0;
@@ -331,6 +355,7 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
                         pass = verify_pred(a.ix, gid[u], a.qlab + q_off[g], q_nl[g], tl.label);
                 }
                 if (pass) buf[atomicAdd(&s_n, 1)] = gid[u];
+            }
             }
             __syncthreads();
             const bool last = r0 + kFiltThreads * kFiltRows >= tl.row_end;

@@ -268,6 +268,36 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     VF_B(cudaMemcpy(ix->pt_off.p, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice));
     VF_B(ix->pt_lab.ensure(plab.size() * 4));
     VF_B(cudaMemcpy(ix->pt_lab.p, plab.data(), plab.size() * 4, cudaMemcpyHostToDevice));
+    // -- membership bitmaps of the largest labels (predicate fast path): labels with
+    // |C_l| >= N / VF_BITMAP_DENSITY (default 256: a bitmap is at most 8x its posting list), at most
+    // kMaxBitmaps of them, largest first. 0 disables them.
+    int64_t n_bitmaps = 0, lbit_words = (N + 31) / 32;
+    {
+        const char *e = getenv("VF_BITMAP_DENSITY");
+        const int64_t dens = e ? atoll(e) : 256;
+        std::vector<int32_t> cand;
+        if (dens > 0 && N > 0)
+            for (int l = 0; l < L; l++)
+                if ((po[l + 1] - po[l]) * dens >= N && po[l + 1] > po[l]) cand.push_back(l);
+        std::stable_sort(cand.begin(), cand.end(),
+                         [&](int32_t x, int32_t y) { return po[x + 1] - po[x] > po[y + 1] - po[y]; });
+        if ((int64_t)cand.size() > kMaxBitmaps) cand.resize(kMaxBitmaps);
+        n_bitmaps = (int64_t)cand.size();
+        if (n_bitmaps > 0) {
+            std::vector<int16_t> slot((size_t)L, (int16_t)-1);
+            std::vector<uint32_t> bits((size_t)(n_bitmaps * lbit_words), 0u);
+            for (int64_t b = 0; b < n_bitmaps; b++) {
+                const int32_t l = cand[(size_t)b];
+                slot[(size_t)l] = (int16_t)b;
+                uint32_t *w = bits.data() + b * lbit_words;
+                for (int64_t e2 = po[l]; e2 < po[l + 1]; e2++) w[pi[e2] >> 5] |= 1u << (pi[e2] & 31);
+            }
+            VF_B(ix->lbits.ensure(bits.size() * 4));
+            VF_B(cudaMemcpy(ix->lbits.p, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+            VF_B(ix->lbit_slot.ensure(slot.size() * 2));
+            VF_B(cudaMemcpy(ix->lbit_slot.p, slot.data(), slot.size() * 2, cudaMemcpyHostToDevice));
+        }
+    }
     if (!owner.empty()) {
         VF_B(ix->owner_dev.ensure(owner.size() * 4));
         VF_B(cudaMemcpy(ix->owner_dev.p, owner.data(), owner.size() * 4, cudaMemcpyHostToDevice));
@@ -292,6 +322,9 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     D.M_ls = ix->M_ls.as<int32_t>();
     D.pt_off = ix->pt_off.as<int64_t>();
     D.pt_lab = ix->pt_lab.as<int32_t>();
+    D.lbits = n_bitmaps ? ix->lbits.as<uint32_t>() : nullptr;
+    D.lbit_slot = n_bitmaps ? ix->lbit_slot.as<int16_t>() : nullptr;
+    D.lbit_words = lbit_words;
     D.owner = owner.empty() ? nullptr : ix->owner_dev.as<int32_t>();
     D.rank = rank;
     D.world = world;
@@ -330,7 +363,7 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     I.bytes_map_hs = hs_rows * 4;
     I.bytes_ls_vectors = ls_rows_pad * row_bytes;
     I.bytes_map_ls = (ls_rows_pad + 4) * 4;
-    I.bytes_predicate = (N + 1) * 8 + n_entries * 4;
+    I.bytes_predicate = (N + 1) * 8 + n_entries * 4 + (n_bitmaps ? n_bitmaps * lbit_words * 4 + (int64_t)L * 2 : 0);
     I.bytes_directory = (int64_t)L * sizeof(LabelDir) + (owner.empty() ? 0 : (int64_t)L * 4);
     I.bytes_norms = tc_rows ? (N + (int64_t)m_ls.size()) * 4 : 0;
     I.bytes_u8_store = enc8 ? (N + ls_rows_pad) * row_bytes8 : 0;

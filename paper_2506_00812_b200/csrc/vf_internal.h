@@ -8,6 +8,7 @@ namespace vf {
 
 constexpr int kMaxQueryLabels = 64;   // labels per query accepted by vf_search
 constexpr int kMaxK = 256;
+constexpr int kMaxBitmaps = 256;      // membership bitmaps of the largest labels (predicate fast path)
 constexpr int kMaxItopk = 1024;
 constexpr int kScanQG = 64;           // queries per scan segment (query group)
 constexpr int kWarpsPerGraphCta = 4;
@@ -44,6 +45,10 @@ struct DevIndex {
     const int32_t *M_ls;   // [ls_rows] (M_LS)
     const int64_t *pt_off; // [n_points+1] predicate table offsets
     const int32_t *pt_lab; // sorted labels per point
+    const uint32_t *lbits; // [n_bitmaps][lbit_words] membership bitmaps of the largest labels (predicate
+                           // fast path: P ⊆ L_x tested bit by bit; identical answers to pt_lab)
+    const int16_t *lbit_slot;  // [n_labels] bitmap of a label, -1 = none
+    int64_t lbit_words;
     const int32_t *owner;  // [n_labels] owning rank of each label (label sharding, §8(e)); NULL = all local
     const uint32_t *xn;    // [n_points] ||x||^2 (u8: exact int32) for the tensor-core scan's expansion
     const uint32_t *xn_ls; // [ls_rows_pad + 4] ||x||^2 of the X_LS rows

@@ -321,3 +321,23 @@ def test_scan_threshold_f2_bit_exact(vf, tiny, thr):
     ids, d = g.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", scan_threshold=thr)
     oi, od = o.search(w.Q, qoff, qlab, k=10, itopk=32, op="and", scan_threshold=thr)
     assert (ids == oi).all() and (d == od.astype(np.float32)).all()
+
+
+@pytest.mark.parametrize("density", ["0", "4", "256"])
+def test_label_bitmaps_do_not_change_results(vf, tiny, density, monkeypatch):
+    """Membership bitmaps of the largest labels (predicate fast path, read at build time): none
+    (0), only labels with >= N/4 points (4: a mix of bitmap and label-list checks inside one query),
+    all labels with >= N/256 points (256, the default). AND / OR results and per-item counters
+    stay bit-identical to the oracle, which has no bitmaps."""
+    from workload import gen
+    monkeypatch.setenv("VF_BITMAP_DENSITY", density)
+    w, go, gi = tiny
+    g, o = _pair(vf, w.X, w, go, gi)
+    for mode_q, op, mode in [("and2", "and", "greedy"), ("and2", "and", "parallel"), ("or2", "or", "greedy")]:
+        qoff, qlab = gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=len(w.Q), mode=mode_q)
+        for thr in (0, 400):
+            ids, d = g.search(w.Q, qoff, qlab, k=10, itopk=32, op=op, recall_mode=mode, and_scan_threshold=thr)
+            oi, od, octr = o.search(w.Q, qoff, qlab, k=10, itopk=32, op=op, recall_mode=mode,
+                                    and_scan_threshold=thr, counters=True)
+            assert (ids == oi).all() and (d == od.astype(np.float32)).all(), (op, mode, thr)
+            _items_match(g, octr)
