@@ -71,17 +71,21 @@ __device__ __forceinline__ bool has_label_bit(const DevIndex &ix, int slot, int3
     return (__ldg(ix.lbits + (int64_t)slot * ix.lbit_words + (gid >> 5)) >> (gid & 31)) & 1u;
 }
 
-__device__ __forceinline__ bool verify_pred(const DevIndex &ix, int32_t gid, const int32_t *P, int np,
-                                            int32_t excl) {
+// Out of line (its registers stay out of the callers' hot loops; only AND items call it), with the
+// index arrays passed as scalars so no parameter struct is spilled to the stack.
+static __device__ __noinline__ bool verify_pred_x(const int64_t *__restrict__ pt_off, const int32_t *__restrict__ pt_lab,
+                                           const uint32_t *__restrict__ lbits, const int16_t *__restrict__ lslot,
+                                           int64_t lwords, int32_t n_labels, int32_t gid, const int32_t *P, int np,
+                                           int32_t excl) {
     // fast path: every label to check has a membership bitmap -> one bit per label, no search
-    if (ix.lbit_slot) {
+    if (lslot) {
         bool all = true, ok = true;
         for (int t = 0; t < np && all; t++) {
             const int32_t l = P[t];
             if (l == excl) continue;
-            const int sl = (l >= 0 && l < ix.n_labels) ? ix.lbit_slot[l] : -1;
+            const int sl = (l >= 0 && l < n_labels) ? lslot[l] : -1;
             if (sl < 0) all = false;
-            else ok = ok && has_label_bit(ix, sl, gid);
+            else ok = ok && ((__ldg(lbits + (int64_t)sl * lwords + (gid >> 5)) >> (gid & 31)) & 1u);
         }
         if (all) return ok;
     }
@@ -89,17 +93,22 @@ __device__ __forceinline__ bool verify_pred(const DevIndex &ix, int32_t gid, con
     if (i0 <= i1 && P[i0] == excl) i0++;
     if (i0 <= i1 && P[i1] == excl) i1--;
     if (i0 > i1) return true;
-    const int64_t lo = __ldg(ix.pt_off + gid), hi = __ldg(ix.pt_off + gid + 1);
-    const int64_t a = bsearch_lab(ix.pt_lab, lo, hi, P[i0]);
+    const int64_t lo = __ldg(pt_off + gid), hi = __ldg(pt_off + gid + 1);
+    const int64_t a = bsearch_lab(pt_lab, lo, hi, P[i0]);
     if (a < 0) return false;
     if (i0 == i1) return true;
-    const int64_t b = bsearch_lab(ix.pt_lab, a + 1, hi, P[i1]);
+    const int64_t b = bsearch_lab(pt_lab, a + 1, hi, P[i1]);
     if (b < 0) return false;
     for (int t = i0 + 1; t < i1; t++) {
         if (P[t] == excl) continue;
-        if (bsearch_lab(ix.pt_lab, a + 1, b, P[t]) < 0) return false;
+        if (bsearch_lab(pt_lab, a + 1, b, P[t]) < 0) return false;
     }
     return true;
+}
+
+__device__ __forceinline__ bool verify_pred(const DevIndex &ix, int32_t gid, const int32_t *P, int np,
+                                            int32_t excl) {
+    return verify_pred_x(ix.pt_off, ix.pt_lab, ix.lbits, ix.lbit_slot, ix.lbit_words, ix.n_labels, gid, P, np, excl);
 }
 
 // ---------------------------------------------------------------- routing of one query (a1)

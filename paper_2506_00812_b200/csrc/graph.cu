@@ -5,10 +5,14 @@
 // search of one item is beam_item() (graph_item.cuh).
 #include "graph_item.cuh"
 
+#ifndef VF_GRAPH_MINB
+#define VF_GRAPH_MINB 8      // CTAs per SM the register budget is sized for (8: 64 registers)
+#endif
+
 namespace vf {
 
 template <int DT, int TEAM, int MAXCPL>
-__global__ void __launch_bounds__(32 * kWarpsPerGraphCta, 8) k_graph(SearchArgs a, GraphLayout GL,
+__global__ void __launch_bounds__(32 * kWarpsPerGraphCta, VF_GRAPH_MINB) k_graph(SearchArgs a, GraphLayout GL,
                                                                   uint32_t *gtab_epoch) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (gate_skip(a)) return;     // u8 row store: the other view's kernel takes this batch

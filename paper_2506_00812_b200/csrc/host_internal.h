@@ -64,8 +64,8 @@ struct Scratch {
     // per-query path (f1): per-CTA item lists of a query split over several CTAs, completion counters
     DevBuf small_part, small_cnt;
     // scan / graph overlap: the graph kernels run on a side stream forked after routing
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side = nullptr, side_hi = nullptr;   // graph kernels; scan kernels (high priority)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
     size_t gtab_slots = 0, gtab_warps = 0;
     // profiled searches record their phase events into a ring: ev points at the current set, so
     // the mean over every search since profiling was enabled (<= kProfRing of them) is readable
@@ -87,8 +87,10 @@ struct Scratch {
             for (auto &set : evs)
                 for (auto &e : set) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
+        if (side_hi) cudaStreamDestroy(side_hi);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (ev_join2) cudaEventDestroy(ev_join2);
     }
 };
 

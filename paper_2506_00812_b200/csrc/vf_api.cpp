@@ -689,16 +689,25 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     static const int overlap_env = [] { const char *e = getenv("VF_OVERLAP"); return e ? atoi(e) : 1; }();
     static const int tc_ctas_env = [] { const char *e = getenv("VF_TC_CTAS"); return e ? atoi(e) : 2; }();
     const bool overlap = overlap_env != 0 && pl.tc;
-    cudaStream_t gs = s;
+    // Both become runnable at the fork; the scan goes on a high-priority stream so the block
+    // scheduler always places the scan CTAs first (otherwise whichever kernel wins the race takes
+    // the SMs and step times become bimodal).
+    cudaStream_t gs = s, ss = s;
     if (overlap) {
         if (!sc->side) {
+            int lo = 0, hi = 0;
+            VF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             VF_CUDA(cudaStreamCreateWithFlags(&sc->side, cudaStreamNonBlocking));
+            VF_CUDA(cudaStreamCreateWithPriority(&sc->side_hi, cudaStreamNonBlocking, hi));
             VF_CUDA(cudaEventCreateWithFlags(&sc->ev_fork, cudaEventDisableTiming));
             VF_CUDA(cudaEventCreateWithFlags(&sc->ev_join, cudaEventDisableTiming));
+            VF_CUDA(cudaEventCreateWithFlags(&sc->ev_join2, cudaEventDisableTiming));
         }
         VF_CUDA(cudaEventRecord(sc->ev_fork, s));
+        VF_CUDA(cudaStreamWaitEvent(sc->side_hi, sc->ev_fork, 0));
         VF_CUDA(cudaStreamWaitEvent(sc->side, sc->ev_fork, 0));
         gs = sc->side;
+        ss = sc->side_hi;
     }
     // Fast kernels gated on "no query outside the exact range" (gate 1), the fp32 FFMA kernels on
     // the opposite (gate 2); without a range check only the fast set runs (gate 0).
@@ -713,14 +722,14 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     static const int graph_first_env = [] { const char *e = getenv("VF_GRAPH_FIRST"); return e ? atoi(e) : 0; }();
     static const int graph_per_sm_env = [] { const char *e = getenv("VF_GRAPH_PER_SM"); return e ? atoi(e) : 0; }();
     auto launch_scans = [&]() -> int {
-        int sl = pl.tc ? launch_scan_tc(fast, s, tb, ix->tm_ls, ix->tm_x, overlap ? tc_ctas_env : 0)
-                       : launch_scan(fast, s, tb);
+        int sl = pl.tc ? launch_scan_tc(fast, ss, tb, ix->tm_ls, ix->tm_x, overlap ? tc_ctas_env : 0)
+                       : launch_scan(fast, ss, tb);
         if (sl >= 0 && pl.wsplit) {
-            const int s3 = launch_scan_warp(fast, s, tb);
+            const int s3 = launch_scan_warp(fast, ss, tb);
             sl = s3 < 0 ? s3 : sl + s3;
         }
         if (sl >= 0 && pl.checked) {
-            const int s2 = launch_scan(slow, s, tb);
+            const int s2 = launch_scan(slow, ss, tb);
             sl = s2 < 0 ? s2 : sl + s2;
         }
         return sl;
@@ -748,7 +757,7 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     const int sl = launch_scans();
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
-    if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], s));
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[3], ss));
     if (!(overlap && graph_first_env)) {
         gl = launch_graphs();
         if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
@@ -757,7 +766,9 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     if (overlap) {
         if (prof) VF_CUDA(cudaEventRecord(sc->ev[7], gs));     // graph phase end (side stream)
         VF_CUDA(cudaEventRecord(sc->ev_join, gs));
+        VF_CUDA(cudaEventRecord(sc->ev_join2, ss));
         VF_CUDA(cudaStreamWaitEvent(s, sc->ev_join, 0));
+        VF_CUDA(cudaStreamWaitEvent(s, sc->ev_join2, 0));
     }
     sc->overlapped = overlap;
     if (prof) sc->evov[sc->prof_n % Scratch::kProfRing] = overlap;
