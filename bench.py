@@ -526,6 +526,11 @@ def main():
             traffic = int(tj["bytes"])
     except (OSError, ValueError, KeyError):
         traffic = None
+    # the dominant kernel's own device-clock span in the last timed step (first CTA start -> last
+    # CTA end): in an overlapped step the phase events above also count time the launched kernel
+    # waited for SMs held by the other phase
+    act_ms = s0["ms_graph_active"] if dom == "graph" else s0["ms_scan_active"]
+    act_gbs = bytes_dom / (act_ms / 1000.0) / 1e9 if act_ms > 0 else None
     line = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": tot / K, "higher_is_better": True, "scaling": "weak",
@@ -554,7 +559,12 @@ def main():
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)" if traffic else None,
                      "algorithmic_bytes_per_launch": int(bytes_dom),
-                     "kernel_ms_per_launch": ms_dom},
+                     "kernel_ms_per_launch": ms_dom,
+                     "kernel_active_ms": act_ms, "achieved_active": act_gbs,
+                     "frac_active": act_gbs / hbm_peak if act_gbs else None,
+                     "note": ("kernel_ms_per_launch: CUDA events of the kernel's phase on its stream, mean of the K "
+                              "timed steps (scan and graph overlap, so it includes waiting for SMs); "
+                              "kernel_active_ms: %globaltimer span of the kernel's CTAs in the last step")},
         "phases_ms": {**{p: s0[f"mean_ms_{p}"] for p in ("route", "scan", "graph", "merge", "copy", "total")},
                       "steps_averaged": s0["n_profiled"]},
         "work": {kk: s0[kk] for kk in ("n_items", "n_scan_items", "n_graph_items", "n_segments",

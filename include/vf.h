@@ -220,6 +220,10 @@ typedef struct {
      * enabled (the most recent 64 of them); n_profiled = how many were averaged */
     int64_t n_profiled;
     double mean_ms_route, mean_ms_scan, mean_ms_graph, mean_ms_merge, mean_ms_copy, mean_ms_total;
+    /* device-clock span (first CTA start -> last CTA end, %globaltimer) of the tensor-core scan kernel
+     * and of the graph kernel in the most recent search; 0 if the kernel did not run. Unlike the
+     * phase events these exclude time a launched kernel waited for SMs (overlapped phases). */
+    double ms_scan_active, ms_graph_active;
 } vf_search_stats;
 
 vf_status vf_set_profiling(vf_index *index, int32_t enable);

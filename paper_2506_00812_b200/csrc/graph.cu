@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, VF_GRAPH_MINB) k_graph
                                                                   uint32_t *gtab_epoch) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (gate_skip(a)) return;     // u8 row store: the other view's kernel takes this batch
+    if (threadIdx.x == 0) atomicMax(&a.ctr->graph_t0_inv, ~gtimer());
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint8_t *wb = smem + (size_t)wid * GL.warp_bytes;
     const DevIndex &ix = a.ix;
@@ -77,7 +78,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, VF_GRAPH_MINB) k_graph
         }
         __syncwarp();
     }
-    if (lane == 0) gtab_epoch[warp_slot] = epoch;
+    if (lane == 0) {
+        gtab_epoch[warp_slot] = epoch;
+        atomicMax(&a.ctr->graph_t1, gtimer());
+    }
 }
 
 // ------------------------------------------------------------------ dispatch

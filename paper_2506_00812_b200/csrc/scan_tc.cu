@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t stage_bytes = (size_t)kTcRows * kpad;
     if (gate_skip(a)) return;     // a batch outside the exact range runs k_scan instead
+    if (threadIdx.x == 0) atomicMax(&a.ctr->scan_t0_inv, ~gtimer());
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
@@ -875,6 +876,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(SL.tmem_cols));
     }
+    if (threadIdx.x == 0) atomicMax(&a.ctr->scan_t1, gtimer());
 }
 
 // ---------------------------------------------------------------- row norms (build time)

@@ -989,6 +989,12 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->graph_V_max = (int64_t)c.graph_V_max;
     st->kernel_launches = sc->last_launches;
     st->row_bytes = ix->enc8 && !c.exact_fallback ? ix->dev8.row_bytes : ix->dev.row_bytes;   // rows the kernels read
+    auto span = [](unsigned long long t0_inv, unsigned long long t1) {
+        const unsigned long long t0 = ~t0_inv;
+        return (t0_inv && t1 > t0) ? (double)(t1 - t0) / 1e6 : 0.0;
+    };
+    st->ms_scan_active = span(c.scan_t0_inv, c.scan_t1);
+    st->ms_graph_active = span(c.graph_t0_inv, c.graph_t1);
     // with scan / graph overlap the graph phase runs from the fork (ev[2]) to its own end (ev[7])
     auto phases = [](cudaEvent_t *e, bool ov, double *out) {
         float t;

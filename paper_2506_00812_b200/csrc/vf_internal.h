@@ -144,6 +144,10 @@ struct Counters {
     int32_t pool_used;       // survivor pool bump allocator
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
+    // device-clock activity spans of the dominant kernels (globaltimer ns; first CTA start stored
+    // inverted so that zeroed counters work with atomicMax): the kernels' own durations, which the
+    // phase events of an overlapped search cannot give
+    unsigned long long scan_t0_inv, scan_t1, graph_t0_inv, graph_t1;
     int32_t remote[kMaxWorld];      // items of this batch owned by each rank (sharded index)
     int32_t remote_pos[kMaxWorld];  // packing cursors
 };

@@ -341,3 +341,17 @@ def test_label_bitmaps_do_not_change_results(vf, tiny, density, monkeypatch):
                                     and_scan_threshold=thr, counters=True)
             assert (ids == oi).all() and (d == od.astype(np.float32)).all(), (op, mode, thr)
             _items_match(g, octr)
+
+
+def test_kernel_activity_spans(vf, tiny):
+    """vf_get_last_stats reports the scan / graph kernels' device-clock spans; they are positive
+    when the kernel ran and fit inside the whole search."""
+    w, go, gi = tiny
+    g = vf.Index(w.X, w.post_off, w.post_ids, w.cfg.threshold_T, w.cfg.degree_R, go, gi)
+    g.set_profiling(True)
+    g.search(w.Q, w.q_off, w.q_lab, k=10, itopk=32)
+    st = g.last_stats()
+    assert st["n_graph_items"] > 0 and st["ms_graph_active"] > 0
+    assert st["ms_graph_active"] <= st["ms_total"] + 1e-3
+    if st["n_scan_items"] > 0 and g.info()["bytes_norms"] > 0:     # tensor-core scan ran
+        assert 0 < st["ms_scan_active"] <= st["ms_total"] + 1e-3
