@@ -513,7 +513,10 @@ def main():
     g_ms = s0["mean_ms_graph"]
     s_bytes = s0["scan_rows"] * (rb + 4)
     s_ms = s0["mean_ms_scan"]
-    dom = "graph" if g_ms >= s_ms else "scan"
+    # dominant kernel: the longer device-clock span (the phase events overlap when scan and graph
+    # run concurrently); phase times if the spans are unavailable
+    ga, sa = s0.get("ms_graph_active", 0.0), s0.get("ms_scan_active", 0.0)
+    dom = ("graph" if ga >= sa else "scan") if (ga > 0 or sa > 0) else ("graph" if g_ms >= s_ms else "scan")
     bytes_dom, ms_dom = (g_bytes, g_ms) if dom == "graph" else (s_bytes, s_ms)
     achieved = bytes_dom / (ms_dom / 1000.0) / 1e9 if ms_dom > 0 else 0.0
     # measured DRAM traffic of that kernel at this operating point, from a committed ncu capture
@@ -521,9 +524,9 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(args.config)
-        if tj and tj["kernel"] == f"k_{dom}" and (tj["itopk"], tj["search_width"], tj["and_scan_threshold"],
-                                                  tj["scan_threshold"]) == (itopk, opnt[3], opnt[5], opnt[6]):
-            traffic = int(tj["bytes"])
+        if tj and f"k_{dom}" in tj and (tj["itopk"], tj["search_width"], tj["and_scan_threshold"],
+                                        tj["scan_threshold"]) == (itopk, opnt[3], opnt[5], opnt[6]):
+            traffic = int(tj[f"k_{dom}"]["bytes"])
     except (OSError, ValueError, KeyError):
         traffic = None
     # the dominant kernel's own device-clock span in the last timed step (first CTA start -> last
