@@ -30,7 +30,7 @@ struct vf_server {
     vf::DevBuf next, gtab, ctr, partials, part_done, dring;
     int nparts = 1;
     cudaStream_t stream = nullptr;
-    int64_t submitted = 0;
+    std::atomic<int64_t> submitted{0};   // written under mu, read by vf_serve_wait / info without it
     std::mutex mu;
     bool running = false;
 };
@@ -193,7 +193,7 @@ extern "C" vf_status vf_serve_submit(vf_server *sv, const void *query, const int
     if (n_labels < 0 || n_labels > kServeLabels) return fail(VF_ERR_INVALID_ARG, "n_labels must be in [0, 16]");
     if (!sv->running) return fail(VF_ERR_INVALID_ARG, "server stopped");
     std::lock_guard<std::mutex> g(sv->mu);
-    const int64_t j = sv->submitted;
+    const int64_t j = sv->submitted.load(std::memory_order_relaxed);
     const int64_t slot = j % sv->cap;
     // the slot's previous job (j - cap) must have been answered before it is overwritten
     if (j >= sv->cap) {
@@ -205,14 +205,15 @@ extern "C" vf_status vf_serve_submit(vf_server *sv, const void *query, const int
     sv->hnlab[slot] = n_labels;
     std::atomic_thread_fence(std::memory_order_release);
     *(volatile long long *)sv->hhead = j + 1;                    // publish job j
-    sv->submitted = j + 1;
+    sv->submitted.store(j + 1, std::memory_order_release);
     *ticket = j;
     return VF_OK;
 }
 
 extern "C" vf_status vf_serve_wait(vf_server *sv, int64_t ticket, int32_t *out_ids, float *out_dists) {
     if (!sv || !out_ids || !out_dists) return fail(VF_ERR_INVALID_ARG, "NULL argument");
-    if (ticket < 0 || ticket >= sv->submitted) return fail(VF_ERR_INVALID_ARG, "unknown ticket");
+    if (ticket < 0 || ticket >= sv->submitted.load(std::memory_order_acquire))
+        return fail(VF_ERR_INVALID_ARG, "unknown ticket");
     const int64_t slot = ticket % sv->cap;
     volatile long long *dn = sv->hdone + slot;
     long long v;
@@ -298,6 +299,6 @@ extern "C" vf_status vf_serve_stats(vf_server *sv, double *wait_us, double *copy
 extern "C" vf_status vf_serve_info(const vf_server *sv, int32_t *n_workers, int64_t *submitted) {
     if (!sv) return fail(VF_ERR_INVALID_ARG, "NULL server");
     if (n_workers) *n_workers = sv->n_ctas;
-    if (submitted) *submitted = sv->submitted;
+    if (submitted) *submitted = sv->submitted.load();
     return VF_OK;
 }

@@ -94,3 +94,16 @@ def test_null_safety(vf):
     vf.lib().vf_free(None)
     st = vf.lib().vf_search(None, None, 0, None, None, None, None, None, None)
     assert st == vf.VF_ERR_INVALID_ARG
+
+
+def test_serve_null_safety(vf):
+    """The serving calls validate their arguments before touching a device (no GPU needed)."""
+    import ctypes as C
+    L = vf.lib()
+    t = C.c_int64()
+    assert L.vf_serve_start(None, None, 16, 0, None) == vf.VF_ERR_INVALID_ARG
+    assert L.vf_serve_submit(None, None, None, 0, C.byref(t)) == vf.VF_ERR_INVALID_ARG
+    assert L.vf_serve_wait(None, 0, None, None) == vf.VF_ERR_INVALID_ARG
+    assert L.vf_serve_run(None, 0, None, None, None, 1, None, None) == vf.VF_ERR_INVALID_ARG
+    assert L.vf_serve_info(None, None, None) == vf.VF_ERR_INVALID_ARG
+    assert L.vf_serve_stop(None) == vf.VF_OK
