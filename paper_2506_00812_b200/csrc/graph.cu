@@ -26,13 +26,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerGraphCta, VF_GRAPH_MINB) k_graph
     const uint64_t gmask = (uint64_t)a.gtab_slots - 1;
     uint32_t epoch = gtab_epoch[warp_slot];
     const int n_graph = a.ctr->n_graph;
+    int cum[kGraphClasses + 1];                 // claim order: size classes, largest labels first
+    cum[0] = 0;
+    for (int c = 0; c < kGraphClasses; c++) cum[c + 1] = cum[c] + a.ctr->n_graph_cls[c];
 
     for (;;) {
         int gi = 0;
         if (lane == 0) gi = atomicAdd(&a.ctr->graph_next, 1);
         gi = __shfl_sync(FULL, gi, 0);
         if (gi >= n_graph) break;
-        const int32_t slot = a.graph_list[gi];
+        int c = 0;
+        while (c + 1 < kGraphClasses && gi >= cum[c + 1]) c++;
+        const int32_t slot = a.graph_list[c * a.graph_stride + (gi - cum[c])];
         const Item it = a.items[slot];
         const LabelDir d = ix.dir[it.label];
         const QueryInfo qi = a.qinfo[it.qid];

@@ -30,15 +30,16 @@ __device__ __forceinline__ void check_query_row(const SearchArgs &a, const float
 
 __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const uint8_t *__restrict__ raw,
                                                              int raw_bytes) {
-    __shared__ int s_ngraph[kPrepWarps];
-    __shared__ int s_gbase;
+    __shared__ int s_ngraph[kGraphClasses][kPrepWarps];
+    __shared__ int s_gbase[kGraphClasses];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * kPrepWarps + wid;
     const bool live = q < a.n_q;
     const DevIndex &ix = a.ix;
     int32_t chosen[kMaxQueryLabels];
     uint32_t cpath[kMaxQueryLabels];
-    int nch = 0, ngraph = 0, nraw = 0;
+    int nch = 0, nraw = 0;
+    int ngc[kGraphClasses] = {0, 0, 0, 0};
     int64_t lo = 0;
     uint32_t pred = 0;
 
@@ -82,23 +83,27 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
         if (lane == 0) {
             int nl = 0;
             route_labels(a, L, nraw, &nl, chosen, cpath, &nch, &pred);
-            for (int t = 0; t < nch; t++) ngraph += cpath[t] == PATH_GRAPH;
+            for (int t = 0; t < nch; t++)
+                if (cpath[t] == PATH_GRAPH) ngc[graph_class(ix.dir[chosen[t]].size)]++;
             QueryInfo qi;
             qi.nl = nl; qi.n_items = nch; qi.qh = qh; qi.pad = 0;
             a.qinfo[q] = qi;
         }
     }
-    if (lane == 0) s_ngraph[wid] = ngraph;
+    if (lane == 0)
+        for (int c = 0; c < kGraphClasses; c++) s_ngraph[c][wid] = ngc[c];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int tot = 0, items = 0;
-        for (int i = 0; i < kPrepWarps; i++) { const int g = s_ngraph[i]; s_ngraph[i] = tot; tot += g; }
-        s_gbase = tot ? atomicAdd(&a.ctr->n_graph, tot) : 0;
-        (void)items;
+    if (threadIdx.x < kGraphClasses) {          // one thread per size class: block prefix + one atomic
+        const int c = threadIdx.x;
+        int tot = 0;
+        for (int i = 0; i < kPrepWarps; i++) { const int g = s_ngraph[c][i]; s_ngraph[c][i] = tot; tot += g; }
+        s_gbase[c] = tot ? atomicAdd(&a.ctr->n_graph_cls[c], tot) : 0;
+        if (tot) atomicAdd(&a.ctr->n_graph, tot);
     }
     __syncthreads();
     if (live && lane == 0) {
-        int gpos = s_gbase + s_ngraph[wid];
+        int gpos[kGraphClasses];
+        for (int c = 0; c < kGraphClasses; c++) gpos[c] = s_gbase[c] + s_ngraph[c][wid];
         for (int t = 0; t < nraw; t++) {
             Item it;
             it.qid = (int32_t)q;
@@ -110,7 +115,10 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
                 it.meta = cpath[t] | pred | (nch == 1 && !remote ? META_DIRECT : 0u);
                 if (remote) atomicAdd(&a.ctr->remote[ix.owner[l]], 1);
                 else if (cpath[t] == PATH_SCAN) it.rank = atomicAdd(a.ls_count + ix.dir[l].bslot, 1);
-                else a.graph_list[gpos++] = (int32_t)(lo + t);
+                else {
+                    const int c = graph_class(ix.dir[l].size);
+                    a.graph_list[c * a.graph_stride + gpos[c]++] = (int32_t)(lo + t);
+                }
             } else {
                 it.label = -1;
                 it.meta = PATH_NONE;
@@ -522,7 +530,11 @@ __global__ void k_unpack_items(SearchArgs a, const uint8_t *__restrict__ recv, i
         it.rank = 0;
         it.meta = path | h->pred | META_DIRECT;
         if (path == PATH_SCAN) it.rank = atomicAdd(a.ls_count + d.bslot, 1);
-        else a.graph_list[atomicAdd(&a.ctr->n_graph, 1)] = (int32_t)i;
+        else {
+            const int c = graph_class(d.size);
+            a.graph_list[c * a.graph_stride + atomicAdd(&a.ctr->n_graph_cls[c], 1)] = (int32_t)i;
+            atomicAdd(&a.ctr->n_graph, 1);
+        }
         a.items[i] = it;
     }
 }

@@ -614,7 +614,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     VF_CUDA(sc->qinfo.ensure((size_t)std::max<int64_t>(n, 1) * sizeof(QueryInfo)));
     VF_CUDA(sc->items.ensure((size_t)slots * sizeof(Item)));
     VF_CUDA(sc->item_ctr.ensure((size_t)slots * 12));
-    VF_CUDA(sc->graph_list.ensure((size_t)slots * 4));
+    VF_CUDA(sc->graph_list.ensure((size_t)slots * kGraphClasses * 4));
     VF_CUDA(sc->scan_slots.ensure((size_t)slots * 4));
     VF_CUDA(sc->scan_q.ensure((size_t)slots * sizeof(ScanQuery)));
     VF_CUDA(sc->segs.ensure((size_t)slots * sizeof(Segment)));
@@ -655,6 +655,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.ls_segbase = sc->ls_segbase.as<int32_t>();
     a.ls_itembase = sc->ls_itembase.as<int32_t>();
     a.graph_list = sc->graph_list.as<int32_t>();
+    a.graph_stride = slots;
     a.scan_slots = sc->scan_slots.as<int32_t>();
     a.scan_q = sc->scan_q.as<ScanQuery>();
     a.segs = sc->segs.as<Segment>();

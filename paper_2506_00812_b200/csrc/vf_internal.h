@@ -8,7 +8,14 @@ namespace vf {
 
 constexpr int kMaxQueryLabels = 64;   // labels per query accepted by vf_search
 constexpr int kMaxK = 256;
-constexpr int kMaxBitmaps = 256;      // membership bitmaps of the largest labels (predicate fast path)
+constexpr int kMaxBitmaps = 256;
+// Graph items are claimed largest-label class first: an item's beam-search cost grows with log |C_l|
+// (oracle counters on SIFT-like: corr(log |C_l|, V) = 0.77), so long items start early and the
+// kernel's tail shrinks (longest-processing-time-first at class granularity).
+constexpr int kGraphClasses = 4;
+__host__ __device__ __forceinline__ int graph_class(int32_t size) {
+    return size >= 131072 ? 0 : size >= 32768 ? 1 : size >= 8192 ? 2 : 3;
+}      // membership bitmaps of the largest labels (predicate fast path)
 constexpr int kMaxItopk = 1024;
 constexpr int kScanQG = 64;           // queries per scan segment (query group)
 constexpr int kWarpsPerGraphCta = 4;
@@ -131,6 +138,7 @@ struct ScanQuery {
 // Device counters, zeroed at the start of every search.
 struct Counters {
     int32_t n_graph;
+    int32_t n_graph_cls[4];  // graph items per label-size class (kGraphClasses; largest labels first)
     int32_t n_segs;
     int32_t n_scan_items;
     int32_t n_tiles;
@@ -166,7 +174,8 @@ struct SearchArgs {
     int32_t *ls_count;        // [n_bslots] scan items per label in this batch
     int32_t *ls_segbase;      // [n_bslots] first segment of the label
     int32_t *ls_itembase;     // [n_bslots] first scan_slots entry of the label
-    int32_t *graph_list;      // [slots]
+    int32_t *graph_list;      // [kGraphClasses][graph_stride] graph item slots, one list per size class
+    int64_t graph_stride;
     int32_t *scan_slots;      // [slots]
     ScanQuery *scan_q;        // [slots] per scan item, scan_slots order
     Segment *segs;            // [slots]
