@@ -63,6 +63,7 @@ struct Scratch {
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
     // per-query path (f1): per-CTA item lists of a query split over several CTAs, completion counters
     DevBuf small_part, small_cnt;
+    DevBuf tile_cls;            // scan tiles by row-count class (claim order of the tensor-core scan)
     // scan / graph overlap: the graph kernels run on a side stream forked after routing
     cudaStream_t side = nullptr, side_hi = nullptr;   // graph kernels; scan kernels (high priority)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;

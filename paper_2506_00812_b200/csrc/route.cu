@@ -185,6 +185,10 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 tl.pad = 0;
                 tl.n_pieces = -1;
                 a.tiles[tb + t] = tl;
+                if (a.tile_cls && !a.split_tiles) {
+                    const int c = tile_class(tl.row_end - tl.row_begin);
+                    a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = tb + t;
+                }
                 if (a.split_tiles) {
                     if (warp_tiles) a.wtiles[atomicAdd(&a.ctr->n_wtiles, 1)] = tb + t;
                     else a.btiles[atomicAdd(&a.ctr->n_btiles, 1)] = tb + t;

@@ -380,6 +380,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
         // between one tile's last row stage and the next tile's first.
         uint32_t tc = 0;
         const int ntiles = a.split_tiles ? a.ctr->n_btiles : a.ctr->n_tiles;
+        const bool by_cls = a.tile_cls && !a.split_tiles;   // longest tiles first (row-count classes)
+        int cum[kTileClasses + 1];
+        cum[0] = 0;
+        for (int c = 0; c < kTileClasses; c++) cum[c + 1] = cum[c] + (by_cls ? a.ctr->n_tile_cls[c] : 0);
         for (;;) {
             const int tp = tc & 1;
             if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
@@ -388,7 +392,11 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
             if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
             t = __shfl_sync(FULL, t, 0);
             if (t < ntiles && a.split_tiles) t = a.btiles[t];
-            else if (t >= ntiles) t = INT32_MAX;
+            else if (t < ntiles && by_cls) {
+                int c = 0;
+                while (c + 1 < kTileClasses && t >= cum[c + 1]) c++;
+                t = a.tile_cls[(int64_t)c * a.max_tiles + (t - cum[c])];
+            } else if (t >= ntiles) t = INT32_MAX;
             if (t == INT32_MAX) {
                 if (lane == 0) {
                     tinfo[tp].tile = -1;

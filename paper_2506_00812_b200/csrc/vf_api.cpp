@@ -660,6 +660,11 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.scan_q = sc->scan_q.as<ScanQuery>();
     a.segs = sc->segs.as<Segment>();
     a.tiles = sc->tiles.as<Tile>();
+    a.tile_cls = nullptr;
+    if (pl.tc && !pl.wsplit) {
+        VF_CUDA(sc->tile_cls.ensure((size_t)kTileClasses * (size_t)std::max<int64_t>(a.max_tiles, 1) * 4));
+        a.tile_cls = sc->tile_cls.as<int32_t>();
+    }
     a.item_seg = sc->item_seg.as<int32_t>();
     a.item_res = sc->item_res.as<unsigned long long>();
     a.partials = pl.multi ? sc->partials.as<unsigned long long>() : nullptr;

@@ -12,6 +12,10 @@ constexpr int kMaxBitmaps = 256;
 // Graph items are claimed largest-label class first: an item's beam-search cost grows with log |C_l|
 // (oracle counters on SIFT-like: corr(log |C_l|, V) = 0.77), so long items start early and the
 // kernel's tail shrinks (longest-processing-time-first at class granularity).
+constexpr int kTileClasses = 4;
+__host__ __device__ __forceinline__ int tile_class(int32_t rows) {
+    return rows >= 1024 ? 0 : rows >= 512 ? 1 : rows >= 256 ? 2 : 3;
+}
 constexpr int kGraphClasses = 4;
 __host__ __device__ __forceinline__ int graph_class(int32_t size) {
     return size >= 131072 ? 0 : size >= 32768 ? 1 : size >= 8192 ? 2 : 3;
@@ -148,6 +152,7 @@ struct Counters {
     int32_t exact_fallback;  // a query of this batch is outside the fast path's exact range (gate)
     int32_t filter_next;     // k_hs_filter tile cursor
     int32_t n_wtiles, n_btiles;   // tiles for k_scan_warp / k_scan_tc (split_tiles)
+    int32_t n_tile_cls[4];        // scan tiles per row-count class (kTileClasses; longest first)
     int32_t wscan_next;
     int32_t pool_used;       // survivor pool bump allocator
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
@@ -208,6 +213,8 @@ struct SearchArgs {
     int32_t tc_parts;         // TC scan: split few-query tiles over several warps (VF_TC_PARTS=0 off)
     int32_t split_tiles;      // small tiles to k_scan_warp (wtiles), the rest to k_scan_tc (btiles)
     int32_t *wtiles, *btiles;
+    int32_t *tile_cls;        // [kTileClasses][max_tiles] tile indices by row-count class (tensor-core scan
+                              // claims longest tiles first; nullptr = creation order)
     int32_t *pool;            // AND pre-filter survivor ids (k_hs_filter)
     int32_t pool_cap;
 };
