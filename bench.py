@@ -1,27 +1,37 @@
 #!/usr/bin/env python3
 """bench.py -- QPS at recall@10 >= 0.90 / 0.99 for batched label-filtered top-k search on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config sift|yfcc|tiny] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config yfcc|sift|tiny] [--impl ours|reference]
 
 A "step" is one vf_search call over the whole query batch of the workload (route -> scan ->
 graph -> merge, all §8(a) rows) with queries, labels and outputs resident in HBM. The workload is
-BASELINE.json configs[1] (SIFT-like: 1M x 128 fp32 integer-valued vectors, 1K Zipf labels, 10K
-single-label queries, k = 10) unless --config says otherwise; see DESIGN.md §3 for the recipe.
+BASELINE.json configs[2] (YFCC-10M-shaped: 10M x 192 u8 vectors, 200,386 Zipf labels, 100K
+queries mixing single-label and two-label AND, k = 10) -- the configuration the metric is quoted
+on -- unless --config says otherwise (configs[1] SIFT-like, configs[0] tiny); DESIGN.md §3 has the
+recipe.
 
 Ground truth comes from vf_search in exact mode (T = infinity; parity-tested bit-exact against the
-CPU oracle in tests/). The operating point for a recall target is the smallest itopk of the grid
-whose mean recall@10 reaches it. L2 is flushed (256 MiB write) before every timed step, outside
-the step's CUDA events. Under torchrun (N > 1) the index is label-sharded across the ranks (LPT
-over |C_l|; X and the predicate table replicated; items exchanged with NCCL inside vf_search) and
-every rank brings its own batch (weak scaling); rank 0 prints the line with value = all ranks'
-queries / max-over-ranks time.
-The CPU oracle is used ONLY for the cpu_baseline leg and for --impl reference.
+CPU oracle in tests/) for EVERY query of the batch. The operating point for a recall target is the
+fastest configuration of the sweep (recall policy x f3 threshold x search width x itopk grid)
+whose mean tie-aware recall@10 reaches it; `at_recall` holds the best overall, `at_recall_paper`
+the best with the paper's routing only (f3 off: greedy or parallel AND), each with
+per-class (single / AND2) and per-path (scan / graph / mixed items) recall. L2 is flushed (256 MiB
+write) before every timed step, outside the step's CUDA events.
+
+--gpus N > 1 (configs[4]): N ranks (re-launched through torch.distributed.run when WORLD_SIZE is
+unset), the index label-sharded across them (LPT over |C_l|; X and the predicate table replicated;
+items exchanged with NCCL inside vf_search); the 1M-query batch is split evenly over the ranks
+(strong scaling); rank 0 prints the line with value = all ranks' queries / max-over-ranks time.
+The CPU oracle is used ONLY in the cpu_baseline leg (which also compares its answers with the
+GPU's on the sample) and for --impl reference.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -32,13 +42,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from workload.metrics import recall_per_query  # noqa: E402  (measurement only, no method arithmetic)
+
 CFG_INDEX = {"tiny": 0, "sift": 1, "yfcc": 2}
 # the 0.90 operating point our arm measured per workload (itopk, search_width, and_scan_threshold,
-# scan_threshold);
-# the reference arm (the oracle) runs at it so both arms answer the same searches
-OP_POINT = {"tiny": (32, 1, 0, 0), "sift": (16, 2, 0, 0), "yfcc": (48, 2, 2000, 0)}
+# scan_threshold, recall_mode); the reference arm (the oracle) runs at it so both arms answer the
+# same searches
+OP_POINT = {"tiny": (32, 1, 0, 0, "greedy"), "sift": (16, 2, 0, 0, "greedy"), "yfcc": (48, 2, 2000, 0, "greedy")}
 ITOPK_GRID = (16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512)
 METRIC = "QPS at recall@10 >=0.90 and >=0.99 (1/2/4/8 B200); p50 latency at batch 1"
+SHARDED_QUERIES = 1_000_000          # BASELINE.json configs[4]: the 1M-query batch at N > 1
 
 
 def log(*a):
@@ -46,11 +59,37 @@ def log(*a):
         print("[bench]", *a, file=sys.stderr, flush=True)
 
 
+def build_ids():
+    """Which code produced the numbers: git HEAD when .git is present, and the library's hash."""
+    ids = {}
+    try:
+        ids["git"] = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                                    text=True, timeout=5).stdout.strip() or None
+    except Exception:
+        ids["git"] = None
+    so = os.path.join(ROOT, "paper_2506_00812_b200", "libvecflow.so")
+    if os.path.exists(so):
+        with open(so, "rb") as f:
+            ids["libvecflow_sha256_16"] = hashlib.sha256(f.read()).hexdigest()[:16]
+    return ids
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ----------------------------------------------------------------------------- workload
-def make_inputs(config: str, device, query_stream: int = 0):
+def make_inputs(config: str, device, query_stream: int = 0, n_queries=None):
     from workload import gen, graphs
     t0 = time.time()
-    w = gen.make_workload(config, query_stream=query_stream)
+    w = gen.make_workload(config, n_queries=n_queries, query_stream=query_stream)
     c = w.cfg
     log(f"workload {config}: N={c.n_points} D={c.dim} L={c.n_labels} Q={c.n_queries} "
         f"dtype={c.dtype} ({time.time() - t0:.1f}s)")
@@ -71,21 +110,36 @@ def make_inputs(config: str, device, query_stream: int = 0):
     return w, go, gi
 
 
-def recall_vs(ids, d, gt, gd, k):
-    """(strict, tie-aware) recall@k against the exact ground truth (reading #24)."""
-    strict, tie = [], []
-    for i in range(ids.shape[0]):
-        g = gt[i][gt[i] >= 0]
-        if g.size == 0:
-            continue
-        a = ids[i][ids[i] >= 0]
-        hits = np.intersect1d(a, g).size
-        kth = gd[i][g.size - 1]
-        extra = int(np.sum((~np.isin(a, g)) & (d[i][:a.size] == kth)))
-        den = min(k, g.size)
-        strict.append(hits / den)
-        tie.append(min(1.0, (hits + extra) / den))
-    return float(np.mean(strict)), float(np.mean(tie))
+def query_classes(w):
+    """Per query: number of distinct labels (1 = single-label, 2 = AND2 for the mixed batches)."""
+    nl = np.empty(len(w.Q), np.int32)
+    for i in range(len(w.Q)):
+        nl[i] = np.unique(w.q_lab[w.q_off[i]:w.q_off[i + 1]]).size
+    return nl
+
+
+def query_paths(recs, n):
+    """Per query from the item records (vf_get_last_items): 1 = all its items scanned, 2 = all
+    graph-searched, 3 = mixed, 0 = no item (empty row)."""
+    p = np.zeros(n, np.int32)
+    if len(recs):
+        q = recs[:, 0].astype(np.int64)
+        path = recs[:, 2]
+        np.bitwise_or.at(p, q[path == 1], 1)
+        np.bitwise_or.at(p, q[path == 2], 2)
+    return p
+
+
+def split_recall(strict, tie, valid, nl, paths):
+    """Mean tie-aware (and strict) recall per query class and per item path."""
+    out = {}
+    groups = {"single": nl == 1, "and2": nl == 2, "scan": paths == 1, "graph": paths == 2, "mixed": paths == 3}
+    for name, m in groups.items():
+        m = m & valid
+        if m.any():
+            out[name] = {"n": int(m.sum()), "recall_tie_aware": float(np.mean(tie[m])),
+                         "recall_strict": float(np.mean(strict[m]))}
+    return out
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -164,17 +218,16 @@ def run_reference(args, config):
     n = len(w.Q) if args.ref_sample < 0 and config != "yfcc" else min(len(w.Q), 5000 if args.ref_sample < 0 else args.ref_sample)
     Q, qo, ql = w.Q[:n], w.q_off[:n + 1], w.q_lab[:w.q_off[n]]
     threads = os.cpu_count() or 1
-    # our arm's 0.90 operating point for this workload (profiles/r01_bench_*.json)
-    itopk, w_, as_, st_ = OP_POINT[config] if args.ref_itopk <= 0 else (args.ref_itopk, 1, 0, 0)
+    itopk, w_, as_, st_, mode = OP_POINT[config] if args.ref_itopk <= 0 else (args.ref_itopk, 1, 0, 0, "greedy")
     op = "and" if c.query_mode in ("and2", "mix_and") else ("or" if c.query_mode == "or2" else "single")
     for _ in range(args.warmup):
         o.search(Q[:64], qo[:65], ql[:qo[64]], k=c.k, itopk=itopk, search_width=w_, op=op, nthreads=threads,
-                 and_scan_threshold=as_, scan_threshold=st_)
+                 and_scan_threshold=as_, scan_threshold=st_, recall_mode=mode)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
         o.search(Q, qo, ql, k=c.k, itopk=itopk, search_width=w_, op=op, nthreads=threads, and_scan_threshold=as_,
-                 scan_threshold=st_)
+                 scan_threshold=st_, recall_mode=mode)
         times.append(time.perf_counter() - t0)
     total = float(np.sum(times))
     qps = n * args.steps / total
@@ -183,11 +236,27 @@ def run_reference(args, config):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"{config} (BASELINE.json configs[{CFG_INDEX[config]}])",
                                              "n_queries_per_step": n, "itopk": itopk, "search_width": w_,
-                                             "and_scan_threshold": as_, "scan_threshold": st_, "k": c.k, "flush": "n/a (CPU)"},
+                                             "and_scan_threshold": as_, "scan_threshold": st_, "recall_mode": mode,
+                                             "k": c.k, "flush": "n/a (CPU)"},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"first {n} queries of the {config} batch per step, itopk={itopk}, w={w_}"},
-            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "build": build_ids()}
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- multi-GPU launch
+def relaunch_distributed(args_list, n):
+    """`bench.py --gpus N` without torchrun: re-run this script under torch.distributed.run with N
+    ranks on this node (NCCL between them); returns its exit code."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + args_list
+    log("launching:", " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -196,33 +265,42 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="sift", choices=["tiny", "sift", "yfcc"])
+    ap.add_argument("--config", default="yfcc", choices=["tiny", "sift", "yfcc"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--targets", default="0.90,0.99")
     ap.add_argument("--widths", default="1,2,4", help="search widths w swept for the operating points")
     ap.add_argument("--lat-calls", type=int, default=1000, help="timed calls per small-batch latency point")
     ap.add_argument("--and-scan", default=None,
                     help="f3 selectivity-aware AND routing thresholds swept (0 = the paper's method)")
+    ap.add_argument("--modes", default=None, help="AND recall policies swept (greedy,parallel; P:L547-L555)")
     ap.add_argument("--scan-thr", default=None,
                     help="f2 search-time specificity thresholds T' swept (0 = the build's T; labels with "
                          "|C_l| < max(T, T') are scanned exactly)")
-    ap.add_argument("--gt-sample", type=int, default=-1,
-                    help="queries whose exact ground truth is computed for recall (-1: all; yfcc: 5000)")
+    ap.add_argument("--gt-sample", type=int, default=0,
+                    help="queries whose exact ground truth is computed for recall (0: all of them)")
     ap.add_argument("--cpu-sample", type=int, default=2000)
     ap.add_argument("--ref-sample", type=int, default=-1, help="queries per reference step (-1: all; yfcc 5000)")
     ap.add_argument("--ref-itopk", type=int, default=0, help="0: our arm's 0.90 operating point")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="cpu_baseline: repeat the oracle over the sample until this much CPU time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-paper-timing", action="store_true", help="skip timing the paper-routing operating points")
     ap.add_argument("--dump-stats", default=None)
     args = ap.parse_args()
 
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        sys.exit(relaunch_distributed(sys.argv[1:], args.gpus))
+    world = int(world_env or "1")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
     if args.and_scan is None:
         args.and_scan = "0,2000,50000" if args.config == "yfcc" else "0"
+    if args.modes is None:
+        args.modes = "greedy,parallel" if args.config == "yfcc" else "greedy"
     if args.scan_thr is None:
         args.scan_thr = "0,10000" if args.config == "sift" else "0"
-    if args.gt_sample < 0:
-        args.gt_sample = 5000 if args.config == "yfcc" else 0
     if args.impl == "reference":
         run_reference(args, args.config)
         return
@@ -231,7 +309,6 @@ def main():
     import torch.distributed as dist
     import paper_2506_00812_b200 as vf
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -243,7 +320,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    w, go, gi = make_inputs(args.config, dev, query_stream=rank)
+    # N > 1: the 1M-query batch of configs[4], split evenly (rank r draws its own slice's stream)
+    nq_rank = SHARDED_QUERIES // world if world > 1 else None
+    w, go, gi = make_inputs(args.config, dev, query_stream=rank, n_queries=nq_rank)
     c = w.cfg
     t0 = time.time()
     if world > 1:
@@ -267,14 +346,14 @@ def main():
     n_ql = int(w.q_off[-1])            # = len(q_lab): lets vf_search skip reading q_off[n] back
     ids = torch.empty((n, k), dtype=torch.int32, device=dev)
     dd = torch.empty((n, k), dtype=torch.float32, device=dev)
+    nl_q = query_classes(w)
 
     # -- ground truth: exact mode (T = inf), in query chunks
     t0 = time.time()
-    # recall sample: the first m queries of the batch (all of them unless --gt-sample says fewer)
     m_gt = n if args.gt_sample <= 0 else min(n, args.gt_sample)
     gt = np.empty((m_gt, k), np.int32)
     gd = np.empty((m_gt, k), np.float32)
-    step = 2000
+    step = 20000
     for s in range(0, m_gt, step):
         e = min(m_gt, s + step)
         Qs, qos, qls = Q[s:e], qo[s:e + 1] - qo[s], ql[int(w.q_off[s]):int(w.q_off[e])]
@@ -285,63 +364,96 @@ def main():
         gt[s:e], gd[s:e] = ti.cpu().numpy(), td.cpu().numpy()
     log(f"ground truth (exact mode) for {m_gt} queries: {time.time() - t0:.1f}s")
 
-    # -- (search_width, itopk) sweep -> operating points: for each recall target the fastest
-    #    configuration whose mean tie-aware recall@10 reaches it (the paper traces QPS-recall curves
-    #    by sweeping its search parameters)
+    # -- sweep -> operating points: for each recall target the fastest configuration whose mean
+    #    tie-aware recall@10 reaches it (the paper traces QPS-recall curves by sweeping its search
+    #    parameters); per family (recall policy, f3, f2) and search width
     targets = [float(x) for x in args.targets.split(",")]
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
 
-    def quick_ms(itopk, w_, as_=0, st_=0):
+    def run(cfg_):
+        itopk, w_, as_, st_, mode = cfg_
+        ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode,
+                       and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+
+    def quick_ms(cfg_):
         ms = []
         for _ in range(3):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+            run(cfg_)
             e1.record(stream)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
         return float(np.median(ms))
 
+    def recall_now():
+        st_, ta, v = recall_per_query(ids[:m_gt].cpu().numpy(), gt, dd[:m_gt].cpu().numpy(), gd, k)
+        return st_, ta, v
+
     sweep = []
+    modes = [m for m in args.modes.split(",")] if op == "and" else ["greedy"]
     and_scans = [int(x) for x in args.and_scan.split(",")] if op == "and" else [0]
     scan_thrs = [int(x) for x in args.scan_thr.split(",")]
-    for as_, st_, w_ in [(a_, t_, b_) for a_ in and_scans for t_ in scan_thrs
-                         for b_ in (int(x) for x in args.widths.split(","))]:
-        for itopk in ITOPK_GRID:
-            if itopk < k:
-                continue
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
-            torch.cuda.synchronize()
-            r_strict, r_tie = recall_vs(ids[:m_gt].cpu().numpy(), dd[:m_gt].cpu().numpy(), gt, gd, k)
-            qms = quick_ms(itopk, w_, as_, st_)
-            if world > 1:   # every rank takes the same decisions (the searches are collective)
-                t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
-                dist.all_reduce(t)
-                r_strict, r_tie, qms = (float(x) / world for x in t.tolist())
-            sweep.append((itopk, r_strict, r_tie, w_, qms, as_, st_))
-            log(f"and_scan={as_} scan_thr={st_} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} tie-aware={r_tie:.4f} "
-                f"{n / qms / 1e3:.2f} MQPS")
-            if r_tie >= max(targets):
-                break
-    ops = {}
-    for tgt in targets:
-        ok = [s for s in sweep if s[2] >= tgt]
-        ops[tgt] = min(ok, key=lambda s: s[4]) if ok else None
+    families = []
+    for mode in modes:
+        for as_ in (and_scans if mode == "greedy" else [0]):      # f3 routes greedy AND items only
+            for st_ in scan_thrs:
+                families.append((mode, as_, st_))
+    t_sweep = time.time()
+    for mode, as_, st_ in families:
+        for w_ in (int(x) for x in args.widths.split(",")):
+            for itopk in ITOPK_GRID:
+                if itopk < k:
+                    continue
+                cfg_ = (itopk, w_, as_, st_, mode)
+                run(cfg_)
+                torch.cuda.synchronize()
+                rs, rt, v = recall_now()
+                r_strict, r_tie = float(np.mean(rs[v])), float(np.mean(rt[v]))
+                qms = quick_ms(cfg_)
+                if world > 1:   # every rank takes the same decisions (the searches are collective)
+                    t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
+                    dist.all_reduce(t)
+                    r_strict, r_tie, qms = (float(x) / world for x in t.tolist())
+                sweep.append({"recall_mode": mode, "and_scan_threshold": as_, "scan_threshold": st_,
+                              "search_width": w_, "itopk": itopk, "recall_strict": r_strict,
+                              "recall_tie_aware": r_tie, "ms": qms})
+                log(f"{mode:8s} f3={as_:5d} T'={st_:5d} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} "
+                    f"tie-aware={r_tie:.4f} {n * world / qms / 1e3:.2f} MQPS")
+                if r_tie >= max(targets):
+                    break
+    log(f"sweep: {len(sweep)} points in {time.time() - t_sweep:.0f}s")
+
+    def cfg_of(s):
+        return (s["itopk"], s["search_width"], s["and_scan_threshold"], s["scan_threshold"], s["recall_mode"])
+
+    def best(tgt, paper_only):
+        ok = [s for s in sweep if s["recall_tie_aware"] >= tgt and
+              (not paper_only or (s["and_scan_threshold"] == 0 and s["scan_threshold"] == 0))]
+        return min(ok, key=lambda s: s["ms"]) if ok else None
+
+    ops = {tgt: best(tgt, False) for tgt in targets}
+    ops_paper = {tgt: best(tgt, True) for tgt in targets}
+
+    def split_at(s):
+        """per-class / per-path recall of one operating point (one more search + item records)"""
+        run(cfg_of(s))
+        torch.cuda.synchronize()
+        rs, rt, v = recall_now()
+        recs = ix.last_items(stream) if world == 1 else np.zeros((0, 6), np.int32)
+        paths = query_paths(recs, n)[:m_gt]
+        return split_recall(rs, rt, v, nl_q[:m_gt], paths)
 
     ix.set_profiling(True)
     hbm_peak, peak_kind = measured_peaks()
 
-    def timed(itopk, w_, as_, st_):
+    def timed(cfg_):
         """W warm-up + exactly K timed steps; per-step CUDA events around vf_search only."""
         for _ in range(args.warmup):
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+            run(cfg_)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
-        stats = []
         barrier()
         torch.cuda.synchronize()
         ix.set_profiling(True)          # phase means are taken over the K timed steps only
@@ -349,53 +461,62 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+            run(cfg_)
             ev[i][1].record(stream)
         # no host sync inside the loop: the host enqueues step i+1 while the device runs step i,
         # so the events time the device work (host-side cost is what `e2e` measures)
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
-        stats.append(ix.last_stats(stream))       # work counters of the last step + phase means of all K
+        stats = ix.last_stats(stream)     # work counters of the last step + phase means of all K
         barrier()
         ms = [a.elapsed_time(b) for a, b in ev]
-        return ms, stats
+        tot = float(np.sum(ms))
+        if world > 1:
+            t = torch.tensor([tot], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+        return tot, stats
 
-    results = {}
+    results, results_paper = {}, {}
+    main_tgt = targets[0]
     with ClockSampler(local) as clk:
-        for tgt, opnt in ops.items():
-            if opnt is None:
-                continue
-            itopk, w_, as_, st_ = opnt[0], opnt[3], opnt[5], opnt[6]
-            ms, stats = timed(itopk, w_, as_, st_)
-            tot = float(np.sum(ms))
-            if world > 1:
-                t = torch.tensor([tot], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                tot = float(t.item())
-            results[tgt] = (itopk, opnt, ms, stats, tot)
+        for tgt, s in ops.items():
+            if s is not None:
+                tot, stats = timed(cfg_of(s))
+                results[tgt] = (s, tot, stats, split_at(s))
+        if not args.no_paper_timing:
+            for tgt, s in ops_paper.items():
+                if s is None:
+                    continue
+                if ops.get(tgt) is not None and cfg_of(ops[tgt]) == cfg_of(s):
+                    results_paper[tgt] = results[tgt]
+                else:
+                    tot, stats = timed(cfg_of(s))
+                    results_paper[tgt] = (s, tot, stats, split_at(s))
     clocks = clk.summary()
 
     # -- end to end through the C-ABI with host (pinned) buffers, copies inside the timed region
-    main_tgt = targets[0]
     e2e = None
     if main_tgt in results:
-        itopk, w_, as_, st_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5], results[main_tgt][1][6]
+        cfg_main = cfg_of(results[main_tgt][0])
         Qh = torch.from_numpy(w.Q).pin_memory()
         qoh = torch.from_numpy(w.q_off).pin_memory()
         qlh = torch.from_numpy(w.q_lab).pin_memory()
         oih = torch.empty((n, k), dtype=torch.int32).pin_memory()
         odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
-        for _ in range(args.warmup):
-            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
+        itopk, w_, as_, st_, mode = cfg_main
+
+        def run_host():
+            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode,
                            and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+        for _ in range(args.warmup):
+            run_host()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.steps):
-            ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+            run_host()
         e1.record(stream)
         torch.cuda.synchronize()
         et = e0.elapsed_time(e1)
@@ -413,7 +534,7 @@ def main():
     #    with device-resident buffers; wall clock per blocking call, p50 / p99 over many calls
     latency = None
     if main_tgt in results and world == 1 and args.lat_calls > 0:
-        itopk, w_, as_, st_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5], results[main_tgt][1][6]
+        itopk, w_, as_, st_, mode = cfg_of(results[main_tgt][0])
         latency = {}
         for bsz in (1, 10, 100):
             Qh = torch.from_numpy(w.Q[:bsz].copy()).pin_memory()
@@ -425,22 +546,22 @@ def main():
             oid = torch.empty((bsz, k), dtype=torch.int32, device=dev)
             odd = torch.empty((bsz, k), dtype=torch.float32, device=dev)
             res = {}
-            for mode in ("host", "device"):
+            for mode_ in ("host", "device"):
                 ts = []
                 for it_ in range(args.lat_calls + 50):
                     t0 = time.perf_counter()
-                    if mode == "host":
+                    if mode_ == "host":
                         ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                                       and_scan_threshold=as_, stream=stream, scan_threshold=st_)
+                                       recall_mode=mode, and_scan_threshold=as_, stream=stream, scan_threshold=st_)
                     else:
                         ix.search_into(Qd, qod, qld, oid, odd, k=k, itopk=itopk, search_width=w_, op=op,
-                                       and_scan_threshold=as_, stream=stream, n_query_labels=int(w.q_off[bsz]),
-                                       scan_threshold=st_)
+                                       recall_mode=mode, and_scan_threshold=as_, stream=stream,
+                                       n_query_labels=int(w.q_off[bsz]), scan_threshold=st_)
                         stream.synchronize()
                     if it_ >= 50:
                         ts.append(time.perf_counter() - t0)
-                res[mode] = {"p50_ms": 1e3 * float(np.percentile(ts, 50)),
-                             "p99_ms": 1e3 * float(np.percentile(ts, 99))}
+                res[mode_] = {"p50_ms": 1e3 * float(np.percentile(ts, 50)),
+                              "p99_ms": 1e3 * float(np.percentile(ts, 99))}
             latency[f"batch{bsz}"] = res
         # f1: the persistent serving kernel (vf_serve_*) -- single-query latency (one job
         # in flight, host query in, host result out) and single-batch-mode throughput (every query
@@ -448,8 +569,8 @@ def main():
         try:
             labs = [np.ascontiguousarray(w.q_lab[w.q_off[i]:w.q_off[i + 1]]) for i in range(min(n, 20000))]
             Qn = np.ascontiguousarray(w.Q)
-            with ix.serve(k=k, itopk=itopk, search_width=w_, op=op, and_scan_threshold=as_, scan_threshold=st_,
-                          capacity=4096) as sv:
+            with ix.serve(k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode, and_scan_threshold=as_,
+                          scan_threshold=st_, capacity=4096) as sv:
                 oi_, od_ = np.empty(k, np.int32), np.empty(k, np.float32)
                 ts = []
                 for it_ in range(args.lat_calls + 50):
@@ -460,37 +581,54 @@ def main():
                         ts.append(time.perf_counter() - t0)
                 # the whole batch, each query its own job, from a C client loop (vf_serve_run)
                 sv.run(Qn[:1024], w.q_off[:1025], w.q_lab[:w.q_off[1024]], max_in_flight=1024)
-                m_q = n
                 t0 = time.perf_counter()
                 sv.run(Qn, w.q_off, w.q_lab, max_in_flight=1024)
                 el = time.perf_counter() - t0
                 latency["serve"] = {"device_means_us": sv.stats(),
                                     "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                                     "p99_ms": 1e3 * float(np.percentile(ts, 99)),
-                                    "single_batch_qps": m_q / el, "in_flight": 1024,
+                                    "single_batch_qps": n / el, "in_flight": 1024,
                                     "workers": sv.info()["n_workers"]}
         except Exception as e:   # reported, not fatal: the batched numbers stand on their own
             latency["serve"] = {"error": str(e)}
         log(f"latency: {latency}")
 
-    # -- CPU baseline: the oracle on this host's cores, bounded sample, rank 0 only
+    # -- CPU baseline: the oracle on this host's cores, bounded sample, rank 0 only; its answers
+    #    are also compared with the GPU's for the same queries (sampled parity on the full-size
+    #    arrays, in the launch configuration timed above)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
         import oracle
-        itopk, w_, as_, st_ = results[main_tgt][0], results[main_tgt][1][3], results[main_tgt][1][5], results[main_tgt][1][6]
+        cfg_main = cfg_of(results[main_tgt][0])
+        itopk, w_, as_, st_, mode = cfg_main
+        run(cfg_main)
+        torch.cuda.synchronize()
+        g_ids, g_d = ids.cpu().numpy(), dd.cpu().numpy()
         o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
         m = min(n, args.cpu_sample)
         threads = os.cpu_count() or 1
+        kw = dict(k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode, and_scan_threshold=as_,
+                  scan_threshold=st_)
         passes, el = 0, 0.0
+        oi = od = None
         while el < args.cpu_seconds and passes < 1000:
             t0 = time.perf_counter()
-            o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], k=k, itopk=itopk, search_width=w_, op=op,
-                     nthreads=threads, and_scan_threshold=as_, scan_threshold=st_)
+            oi, od = o.search(w.Q[:m], w.q_off[:m + 1], w.q_lab[:w.q_off[m]], nthreads=threads, **kw)
             el += time.perf_counter() - t0
             passes += 1
+        m1 = min(m, 200)
+        t0 = time.perf_counter()
+        o.search(w.Q[:m1], w.q_off[:m1 + 1], w.q_lab[:w.q_off[m1]], nthreads=1, **kw)
+        el1 = time.perf_counter() - t0
+        same_ids = int(np.sum(np.all(oi == g_ids[:m], axis=1)))
+        same_d = int(np.sum(np.all(od.astype(np.float32) == g_d[:m], axis=1)))
         cpu = {"value": m * passes / el, "unit": "queries/s", "cores": threads, "kind": "oracle",
-               "sample": f"first {m} of the {n} queries x {passes} passes, itopk={itopk}, w={w_}, "
-                         f"{threads} threads, {el:.1f}s"}
+               "cpu_model": cpu_model(),
+               "sample": f"first {m} of the {n} queries x {passes} passes at the 0.90 operating point "
+                         f"(itopk={itopk}, w={w_}, {mode}, f3={as_}), {threads} threads, {el:.1f}s",
+               "one_thread": {"value": m1 / el1, "unit": "queries/s", "sample": f"first {m1} queries, 1 thread"},
+               "parity_vs_gpu": {"queries": m, "rows_ids_identical": same_ids, "rows_dists_identical": same_d}}
+        log(f"cpu baseline / parity: {cpu}")
 
     if rank != 0:
         if world > 1:
@@ -500,18 +638,17 @@ def main():
         print(json.dumps({"metric": METRIC, "value": None, "error": "recall target not reached",
                           "sweep": sweep}), flush=True)
         return
-    itopk, opnt, ms, stats, tot = results[main_tgt]
+    s_main, tot, s0, split_main = results[main_tgt]
     K = args.steps
     qps = n * world * K / (tot / 1000.0)
-    # roofline of the dominant kernel (graph beam search): algorithmic bytes / kernel time
-    s0 = stats[-1]
+    # roofline of the dominant kernel: algorithmic bytes / kernel time
     rb = s0["row_bytes"]
     R = c.degree_R
-    # per graph item V vector rows + E adjacency rows of R (local, global) int32 pairs;
-    # per scan tile row: the X_LS row + its global id
+    # per graph item V vector rows + E adjacency rows of R (local, global) int32 pairs; per scan
+    # row: the row + its global id + its norm
     g_bytes = s0["graph_V"] * rb + s0["graph_E"] * R * 8
     g_ms = s0["mean_ms_graph"]
-    s_bytes = s0["scan_rows"] * (rb + 4)
+    s_bytes = s0["scan_rows"] * (rb + 8)
     s_ms = s0["mean_ms_scan"]
     # dominant kernel: the longer device-clock span (the phase events overlap when scan and graph
     # run concurrently); phase times if the spans are unavailable
@@ -519,45 +656,59 @@ def main():
     dom = ("graph" if ga >= sa else "scan") if (ga > 0 or sa > 0) else ("graph" if g_ms >= s_ms else "scan")
     bytes_dom, ms_dom = (g_bytes, g_ms) if dom == "graph" else (s_bytes, s_ms)
     achieved = bytes_dom / (ms_dom / 1000.0) / 1e9 if ms_dom > 0 else 0.0
-    # measured DRAM traffic of that kernel at this operating point, from a committed ncu capture
+    itopk, w_, as_, st_, mode = cfg_of(s_main)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(args.config)
         if tj and f"k_{dom}" in tj and (tj["itopk"], tj["search_width"], tj["and_scan_threshold"],
-                                        tj["scan_threshold"]) == (itopk, opnt[3], opnt[5], opnt[6]):
+                                        tj["scan_threshold"], tj.get("recall_mode", "greedy")) == (itopk, w_, as_, st_, mode):
             traffic = int(tj[f"k_{dom}"]["bytes"])
     except (OSError, ValueError, KeyError):
         traffic = None
-    # the dominant kernel's own device-clock span in the last timed step (first CTA start -> last
-    # CTA end): in an overlapped step the phase events above also count time the launched kernel
-    # waited for SMs held by the other phase
     act_ms = s0["ms_graph_active"] if dom == "graph" else s0["ms_scan_active"]
     act_gbs = bytes_dom / (act_ms / 1000.0) / 1e9 if act_ms > 0 else None
+
+    def at_entry(r):
+        s, t, st, split = r
+        return {"itopk": s["itopk"], "search_width": s["search_width"], "recall_mode": s["recall_mode"],
+                "and_scan_threshold": s["and_scan_threshold"], "scan_threshold": s["scan_threshold"],
+                "qps": n * world * K / (t / 1000.0), "ms_per_step": t / K,
+                "recall_strict": s["recall_strict"], "recall_tie_aware": s["recall_tie_aware"],
+                "by_class_and_path": split}
+
+    def best_reached(paper_only):
+        pool = [s for s in sweep if not paper_only or (s["and_scan_threshold"] == 0 and s["scan_threshold"] == 0)]
+        b = max(pool, key=lambda s: s["recall_tie_aware"]) if pool else None
+        return None if b is None else {k_: b[k_] for k_ in ("recall_mode", "and_scan_threshold", "search_width", "itopk",
+                                                            "recall_tie_aware")}
+
     line = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": tot / K, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": tot / K, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "u8" if (c.dtype == "u8" or info["bytes_u8_store"] > 0) else "f32",
         "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE.json configs[{CFG_INDEX[args.config]}])",
+        "config": {"workload": f"{args.config} (BASELINE.json configs[{CFG_INDEX[args.config]}])"
+                               + (f" label-sharded, configs[4] 1M-query batch split over {world} ranks" if world > 1 else ""),
                    "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
-                   "queries_per_step": n, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
-                   "R": R, "itopk": itopk, "search_width": opnt[3], "and_scan_threshold": opnt[5],
-                   "scan_threshold": opnt[6],
-                   "recall_target": main_tgt,
-                   "recall": {"strict": opnt[1], "tie_aware": opnt[2]},
-                   "recall_sample": f"first {m_gt} queries (exact-mode ground truth)",
+                   "queries_per_step": n * world, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
+                   "R": R, "itopk": itopk, "search_width": w_, "recall_mode": mode, "and_scan_threshold": as_,
+                   "scan_threshold": st_, "recall_target": main_tgt,
+                   "recall": {"strict": s_main["recall_strict"], "tie_aware": s_main["recall_tie_aware"]},
+                   "recall_sample": f"all {m_gt} queries (exact-mode ground truth)" if m_gt == n else f"first {m_gt} queries",
                    "flush": "256 MiB L2 flush before every timed step (outside the step events)",
                    "parallelism": f"label-shard{world}" if world > 1 else "single",
-                   "queries": "per rank (weak scaling)" if world > 1 else "batch",
                    "storage": ("u8 rows (lossless store of integer-valued fp32 in [0,255]; fp32 rows kept "
                                "for out-of-range query batches)") if (c.dtype != "u8" and info["bytes_u8_store"] > 0)
                               else c.dtype},
-        "at_recall": {f"{t:.2f}": {"itopk": r[0], "search_width": r[1][3], "and_scan_threshold": r[1][5], "scan_threshold": r[1][6], "qps": n * world * K / (r[4] / 1000.0),
-                                   "ms_per_step": r[4] / K, "recall_strict": r[1][1],
-                                   "recall_tie_aware": r[1][2]} for t, r in results.items()},
-        "sweep": [{"and_scan_threshold": s[5], "scan_threshold": s[6], "search_width": s[3], "itopk": s[0], "recall_strict": s[1], "recall_tie_aware": s[2],
-                   "ms": s[4]} for s in sweep],
+        "at_recall": {f"{t:.2f}": at_entry(r) for t, r in results.items()},
+        "at_recall_paper": {f"{t:.2f}": (at_entry(results_paper[t]) if t in results_paper else
+                                         ({"not_reached": True, "best": best_reached(True)} if ops_paper.get(t) is None
+                                          else {"untimed": ops_paper[t]}))
+                            for t in targets},
+        "max_recall": {"any": best_reached(False), "paper_routing": best_reached(True)},
+        "sweep": sweep,
         "roofline": {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full)" if traffic else None,
@@ -578,10 +729,11 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clocks,
         "index_bytes": info["bytes_total"],
+        "build": build_ids(),
     }
     if args.dump_stats:
         with open(args.dump_stats, "w") as f:
-            json.dump({"stats": stats, "ms": ms}, f)
+            json.dump({"stats": s0, "results": {str(t): r[2] for t, r in results.items()}}, f)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

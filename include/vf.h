@@ -124,7 +124,10 @@ typedef struct {
     /* Length of the query-label array (= qlabel_offsets[n]) when the offsets live in DEVICE memory:
      * > 0 lets vf_search size its work without reading qlabel_offsets[n] back (no stream sync, so
      * consecutive searches overlap their host and device work). 0 = read it (one stream sync).
-     * Must equal qlabel_offsets[n] when given; ignored for host offsets. */
+     * Must equal qlabel_offsets[n] when given; ignored for host offsets. With device offsets the
+     * library never reads outside [0, n_query_labels) of qlabels: a query whose offsets leave that
+     * range or that carries too many labels gets an empty row and is counted in
+     * vf_search_stats.n_invalid_queries (no error status: the check runs on the device). */
     int64_t n_query_labels;
 } vf_search_params;
 
@@ -224,6 +227,10 @@ typedef struct {
      * and of the graph kernel in the most recent search; 0 if the kernel did not run. Unlike the
      * phase events these exclude time a launched kernel waited for SMs (overlapped phases). */
     double ms_scan_active, ms_graph_active;
+    /* queries the device rejected (device offset arrays only; host arrays are checked before the
+     * search and fail it with VF_ERR_INVALID_ARG instead): labels outside [0, n_query_labels) or
+     * more labels than allowed (64; 16 on a label-sharded index). Their rows come out empty. */
+    int64_t n_invalid_queries;
 } vf_search_stats;
 
 vf_status vf_set_profiling(vf_index *index, int32_t enable);
@@ -254,6 +261,9 @@ vf_status vf_get_last_items(vf_index *index, void *cuda_stream, int64_t max_item
  *                    stay readable until `capacity` more queries have been submitted; a later wait
  *                    returns VF_ERR_INVALID_ARG. VF_ERR_CUDA if the kernel died.
  *   vf_serve_stop    stops the kernel once every submitted job is answered; frees the server.
+ * Environment VF_SERVE_IDLE_MS (read by vf_serve_start; default 0 = never): the kernel exits by
+ * itself after that many ms without a new job (a profiler that serialises launches would otherwise
+ * wait forever); later waits then return VF_ERR_CUDA.
  * The resident kernel occupies the GPU's SMs: batched vf_search calls on the same device compete
  * with it for SMs while it runs. The index must outlive the server.
  */

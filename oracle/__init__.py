@@ -218,28 +218,6 @@ def memory_model_gib(N, D, R, Rp, F, F_HS, F_LS, b):
     return hs, ls, hs + ls, L.or_mem_single_bytes(N, D, R, b) / g, L.or_mem_map_bytes(N, F, b) / g
 
 
-def recall_at_k(ids, gt_ids, gt_dists=None, dists_exact=None, k=10):
-    """Recall@K = |A cap GT| / min(K, |GT|) per query (reading #24), mean
-    over queries whose GT is non-empty. If gt_dists and dists_exact (the exact distance of every
-    returned id) are given, also the tie-aware variant: a returned id also counts as a hit when
-    its exact distance equals the K-th GT distance. Returns (strict, tie_aware or None)."""
-    ids = np.asarray(ids)[:, :k]
-    gt = np.asarray(gt_ids)[:, :k]
-    strict, tie = [], []
-    for i in range(ids.shape[0]):
-        g = gt[i][gt[i] >= 0]
-        if g.size == 0:
-            continue
-        a = ids[i][ids[i] >= 0]
-        hits = np.intersect1d(a, g).size
-        strict.append(hits / min(k, g.size))
-        if gt_dists is not None and dists_exact is not None:
-            kth = np.asarray(gt_dists)[i][g.size - 1]
-            extra = 0
-            for t, gid in enumerate(ids[i]):
-                if gid >= 0 and gid not in g and dists_exact[i][t] == kth:
-                    extra += 1
-            tie.append(min(1.0, (hits + extra) / min(k, g.size)))
-    s = float(np.mean(strict)) if strict else 1.0
-    ta = (float(np.mean(tie)) if tie else 1.0) if gt_dists is not None and dists_exact is not None else None
-    return s, ta
+# Recall@K (reading #24) is a measurement over result arrays, not part of the
+# method: one definition, shared with bench.py, pinned in tests/test_metrics.py.
+from workload.metrics import recall_at_k, recall_per_query  # noqa: E402,F401

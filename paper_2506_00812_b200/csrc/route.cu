@@ -75,7 +75,21 @@ __global__ void __launch_bounds__(32 * kPrepWarps) k_prepare(SearchArgs a, const
         }
 
         lo = a.q_off[q];
-        nraw = (int)(a.q_off[q + 1] - lo);
+        const int64_t hi = a.q_off[q + 1];
+        const bool bad = lo < 0 || hi < lo || hi > a.n_slots || hi - lo > a.max_nl;
+        if (bad) {
+            // never index outside the label array; a query whose own range is in bounds but too
+            // long marks its slots empty (no stale item is ever read from them)
+            if (lane == 0) atomicAdd(&a.ctr->n_invalid, 1);
+            if (lo >= 0 && hi >= lo && hi <= a.n_slots)
+                for (int64_t t = lo + lane; t < hi; t += 32) {
+                    Item it;
+                    it.qid = (int32_t)q; it.rank = 0; it.label = -1; it.meta = PATH_NONE;
+                    a.items[t] = it;
+                }
+            lo = 0;
+        }
+        nraw = bad ? 0 : (int)(hi - lo);
         int32_t *L = a.qlab + lo;   // the search's private copy of the labels, sorted in place
         if (a.qlab_in)              // fused copy of the caller's device labels (no separate memcpy)
             for (int t = lane; t < nraw; t += 32) L[t] = a.qlab_in[lo + t];
@@ -145,23 +159,15 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
         const LabelDir d = a.ix.dir[it.label];
         const int count = a.ls_count[d.bslot];
         const int nseg = (count + qg - 1) / qg;
-        // tiles per segment: small query groups on short lists are cut into kWarpTileRows-row tiles
-        // for the warp-per-tile scan (load balance); everything else uses tile_rows
-        auto seg_rows = [&](int g) {
-            const int nq = min(qg, count - g * qg);
-            return (a.split_tiles && nq <= kWarpScanQ && d.size <= kWarpScanRows) ? kWarpTileRows : a.tile_rows;
-        };
-        int total = 0;
-        for (int g = 0; g < nseg; g++) total += (d.size + seg_rows(g) - 1) / seg_rows(g);
+        const int tr = a.tile_rows;
+        const int ntile = (d.size + tr - 1) / tr;
+        const int total = nseg * ntile;
         const int seg0 = atomicAdd(&a.ctr->n_segs, nseg);
         const int ib = atomicAdd(&a.ctr->n_scan_items, count);
         int tb = atomicAdd(&a.ctr->n_tiles, total);
         a.ls_segbase[d.bslot] = seg0;
         a.ls_itembase[d.bslot] = ib;
         for (int g = 0; g < nseg; g++) {
-            const int tr = seg_rows(g);
-            const int ntile = (d.size + tr - 1) / tr;
-            const bool warp_tiles = tr == kWarpTileRows && a.split_tiles;
             Segment sg;
             sg.label = it.label;
             sg.item_base = ib + g * qg;
@@ -185,13 +191,9 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 tl.pad = 0;
                 tl.n_pieces = -1;
                 a.tiles[tb + t] = tl;
-                if (a.tile_cls && !a.split_tiles) {
+                if (a.tile_cls) {
                     const int c = tile_class(tl.row_end - tl.row_begin);
                     a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = tb + t;
-                }
-                if (a.split_tiles) {
-                    if (warp_tiles) a.wtiles[atomicAdd(&a.ctr->n_wtiles, 1)] = tb + t;
-                    else a.btiles[atomicAdd(&a.ctr->n_btiles, 1)] = tb + t;
                 }
             }
             tb += ntile;

@@ -379,8 +379,8 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
         // the tile slot of its parity ahead of the producer, so no dependent global round trip sits
         // between one tile's last row stage and the next tile's first.
         uint32_t tc = 0;
-        const int ntiles = a.split_tiles ? a.ctr->n_btiles : a.ctr->n_tiles;
-        const bool by_cls = a.tile_cls && !a.split_tiles;   // longest tiles first (row-count classes)
+        const int ntiles = a.ctr->n_tiles;
+        const bool by_cls = a.tile_cls != nullptr;          // longest tiles first (row-count classes)
         int cum[kTileClasses + 1];
         cum[0] = 0;
         for (int c = 0; c < kTileClasses; c++) cum[c + 1] = cum[c] + (by_cls ? a.ctr->n_tile_cls[c] : 0);
@@ -391,8 +391,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
             int t = 0;
             if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
             t = __shfl_sync(FULL, t, 0);
-            if (t < ntiles && a.split_tiles) t = a.btiles[t];
-            else if (t < ntiles && by_cls) {
+            if (t < ntiles && by_cls) {
                 int c = 0;
                 while (c + 1 < kTileClasses && t >= cum[c + 1]) c++;
                 t = a.tile_cls[(int64_t)c * a.max_tiles + (t - cum[c])];

@@ -175,6 +175,13 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
     r.part_done = sv->part_done.as<int32_t>();
     r.dev_head = reinterpret_cast<long long *>(sv->next.as<uint8_t>() + 16);
     r.dev_stop = reinterpret_cast<int32_t *>(sv->next.as<uint8_t>() + 32);
+    // VF_SERVE_IDLE_MS > 0: the resident kernel exits after that long without a new job (then
+    // vf_serve_wait reports VF_ERR_CUDA "serving kernel ended"); default: it runs until stopped
+    {
+        const char *e = getenv("VF_SERVE_IDLE_MS");
+        const long long ms = e ? atoll(e) : 0;
+        r.idle_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
+    }
 
     if ((e = cudaStreamCreateWithFlags(&sv->stream, cudaStreamNonBlocking)) != cudaSuccess)
         return bail(fail(VF_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e)));

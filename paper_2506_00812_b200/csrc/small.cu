@@ -451,10 +451,15 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_small(SearchArgs a, DevInd
     const SmallSmem s = small_smem(smem, L);
     small_init_bars(s, L.n_stages);
     uint32_t bar_phase = 0;
-    const int64_t lo = a.q_off[q];
-    const int nraw = (int)(a.q_off[q + 1] - lo);
+    int64_t lo = a.q_off[q];
+    const int64_t hi = a.q_off[q + 1];
+    // device-side check of the caller's offsets (empty row + n_invalid; see SearchArgs)
+    const bool bad = lo < 0 || hi < lo || hi > a.n_slots || hi - lo > a.max_nl;
+    if (bad && part == 0 && threadIdx.x == 0) atomicAdd(&a.ctr->n_invalid, 1);
+    if (bad) lo = 0;
+    const int nraw = bad ? 0 : (int)(hi - lo);
     small_query<DTF, TF, CF, TS, CS>(a, native, L, smem, a.Qraw + q * (int64_t)raw_bytes, raw_bytes, a.qlab + lo,
-                                     nraw, (int32_t)q, (int32_t)lo, a.out_ids + q * a.k, a.out_dists + q * a.k,
+                                     nraw, (int32_t)q, bad ? -1 : (int32_t)lo, a.out_ids + q * a.k, a.out_dists + q * a.k,
                                      (int)blockIdx.x * kSmallWarps, epochs, bar_phase, part, nparts,
                                      partials + (size_t)q * nparts * kMaxQueryLabels * kSmallMaxK, done_ctr + q);
 }
@@ -476,6 +481,8 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
         // published through the device head; workers never touch PCIe for their inputs.
         long long *sh = reinterpret_cast<long long *>(smem);
         long long copied = 0;
+        unsigned long long last_job = 0;
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(last_job));
         const int qv = ring.raw_stride / 16;             // 16-byte words of a query slot
         const int per_job = qv + kServeLabels / 4 + 1;   // + labels (4 x 16 B) + the count
         for (;;) {
@@ -487,8 +494,16 @@ __global__ void __launch_bounds__(32 * kSmallWarps) k_serve(SearchArgs a, DevInd
                     __threadfence_system();
                     h = *(volatile const long long *)ring.head;
                     if (h != copied || st) break;
+                    if (ring.idle_ns) {
+                        // idle exit: no job published for idle_ns (e.g. a profiler serialises the
+                        // launch, so the host can never submit); answered like a stop
+                        unsigned long long now;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                        if (now - last_job > ring.idle_ns) { st = 1; break; }
+                    }
                     __nanosleep(64);
                 }
+                if (h != copied) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(last_job));
                 sh[0] = h;
                 sh[1] = st;
             }

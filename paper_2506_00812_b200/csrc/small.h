@@ -45,6 +45,7 @@ struct ServeRing {
     unsigned long long *stats;          // [4] ns waiting for jobs, copying slots, searching; parts done
     uint8_t *dq;                        // device copies of the slots (written by the dispatcher CTA)
     int32_t *dlab, *dnlab;
+    unsigned long long idle_ns;         // > 0: the kernel exits after this long without a new job
 };
 
 bool small_supported(const DevIndex &fast, const DevIndex &native, bool two_views, int k);

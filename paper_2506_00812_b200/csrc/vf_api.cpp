@@ -558,23 +558,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0 || p->scan_threshold > D.T);
     a.pool = nullptr;
     a.pool_cap = 0;
-    // small tiles (<= 4 queries, <= 4096 rows) to the warp-per-tile scan, the rest to tcgen05 (opt-in)
-    {
-        // opt-in (VF_WARP_SCAN=1, read per search): measured slower than the tensor-core scan on
-        // both BASELINE workloads (scripts/ab_env.py), kept for small-group studies
-        const char *ws_env = getenv("VF_WARP_SCAN");
-        const bool ws_off = !(ws_env && atoi(ws_env) == 1);
-        const DevIndex &F8 = ix->enc8 ? ix->dev8 : D;
-        pl.wsplit = pl.tc && !ws_off && warp_scan_supported(F8.dtype, F8.row_bytes, k);
-        a.split_tiles = pl.wsplit ? 1 : 0;
-        a.wtiles = a.btiles = nullptr;
-        if (pl.wsplit && a.max_tiles_per_label < kWarpScanRows / kWarpTileRows) {
-            a.max_tiles_per_label = kWarpScanRows / kWarpTileRows;     // small-group lists, cut finer
-            pl.multi = true;
-            pl.max_tiles = std::max<int64_t>(n_slots, 1) * a.max_tiles_per_label;
-            a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
-        }
-    }
+    a.n_slots = n_slots;
+    a.max_nl = ix->world > 1 ? kRecLabels : kMaxQueryLabels;
     {
         const char *e = getenv("VF_TC_PARTS");
         a.tc_parts = e ? atoi(e) : 1;
@@ -592,12 +577,6 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
 
     bool fresh = false;
     VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
-    if (pl.wsplit) {
-        VF_CUDA(sc->wtiles.ensure((size_t)pl.max_tiles * 4));
-        VF_CUDA(sc->btiles.ensure((size_t)pl.max_tiles * 4));
-        a.wtiles = sc->wtiles.as<int32_t>();
-        a.btiles = sc->btiles.as<int32_t>();
-    }
     if (pl.filter) {
         int64_t cap = 16ll << 20;                       // 64 MB of survivor ids
         if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
@@ -661,7 +640,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.segs = sc->segs.as<Segment>();
     a.tiles = sc->tiles.as<Tile>();
     a.tile_cls = nullptr;
-    if (pl.tc && !pl.wsplit) {
+    if (pl.tc) {
         VF_CUDA(sc->tile_cls.ensure((size_t)kTileClasses * (size_t)std::max<int64_t>(a.max_tiles, 1) * 4));
         a.tile_cls = sc->tile_cls.as<int32_t>();
     }
@@ -682,8 +661,12 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     VF_CUDA(cudaMemsetAsync(sc->ctr.p, 0, sizeof(Counters), s));
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[1], s));
     int nl = 0;
-    if (recv) nl += launch_unpack_items(a, s, recv, n_recv, rec_bytes);
-    else nl += launch_prepare(a, s);
+    if (recv) {
+        nl += launch_unpack_items(a, s, recv, n_recv, rec_bytes);
+    } else {
+        if (pl.clear_items && pl.n_slots > 0) VF_CUDA(cudaMemsetAsync(a.items, 0, (size_t)pl.n_slots * sizeof(Item), s));
+        nl += launch_prepare(a, s);
+    }
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
     if (pl.filter) nl += launch_hs_filter(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
@@ -730,10 +713,6 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     auto launch_scans = [&]() -> int {
         int sl = pl.tc ? launch_scan_tc(fast, ss, tb, ix->tm_ls, ix->tm_x, overlap ? tc_ctas_env : 0)
                        : launch_scan(fast, ss, tb);
-        if (sl >= 0 && pl.wsplit) {
-            const int s3 = launch_scan_warp(fast, ss, tb);
-            sl = s3 < 0 ? s3 : sl + s3;
-        }
         if (sl >= 0 && pl.checked) {
             const int s2 = launch_scan(slow, ss, tb);
             sl = s2 < 0 ? s2 : sl + s2;
@@ -898,6 +877,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     Plan pl;
     st = plan_search(ix, sc, n, n_slots, p, s, &pl);
     if (st != VF_OK) return st;
+    pl.clear_items = off_dev;
     SearchArgs &a = pl.a;
     const int raw_bytes = D.dim * elem_size(D.dtype);
     if (!q_dev) VF_CUDA(sc->raw.ensure((size_t)n * raw_bytes));
@@ -993,6 +973,7 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->graph_E = (int64_t)c.graph_E;
     st->graph_iterations = (int64_t)c.graph_iters;
     st->graph_V_max = (int64_t)c.graph_V_max;
+    st->n_invalid_queries = c.n_invalid;
     st->kernel_launches = sc->last_launches;
     st->row_bytes = ix->enc8 && !c.exact_fallback ? ix->dev8.row_bytes : ix->dev.row_bytes;   // rows the kernels read
     auto span = [](unsigned long long t0_inv, unsigned long long t1) {

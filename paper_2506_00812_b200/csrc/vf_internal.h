@@ -23,9 +23,6 @@ __host__ __device__ __forceinline__ int graph_class(int32_t size) {
 constexpr int kMaxItopk = 1024;
 constexpr int kScanQG = 64;           // queries per scan segment (query group)
 constexpr int kWarpsPerGraphCta = 4;
-constexpr int kWarpScanQ = 4;         // k_scan_warp: tiles of <= 4 queries ...
-constexpr int kWarpScanRows = 4096;   // ... on lists of <= 4096 rows (the rest: tensor-core scan),
-constexpr int kWarpTileRows = 256;    // cut into tiles of 256 rows (one warp each)
 
 enum Path : uint32_t { PATH_NONE = 0, PATH_SCAN = 1, PATH_GRAPH = 2 };
 
@@ -151,10 +148,9 @@ struct Counters {
     int32_t n_items;
     int32_t exact_fallback;  // a query of this batch is outside the fast path's exact range (gate)
     int32_t filter_next;     // k_hs_filter tile cursor
-    int32_t n_wtiles, n_btiles;   // tiles for k_scan_warp / k_scan_tc (split_tiles)
     int32_t n_tile_cls[4];        // scan tiles per row-count class (kTileClasses; longest first)
-    int32_t wscan_next;
     int32_t pool_used;       // survivor pool bump allocator
+    int32_t n_invalid;       // queries rejected by the device-side offset / label-count check
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
     // device-clock activity spans of the dominant kernels (globaltimer ns; first CTA start stored
@@ -211,12 +207,15 @@ struct SearchArgs {
     int32_t q8_row_bytes;
     int32_t gate;             // 0 always run; 1 run iff !exact_fallback; 2 run iff exact_fallback
     int32_t tc_parts;         // TC scan: split few-query tiles over several warps (VF_TC_PARTS=0 off)
-    int32_t split_tiles;      // small tiles to k_scan_warp (wtiles), the rest to k_scan_tc (btiles)
-    int32_t *wtiles, *btiles;
     int32_t *tile_cls;        // [kTileClasses][max_tiles] tile indices by row-count class (tensor-core scan
                               // claims longest tiles first; nullptr = creation order)
     int32_t *pool;            // AND pre-filter survivor ids (k_hs_filter)
     int32_t pool_cap;
+    // device-side validation of caller offsets (device label arrays are not read by the host): a
+    // query whose labels fall outside [0, n_slots) or number more than max_nl gets an empty row
+    // and is counted in ctr->n_invalid (vf_search_stats.n_invalid_queries)
+    int64_t n_slots;
+    int32_t max_nl;
 };
 
 __device__ __forceinline__ bool gate_skip(const SearchArgs &a) {
@@ -232,8 +231,6 @@ int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // 
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
 int launch_hs_filter(const SearchArgs &a, cudaStream_t s);  // AND pre-filter of HS scan tiles
-bool warp_scan_supported(int dtype, int row_bytes, int k);
-int launch_scan_warp(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);
 // a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
 int scan_tc_qg(int row_bytes, int k);
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x);

@@ -355,3 +355,61 @@ def test_kernel_activity_spans(vf, tiny):
     assert st["ms_graph_active"] <= st["ms_total"] + 1e-3
     if st["n_scan_items"] > 0 and g.info()["bytes_norms"] > 0:     # tensor-core scan ran
         assert 0 < st["ms_scan_active"] <= st["ms_total"] + 1e-3
+
+
+@pytest.mark.parametrize("w_", [3, 4])
+@pytest.mark.parametrize("op,mode", [("single", "greedy"), ("and", "greedy"), ("and", "parallel")])
+@pytest.mark.parametrize("itopk", [64, 384])
+def test_search_width_3_4_bit_exact(vf, tiny, w_, op, mode, itopk):
+    """w * R > 32: more than one 32-child batch per iteration and n_init = w * R entries in two
+    batches (reading #37); the oracle's multi-parent rule is pinned by
+    tests/golden/beam_multi_parent.json. ids, distances and per-item V / E identical."""
+    from workload import gen
+    w, go, gi = tiny
+    X, Q = _variant(tiny, "u8")
+    if op == "single":
+        qoff, qlab = w.q_off, w.q_lab
+    else:
+        qoff, qlab = gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=len(Q), mode="and2")
+    g, o = _pair(vf, X, w, go, gi)
+    ids, d = g.search(Q, qoff, qlab, k=10, itopk=itopk, search_width=w_, op=op, recall_mode=mode)
+    oi, od, octr = o.search(Q, qoff, qlab, k=10, itopk=itopk, search_width=w_, op=op, recall_mode=mode,
+                            counters=True)
+    assert (ids == oi).all()
+    assert (d == od.astype(np.float32)).all()
+    _items_match(g, octr)
+
+
+def test_device_offsets_invalid_queries_get_empty_rows(vf, tiny):
+    """Device offset arrays are checked on the device (include/vf.h n_query_labels): a query with
+    more than 64 labels, or whose offsets leave [0, n_query_labels), gets an empty row and is
+    counted in n_invalid_queries; the other queries are answered as usual. Both the per-query
+    path (<= 64 queries) and the batched path."""
+    import torch
+    w, go, gi = tiny
+    g, o = _pair(vf, w.X, w, go, gi)
+    for n in (40, 120):
+        Q = w.Q[:n]
+        qoff = w.q_off[:n + 1].copy()
+        qlab = w.q_lab[:qoff[-1]].copy()
+        oi, od = o.search(Q, qoff, qlab, k=10, itopk=32)
+        # query 5 carries its label 70 times (> 64 labels)
+        extra = 69
+        qlab = np.concatenate([qlab[:qoff[6]], np.full(extra, qlab[qoff[5]], np.int32), qlab[qoff[6]:]])
+        qoff[6:] += extra
+        # query 9 ends beyond the label array (and so query 10 starts after it ends)
+        qoff[10] = 10 ** 9
+        bad = {5, 9, 10}
+        ids = torch.empty((n, 10), dtype=torch.int32, device="cuda")
+        dd = torch.empty((n, 10), dtype=torch.float32, device="cuda")
+        g.search_into(torch.from_numpy(Q).cuda(), torch.from_numpy(qoff).cuda(), torch.from_numpy(qlab).cuda(),
+                      ids, dd, k=10, itopk=32, n_query_labels=int(qlab.size))
+        torch.cuda.synchronize()
+        st = g.last_stats()
+        ids, dd = ids.cpu().numpy(), dd.cpu().numpy()
+        assert st["n_invalid_queries"] == len(bad), (n, st["n_invalid_queries"])
+        for i in range(n):
+            if i in bad:
+                assert (ids[i] == -1).all() and np.isinf(dd[i]).all(), (n, i)
+            else:
+                assert (ids[i] == oi[i]).all() and (dd[i] == od[i].astype(np.float32)).all(), (n, i)

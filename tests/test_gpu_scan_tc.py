@@ -236,11 +236,10 @@ def test_u8_scan_mixed_query_group_sizes_exact_mode(vf):
 
 
 @pytest.mark.parametrize("op", ["single", "and"])
-def test_warp_scan_opt_in_is_exact(vf, monkeypatch, op):
-    """VF_WARP_SCAN=1 sends tiles of <= 4 queries on lists of <= 4096 rows to the warp-per-tile
-    scan (k_scan_warp, 256-row tiles merged through partials); results stay bit-exact."""
+def test_small_query_groups_are_exact(vf, op):
+    """Tiles of few queries on short lists (the YFCC-shaped mix): single and AND, normal and
+    exact mode, bit-exact against the oracle."""
     from workload import gen
-    monkeypatch.setenv("VF_WARP_SCAN", "1")
     cfg, X, off, ids, go, gi = small_random_index(seed=41, N=5000, D=96, L=12, F=2.5, T=800, R=8,
                                                   dtype="u8")
     g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)

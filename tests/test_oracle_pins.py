@@ -341,3 +341,26 @@ def test_f2_infinite_threshold_equals_definition_1(tiny, tiny_oracle):
     ids, d = tiny_oracle.search(Q, qoff, qlab, k=10, scan_threshold=2**31 - 1)
     gt, gd = tiny_oracle.exact_knn(Q, qoff, qlab, k=10)
     assert (ids == gt).all() and (d == gd).all()
+
+
+def test_beam_multi_parent_trace():
+    """search_width w > 1: parents = the first w UNEXPANDED entries of Top in key order (c.2
+    step 2; readings #8/#9). Hand-derived trace in tests/golden/beam_multi_parent.json."""
+    g = golden("beam_multi_parent.json")
+    pts = np.array(g["points_1d"], np.float32)
+    rows = np.array(g["rows"], np.int32)
+    S = len(pts)
+    X = np.zeros((S, 4), np.float32)
+    X[:, 0] = pts
+    ix = oracle.Index(X, np.array([0, S], np.int64), np.arange(S, dtype=np.int32), S, rows.shape[1],
+                      np.array([0, S], np.int64), rows.reshape(-1))
+    q = np.zeros((1, 4), np.float32)
+    q[0, 0] = g["query_1d"]
+    for w, key in ((2, "expected_w2"), (1, "expected_w1")):
+        ids, d, ctr = ix.search(q, np.array([0, 1], np.int64), np.array([0], np.int32), k=g["k"],
+                                itopk=g["itopk"], search_width=w, n_init=g["n_init"],
+                                max_iterations=g["max_iterations"], forced_entry=g["forced_entry"],
+                                counters=True)
+        e = g[key]
+        assert ids[0].tolist() == e["ids"] and d[0].tolist() == e["dists"], key
+        assert int(ctr[0, 0, 2]) == e["V"] and int(ctr[0, 0, 3]) == e["E"], key
