@@ -130,10 +130,26 @@ def query_paths(recs, n):
     return p
 
 
-def split_recall(strict, tie, valid, nl, paths):
-    """Mean tie-aware (and strict) recall per query class and per item path."""
+SIZE_CLASSES = ((2_000, 20_000), (20_000, 200_000), (200_000, 1_000_000), (1_000_000, 1 << 40))
+
+
+def query_graph_label_size(recs, n, sizes):
+    """Per query: |C_l| of its (first) graph item's label, 0 if it has none."""
+    out = np.zeros(n, np.int64)
+    if len(recs):
+        g = recs[recs[:, 2] == 2]
+        out[g[:, 0]] = sizes[g[:, 1]]
+    return out
+
+
+def split_recall(strict, tie, valid, nl, paths, gsize=None):
+    """Mean tie-aware (and strict) recall per query class, per item path and, for single-label
+    graph queries, per label-size class."""
     out = {}
     groups = {"single": nl == 1, "and2": nl == 2, "scan": paths == 1, "graph": paths == 2, "mixed": paths == 3}
+    if gsize is not None:
+        for lo, hi in SIZE_CLASSES:
+            groups[f"single_graph_|C|{lo}-{hi if hi < 1 << 40 else 'inf'}"] = (nl == 1) & (paths == 2) & (gsize >= lo) & (gsize < hi)
     for name, m in groups.items():
         m = m & valid
         if m.any():
@@ -273,6 +289,7 @@ def main():
     ap.add_argument("--and-scan", default=None,
                     help="f3 selectivity-aware AND routing thresholds swept (0 = the paper's method)")
     ap.add_argument("--modes", default=None, help="AND recall policies swept (greedy,parallel; P:L547-L555)")
+    ap.add_argument("--n-init", default="0", help="entry samples n_init swept (0 = the library default R*w)")
     ap.add_argument("--scan-thr", default=None,
                     help="f2 search-time specificity thresholds T' swept (0 = the build's T; labels with "
                          "|C_l| < max(T, T') are scanned exactly)")
@@ -371,9 +388,10 @@ def main():
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)
 
     def run(cfg_):
-        itopk, w_, as_, st_, mode = cfg_
+        itopk, w_, as_, st_, mode, ni = cfg_
         ix.search_into(Q, qo, ql, ids, dd, k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode,
-                       and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+                       and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_,
+                       n_init=ni)
 
     def quick_ms(cfg_):
         ms = []
@@ -396,17 +414,18 @@ def main():
     and_scans = [int(x) for x in args.and_scan.split(",")] if op == "and" else [0]
     scan_thrs = [int(x) for x in args.scan_thr.split(",")]
     families = []
-    for mode in modes:
-        for as_ in (and_scans if mode == "greedy" else [0]):      # f3 routes greedy AND items only
-            for st_ in scan_thrs:
-                families.append((mode, as_, st_))
+    for ni in (int(x) for x in args.n_init.split(",")):
+        for mode in modes:
+            for as_ in (and_scans if mode == "greedy" else [0]):      # f3 routes greedy AND items only
+                for st_ in scan_thrs:
+                    families.append((mode, as_, st_, ni))
     t_sweep = time.time()
-    for mode, as_, st_ in families:
+    for mode, as_, st_, ni in families:
         for w_ in (int(x) for x in args.widths.split(",")):
             for itopk in ITOPK_GRID:
                 if itopk < k:
                     continue
-                cfg_ = (itopk, w_, as_, st_, mode)
+                cfg_ = (itopk, w_, as_, st_, mode, ni)
                 run(cfg_)
                 torch.cuda.synchronize()
                 rs, rt, v = recall_now()
@@ -416,17 +435,18 @@ def main():
                     t = torch.tensor([r_strict, r_tie, qms], dtype=torch.float64, device=dev)
                     dist.all_reduce(t)
                     r_strict, r_tie, qms = (float(x) / world for x in t.tolist())
-                sweep.append({"recall_mode": mode, "and_scan_threshold": as_, "scan_threshold": st_,
+                sweep.append({"recall_mode": mode, "and_scan_threshold": as_, "scan_threshold": st_, "n_init": ni,
                               "search_width": w_, "itopk": itopk, "recall_strict": r_strict,
                               "recall_tie_aware": r_tie, "ms": qms})
-                log(f"{mode:8s} f3={as_:5d} T'={st_:5d} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} "
+                log(f"{mode:8s} f3={as_:5d} T'={st_:5d} n_init={ni} w={w_} itopk={itopk:4d} recall@{k} strict={r_strict:.4f} "
                     f"tie-aware={r_tie:.4f} {n * world / qms / 1e3:.2f} MQPS")
                 if r_tie >= max(targets):
                     break
     log(f"sweep: {len(sweep)} points in {time.time() - t_sweep:.0f}s")
 
     def cfg_of(s):
-        return (s["itopk"], s["search_width"], s["and_scan_threshold"], s["scan_threshold"], s["recall_mode"])
+        return (s["itopk"], s["search_width"], s["and_scan_threshold"], s["scan_threshold"], s["recall_mode"],
+                s["n_init"])
 
     def best(tgt, paper_only):
         ok = [s for s in sweep if s["recall_tie_aware"] >= tgt and
@@ -443,7 +463,8 @@ def main():
         rs, rt, v = recall_now()
         recs = ix.last_items(stream) if world == 1 else np.zeros((0, 6), np.int32)
         paths = query_paths(recs, n)[:m_gt]
-        return split_recall(rs, rt, v, nl_q[:m_gt], paths)
+        gsize = query_graph_label_size(recs, n, np.diff(w.post_off))[:m_gt]
+        return split_recall(rs, rt, v, nl_q[:m_gt], paths, gsize)
 
     ix.set_profiling(True)
     hbm_peak, peak_kind = measured_peaks()
@@ -504,11 +525,12 @@ def main():
         qlh = torch.from_numpy(w.q_lab).pin_memory()
         oih = torch.empty((n, k), dtype=torch.int32).pin_memory()
         odh = torch.empty((n, k), dtype=torch.float32).pin_memory()
-        itopk, w_, as_, st_, mode = cfg_main
+        itopk, w_, as_, st_, mode, ni = cfg_main
 
         def run_host():
             ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode,
-                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_)
+                           and_scan_threshold=as_, stream=stream, n_query_labels=n_ql, scan_threshold=st_,
+                           n_init=ni)
         for _ in range(args.warmup):
             run_host()
         barrier()
@@ -534,7 +556,7 @@ def main():
     #    with device-resident buffers; wall clock per blocking call, p50 / p99 over many calls
     latency = None
     if main_tgt in results and world == 1 and args.lat_calls > 0:
-        itopk, w_, as_, st_, mode = cfg_of(results[main_tgt][0])
+        itopk, w_, as_, st_, mode, ni = cfg_of(results[main_tgt][0])
         latency = {}
         for bsz in (1, 10, 100):
             Qh = torch.from_numpy(w.Q[:bsz].copy()).pin_memory()
@@ -552,11 +574,12 @@ def main():
                     t0 = time.perf_counter()
                     if mode_ == "host":
                         ix.search_into(Qh, qoh, qlh, oih, odh, k=k, itopk=itopk, search_width=w_, op=op,
-                                       recall_mode=mode, and_scan_threshold=as_, stream=stream, scan_threshold=st_)
+                                       recall_mode=mode, and_scan_threshold=as_, stream=stream, scan_threshold=st_,
+                                       n_init=ni)
                     else:
                         ix.search_into(Qd, qod, qld, oid, odd, k=k, itopk=itopk, search_width=w_, op=op,
                                        recall_mode=mode, and_scan_threshold=as_, stream=stream,
-                                       n_query_labels=int(w.q_off[bsz]), scan_threshold=st_)
+                                       n_query_labels=int(w.q_off[bsz]), scan_threshold=st_, n_init=ni)
                         stream.synchronize()
                     if it_ >= 50:
                         ts.append(time.perf_counter() - t0)
@@ -569,7 +592,7 @@ def main():
         try:
             labs = [np.ascontiguousarray(w.q_lab[w.q_off[i]:w.q_off[i + 1]]) for i in range(min(n, 20000))]
             Qn = np.ascontiguousarray(w.Q)
-            with ix.serve(k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode, and_scan_threshold=as_,
+            with ix.serve(k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode, n_init=ni, and_scan_threshold=as_,
                           scan_threshold=st_, capacity=4096) as sv:
                 oi_, od_ = np.empty(k, np.int32), np.empty(k, np.float32)
                 ts = []
@@ -600,14 +623,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and main_tgt in results:
         import oracle
         cfg_main = cfg_of(results[main_tgt][0])
-        itopk, w_, as_, st_, mode = cfg_main
+        itopk, w_, as_, st_, mode, ni = cfg_main
         run(cfg_main)
         torch.cuda.synchronize()
         g_ids, g_d = ids.cpu().numpy(), dd.cpu().numpy()
         o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
         m = min(n, args.cpu_sample)
         threads = os.cpu_count() or 1
-        kw = dict(k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode, and_scan_threshold=as_,
+        kw = dict(k=k, itopk=itopk, search_width=w_, op=op, recall_mode=mode, n_init=ni, and_scan_threshold=as_,
                   scan_threshold=st_)
         passes, el = 0, 0.0
         oi = od = None
@@ -656,7 +679,7 @@ def main():
     dom = ("graph" if ga >= sa else "scan") if (ga > 0 or sa > 0) else ("graph" if g_ms >= s_ms else "scan")
     bytes_dom, ms_dom = (g_bytes, g_ms) if dom == "graph" else (s_bytes, s_ms)
     achieved = bytes_dom / (ms_dom / 1000.0) / 1e9 if ms_dom > 0 else 0.0
-    itopk, w_, as_, st_, mode = cfg_of(s_main)
+    itopk, w_, as_, st_, mode, ni = cfg_of(s_main)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -672,6 +695,7 @@ def main():
     def at_entry(r):
         s, t, st, split = r
         return {"itopk": s["itopk"], "search_width": s["search_width"], "recall_mode": s["recall_mode"],
+                "n_init": s["n_init"],
                 "and_scan_threshold": s["and_scan_threshold"], "scan_threshold": s["scan_threshold"],
                 "qps": n * world * K / (t / 1000.0), "ms_per_step": t / K,
                 "recall_strict": s["recall_strict"], "recall_tie_aware": s["recall_tie_aware"],
@@ -693,7 +717,8 @@ def main():
                                + (f" label-sharded, configs[4] 1M-query batch split over {world} ranks" if world > 1 else ""),
                    "n_points": c.n_points, "dim": c.dim, "n_labels": c.n_labels,
                    "queries_per_step": n * world, "query_mode": c.query_mode, "k": k, "T": c.threshold_T,
-                   "R": R, "itopk": itopk, "search_width": w_, "recall_mode": mode, "and_scan_threshold": as_,
+                   "R": R, "itopk": itopk, "search_width": w_, "recall_mode": mode, "n_init": ni,
+                   "and_scan_threshold": as_,
                    "scan_threshold": st_, "recall_target": main_tgt,
                    "recall": {"strict": s_main["recall_strict"], "tie_aware": s_main["recall_tie_aware"]},
                    "recall_sample": f"all {m_gt} queries (exact-mode ground truth)" if m_gt == n else f"first {m_gt} queries",

@@ -57,7 +57,7 @@ struct DevBuf {
 
 // Per-stream (and per role) scratch of a search.
 struct Scratch {
-    DevBuf raw, Qp, Q8, pool, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
+    DevBuf raw, Qp, Q8, pool, pool_bits, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
         item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
     // label sharding: item records out / in, returned results, slots of the sent items
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;
@@ -135,7 +135,7 @@ struct Plan {
     int qg = 0;
     bool tc = false;          // tensor-core scan (scan_tc.cu)
     bool checked = false;     // fast path with a query-range check (fp32 fallback kernels launched too)
-    bool filter = false;      // AND pre-filter of HS scan tiles (k_hs_filter)
+    bool filter = false;      // AND pre-filter of the scan tiles (k_and_filter)
     int graph_ctas8 = 0;      // graph grid on the u8 view (enc8)
     int64_t max_tiles = 0;
     int graph_ctas = 0;

@@ -188,7 +188,7 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 tl.item_base = sg.item_base;
                 tl.n_tiles = ntile;
                 tl.hs = d.size >= a.ix.T;
-                tl.pad = 0;
+                tl.bits_off = -1;
                 tl.n_pieces = -1;
                 a.tiles[tb + t] = tl;
                 if (a.tile_cls) {
@@ -227,26 +227,33 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
     }
 }
 
-// ---------------------------------------------------------------- AND pre-filter (HS scan tiles)
-// An AND item scanned on an HS label (f3 routing, or exact mode) keeps only the points of C_l* that
-// carry every other query label -- typically a tiny fraction. Checking that needs the point's id and
-// label list (~3 sectors), gathering its vector 192+ bytes, so the rows of such tiles are filtered
-// here first, by the whole GPU: survivors (rows passing the predicate of at least one query of the
-// segment) are compacted into the pool, and the scan gathers only those and re-verifies per query.
-// A tile that overflows its piece list or the pool stays unfiltered (every row scanned): exact.
+// ---------------------------------------------------------------- AND pre-filter (scan tiles)
+// "Before distance computation ... points that do not contain all required labels are filtered
+// out": the predicate of every AND scan item is evaluated here, for every row of its tile,
+// by the whole GPU (many independent rows per SM hide the dependent id -> labels chains), and the
+// scan no longer checks it row by row inside its epilogue.
+//   * tile whose queries ALL carry a predicate: rows passing some query are compacted into the
+//     survivor pool with their per-query pass bits; the scan gathers only those rows;
+//   * tile mixing predicate and plain queries: every row is kept, its pass bits go to pool_bits;
+//   * pool exhausted / piece list full: the tile keeps -1 and the scan verifies by itself (exact).
+// Membership: the segment's other labels (<= 64 distinct) become bit positions; a label with a
+// membership bitmap costs one bit read per row, the others one pass over the row's sorted labels;
+// query g passes iff its labels' mask is a subset of the row's.
 constexpr int kFiltThreads = 256;
-constexpr int kFiltBuf = 4096;
+constexpr int kFiltBuf = 2048;
 constexpr int kFiltUnion = 64;
 constexpr int kFiltRows = 4;          // rows per thread per round
 
-__global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
+__global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
     __shared__ int32_t buf[kFiltBuf];
+    __shared__ unsigned long long bbuf[kFiltBuf];
     __shared__ int64_t q_off[kScanQG];
     __shared__ int32_t q_nl[kScanQG];
     __shared__ int32_t p_off[kMaxPieces], p_cnt[kMaxPieces];
-    __shared__ int s_tile, s_ok, s_n, s_np, s_bad, s_flush_off, s_nu;
-    __shared__ int32_t s_u[kFiltUnion];           // union of the segment's other query labels, sorted
-    __shared__ unsigned long long s_qm[kScanQG];  // per query: its labels' bits in s_u
+    __shared__ int s_tile, s_npred, s_n, s_np, s_bad, s_flush_off, s_nu, s_bits_off;
+    __shared__ int32_t s_u[kFiltUnion];           // union of the tile's other query labels, sorted
+    __shared__ unsigned long long s_qm[kScanQG];  // per query: its labels' bits in s_u (0: no predicate)
+    __shared__ unsigned long long s_plain;        // queries without a predicate (always pass)
     __shared__ int16_t s_slot[kFiltUnion];        // membership bitmap of each s_u label
     __shared__ int s_allbits;                     // every s_u label has a bitmap: no label-list reads
     const int ntiles = a.ctr->n_tiles;
@@ -256,28 +263,29 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
         const int t = s_tile;
         if (t >= ntiles) break;
         const Tile tl = a.tiles[t];
-        if (!tl.hs) {
-            __syncthreads();
-            continue;
-        }
-        if (threadIdx.x == 0) { s_ok = 1; s_n = 0; s_np = 0; s_bad = 0; }
+        const int nq = tl.nq;
+        if (threadIdx.x == 0) { s_npred = 0; s_n = 0; s_np = 0; s_bad = 0; s_plain = 0; s_bits_off = -1; }
         __syncthreads();
-        if (threadIdx.x < tl.nq) {
+        if (threadIdx.x < nq) {
             const ScanQuery sq = a.scan_q[tl.item_base + threadIdx.x];
             q_off[threadIdx.x] = sq.p_off;
-            q_nl[threadIdx.x] = sq.nl;
-            if (!(sq.meta & META_PRED)) s_ok = 0;
+            q_nl[threadIdx.x] = (sq.meta & META_PRED) ? sq.nl : 0;
+            if (sq.meta & META_PRED) atomicAdd(&s_npred, 1);
+            else atomicOr(&s_plain, 1ull << threadIdx.x);
         }
         __syncthreads();
-        if (!s_ok) {
+        const int npred = s_npred;
+        if (npred == 0) {
             __syncthreads();
             continue;
         }
-        // the segment's other labels -> bit positions (one thread; <= 64 distinct, else per-query
-        // verification); each query then passes iff its mask is a subset of the point's bits
+        const bool compact = npred == nq;
+        const int nrows = tl.row_end - tl.row_begin;
+        // the tile's other labels -> bit positions (one thread; <= 64 distinct, else per-query
+        // verification); a mixed tile also reserves one pass-bit word per row
         if (threadIdx.x == 0) {
             int nu = 0;
-            for (int g = 0; g < tl.nq && nu <= 64; g++)
+            for (int g = 0; g < nq && nu <= 64; g++)
                 for (int i = 0; i < q_nl[g] && nu <= 64; i++) {
                     const int32_t l = a.qlab[q_off[g] + i];
                     if (l == tl.label) continue;
@@ -298,11 +306,21 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
                 all = sl >= 0;
             }
             s_allbits = all;
+            if (!compact) {
+                const int need = (nrows + 1) & ~1;        // even: 16-B aligned bulk copies of the words
+                const int off = atomicAdd(&a.ctr->pool_used, need);
+                s_bits_off = (int64_t)off + need > a.pool_cap ? -1 : off;
+            }
         }
         __syncthreads();
         const int nu = s_nu;
         const bool allbits = s_allbits != 0;
-        if (nu <= 64 && threadIdx.x < tl.nq) {
+        const int bits_off = s_bits_off;
+        if (!compact && bits_off < 0) {          // pool exhausted: the scan verifies this tile
+            __syncthreads();
+            continue;
+        }
+        if (nu <= 64 && threadIdx.x < nq) {
             unsigned long long qm = 0;
             for (int i = 0; i < q_nl[threadIdx.x]; i++) {
                 const int32_t l = a.qlab[q_off[threadIdx.x] + i];
@@ -312,65 +330,93 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
             s_qm[threadIdx.x] = qm;
         }
         __syncthreads();
+        const unsigned long long plain = s_plain;
+        const int32_t *rowid = tl.hs ? a.ix.M_hs + tl.base : a.ix.M_ls + tl.base;
         for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads * kFiltRows) {
             // kFiltRows rows per thread, their dependent chains (id -> label offsets -> labels)
             // interleaved so several memory latencies overlap
             int32_t gid[kFiltRows];
-            int64_t lo[kFiltRows], hi[kFiltRows];
+            unsigned long long pb[kFiltRows];
 #pragma unroll
             for (int u = 0; u < kFiltRows; u++) {
                 const int r = r0 + u * kFiltThreads + threadIdx.x;
-                gid[u] = r < tl.row_end ? __ldg(a.ix.M_hs + tl.base + r) : -1;
+                gid[u] = r < tl.row_end ? __ldg(rowid + r) : -1;
+                pb[u] = 0;
             }
-            if (allbits) {
-                // membership bitmaps: one bit read per (row, other label), independent loads
+            if (nu > 64) {
 #pragma unroll
                 for (int u = 0; u < kFiltRows; u++) {
                     if (gid[u] < 0) continue;
-                    unsigned long long bits = 0;
-                    for (int j = 0; j < nu; j++)
-                        if (has_label_bit(a.ix, s_slot[j], gid[u])) bits |= 1ull << j;
-                    bool pass = false;
-                    for (int g = 0; g < tl.nq && !pass; g++) pass = (bits & s_qm[g]) == s_qm[g];
-                    if (pass) buf[atomicAdd(&s_n, 1)] = gid[u];
+                    unsigned long long b = plain;
+                    for (int g = 0; g < nq; g++)
+                        if (q_nl[g] && verify_pred(a.ix, gid[u], a.qlab + q_off[g], q_nl[g], tl.label)) b |= 1ull << g;
+                    pb[u] = b;
                 }
             } else {
+                unsigned long long lb[kFiltRows];
+                if (allbits) {
+                    // membership bitmaps: one bit read per (row, other label), independent loads
 #pragma unroll
-            for (int u = 0; u < kFiltRows; u++) {
-                lo[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u]) : 0;
-                hi[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u] + 1) : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < kFiltRows; u++) {
-                if (gid[u] < 0) continue;
-                bool pass = false;
-                if (nu <= 64) {
-                    unsigned long long bits = 0;
-                    const int32_t umax = nu > 0 ? s_u[nu - 1] : -1;
-                    // the point's sorted labels, 8 independent loads per round
-                    for (int64_t e0 = lo[u]; e0 < hi[u]; e0 += 8) {
-                        int32_t l8[8];
-#pragma unroll
-                        for (int t = 0; t < 8; t++) l8[t] = e0 + t < hi[u] ? __ldg(a.ix.pt_lab + e0 + t) : INT32_MAX;
-                        bool stop = false;
-#pragma unroll
-                        for (int t = 0; t < 8; t++) {
-                            const int32_t l = l8[t];
-                            if (l > umax) { stop = true; break; }
-                            int b0 = 0, b1 = nu - 1;
-                            while (b0 < b1) { const int mid = (b0 + b1) >> 1; if (s_u[mid] < l) b0 = mid + 1; else b1 = mid; }
-                            if (s_u[b0] == l) bits |= 1ull << b0;
-                        }
-                        if (stop) break;
+                    for (int u = 0; u < kFiltRows; u++) {
+                        lb[u] = 0;
+                        if (gid[u] < 0) continue;
+                        for (int j = 0; j < nu; j++)
+                            if (has_label_bit(a.ix, s_slot[j], gid[u])) lb[u] |= 1ull << j;
                     }
-                    for (int g = 0; g < tl.nq && !pass; g++) pass = (bits & s_qm[g]) == s_qm[g];
                 } else {
-                    for (int g = 0; g < tl.nq && !pass; g++)
-                        pass = verify_pred(a.ix, gid[u], a.qlab + q_off[g], q_nl[g], tl.label);
+                    int64_t lo[kFiltRows], hi[kFiltRows];
+#pragma unroll
+                    for (int u = 0; u < kFiltRows; u++) {
+                        lo[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u]) : 0;
+                        hi[u] = gid[u] >= 0 ? __ldg(a.ix.pt_off + gid[u] + 1) : 0;
+                    }
+                    const int32_t umax = nu > 0 ? s_u[nu - 1] : -1;
+#pragma unroll
+                    for (int u = 0; u < kFiltRows; u++) {
+                        lb[u] = 0;
+                        if (gid[u] < 0) continue;
+                        // the point's sorted labels, 8 independent loads per round
+                        for (int64_t e0 = lo[u]; e0 < hi[u]; e0 += 8) {
+                            int32_t l8[8];
+#pragma unroll
+                            for (int t8 = 0; t8 < 8; t8++) l8[t8] = e0 + t8 < hi[u] ? __ldg(a.ix.pt_lab + e0 + t8) : INT32_MAX;
+                            bool stop = false;
+#pragma unroll
+                            for (int t8 = 0; t8 < 8; t8++) {
+                                const int32_t l = l8[t8];
+                                if (l > umax) { stop = true; break; }
+                                int b0 = 0, b1 = nu - 1;
+                                while (b0 < b1) { const int mid = (b0 + b1) >> 1; if (s_u[mid] < l) b0 = mid + 1; else b1 = mid; }
+                                if (s_u[b0] == l) lb[u] |= 1ull << b0;
+                            }
+                            if (stop) break;
+                        }
+                    }
                 }
-                if (pass) buf[atomicAdd(&s_n, 1)] = gid[u];
+#pragma unroll
+                for (int u = 0; u < kFiltRows; u++) {
+                    if (gid[u] < 0) continue;
+                    unsigned long long b = plain;
+                    for (int g = 0; g < nq; g++)
+                        if (q_nl[g] && (lb[u] & s_qm[g]) == s_qm[g]) b |= 1ull << g;
+                    pb[u] = b;
+                }
             }
+            if (!compact) {
+#pragma unroll
+                for (int u = 0; u < kFiltRows; u++) {
+                    const int r = r0 + u * kFiltThreads + threadIdx.x;
+                    if (r < tl.row_end) a.pool_bits[bits_off + (r - tl.row_begin)] = pb[u];
+                }
+                continue;
             }
+#pragma unroll
+            for (int u = 0; u < kFiltRows; u++)
+                if (gid[u] >= 0 && pb[u]) {
+                    const int i = atomicAdd(&s_n, 1);
+                    buf[i] = gid[u];
+                    bbuf[i] = pb[u];
+                }
             __syncthreads();
             const bool last = r0 + kFiltThreads * kFiltRows >= tl.row_end;
             if (s_n > kFiltBuf - kFiltThreads * kFiltRows || (last && s_n > 0)) {
@@ -391,16 +437,22 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
                 }
                 __syncthreads();
                 if (!s_bad)
-                    for (int i = threadIdx.x; i < s_n; i += kFiltThreads) a.pool[s_flush_off + i] = buf[i];
+                    for (int i = threadIdx.x; i < s_n; i += kFiltThreads) {
+                        a.pool[s_flush_off + i] = buf[i];
+                        a.pool_bits[s_flush_off + i] = bbuf[i];
+                    }
                 __syncthreads();
                 if (threadIdx.x == 0) s_n = 0;
                 __syncthreads();
             }
             if (s_bad) break;
         }
+        __syncthreads();
         if (threadIdx.x == 0) {
             Tile *T = a.tiles + t;
-            if (s_bad) {
+            if (!compact) {
+                T->bits_off = bits_off;
+            } else if (s_bad) {
                 T->n_pieces = -1;
             } else {
                 for (int i = 0; i < s_np; i++) { T->piece_off[i] = p_off[i]; T->piece_cnt[i] = p_cnt[i]; }
@@ -411,9 +463,9 @@ __global__ void __launch_bounds__(kFiltThreads) k_hs_filter(SearchArgs a) {
     }
 }
 
-int launch_hs_filter(const SearchArgs &a, cudaStream_t s) {
+int launch_and_filter(const SearchArgs &a, cudaStream_t s) {
     if (!a.pool || a.pool_cap <= 0) return 0;
-    k_hs_filter<<<148 * 8, kFiltThreads, 0, s>>>(a);
+    k_and_filter<<<148 * 8, kFiltThreads, 0, s>>>(a);
     return 1;
 }
 

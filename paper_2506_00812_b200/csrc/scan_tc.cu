@@ -53,7 +53,7 @@ struct TcQMeta {
 
 struct TcTInfo {
     int64_t base;
-    int32_t tile, seg, label, nq, tile_in_seg, n_tiles, hs, row_begin, row_end, n_pieces;
+    int32_t tile, seg, label, nq, tile_in_seg, n_tiles, hs, row_begin, row_end, n_pieces, bits_off;
     int32_t piece_off[kMaxPieces], piece_cnt[kMaxPieces];
 };
 
@@ -61,7 +61,7 @@ struct TcTInfo {
 
 struct TcLayout {
     int nst, qg, k, row_bytes, cw, nch, kpad, nmax, tmem_cols, ctas;
-    size_t off_bar, off_misc, off_meta, off_tinfo, off_rows, off_sid, off_snorm, off_qbuf, off_bsm, off_qmeta,
+    size_t off_bar, off_misc, off_meta, off_tinfo, off_rows, off_sid, off_snorm, off_sbits, off_qbuf, off_bsm, off_qmeta,
         off_qn, off_thr, off_lists, off_lcnt, off_scratch, off_dist, off_gid, off_mask, off_sinfo, total;
 };
 
@@ -83,7 +83,7 @@ static TcLayout tc_layout_for(int row_bytes, int k, int ctas) {
                              (size_t)kTcSelW * (32 + 2 * k) * 8 + 2 * (size_t)qg * kTcRows * 4 + 2 * kTcRows * 4 +
                              2 * (size_t)qg * 16 + 4096;
         const size_t budget = (227 * 1024) / ctas - 2048;
-        return fixed >= budget ? 0 : (int)((budget - fixed) / (stage + 2 * kTcRows * 4));
+        return fixed >= budget ? 0 : (int)((budget - fixed) / (stage + 2 * kTcRows * 4 + kTcRows * 8));
     };
     // queries per segment: as many as keep >= 3 row stages in flight per CTA (>= 2 for wide rows)
     int qg = kScanQG;
@@ -113,6 +113,7 @@ static TcLayout tc_layout_for(int row_bytes, int k, int ctas) {
     L.off_bsm = take(2 * (size_t)L.nch * L.nmax * L.cw, 1024);
     L.off_sid = take((size_t)nst * kTcRows * 4, 16);
     L.off_snorm = take((size_t)nst * kTcRows * 4, 16);
+    L.off_sbits = take((size_t)nst * kTcRows * 8, 16);
     L.off_qbuf = take(2 * (size_t)qg * row_bytes, 16);
     L.off_qmeta = take(2 * (size_t)qg * sizeof(TcQMeta), 16);
     L.off_qn = take(2 * (size_t)qg * 4, 16);
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
     uint8_t *bsm = smem + SL.off_bsm;
     int32_t *sid = reinterpret_cast<int32_t *>(smem + SL.off_sid);
     uint32_t *snorm = reinterpret_cast<uint32_t *>(smem + SL.off_snorm);
+    unsigned long long *sbits = reinterpret_cast<unsigned long long *>(smem + SL.off_sbits);
     uint8_t *qbuf = smem + SL.off_qbuf;
     TcQMeta *qmeta = reinterpret_cast<TcQMeta *>(smem + SL.off_qmeta);
     uint32_t *qn = reinterpret_cast<uint32_t *>(smem + SL.off_qn);
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                 ti.tile = t; ti.seg = tl.seg; ti.label = tl.label; ti.nq = nq;
                 ti.tile_in_seg = tl.tile_in_seg; ti.n_tiles = tl.n_tiles; ti.hs = tl.hs != 0;
                 ti.row_begin = tl.row_begin; ti.row_end = tl.row_end; ti.n_pieces = tl.n_pieces;
+                ti.bits_off = tl.bits_off;
                 for (int i = 0; i < kMaxPieces; i++) { ti.piece_off[i] = tl.piece_off[i]; ti.piece_cnt[i] = tl.piece_cnt[i]; }
                 tinfo[tp] = ti;
             }
@@ -461,7 +464,8 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                             (uint32_t)row_bytes, qfull + tp);
             tc++;
             // rows of the tile: its range of the label, or only the AND pre-filter's survivors
-            const bool filt = hs && tl.n_pieces >= 0;
+            const bool filt = tl.n_pieces >= 0;
+            const bool rbits = !filt && tl.bits_off >= 0;     // per-row pass bits of a mixed tile
             int total = tl.row_end - tl.row_begin;
             if (filt) {
                 total = 0;
@@ -476,20 +480,23 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                 uint8_t *dst = rows + (size_t)slot * stage_bytes;
                 int32_t *dsid = sid + (size_t)slot * kTcRows;
                 uint32_t *dnorm = snorm + (size_t)slot * kTcRows;
+                unsigned long long *dbits = sbits + (size_t)slot * kTcRows;
                 const int flags = (si == 0 ? TS_FIRST : 0) | (si == nstage - 1 ? TS_LAST : 0);
                 TP_MARK(3)
-                if (!hs) {
+                if (!hs && !filt) {
                     if (lane == 0) {
                         mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
                         TP_MARK(1)
                         meta[slot] = make_int4(t, r0, nr, flags);
                         const uint32_t idb = (uint32_t)((nr * 4 + 15) & ~15);
-                        mbar_arrive_expect_tx(full + slot, (uint32_t)stage_bytes + 2 * idb);
+                        const uint32_t bb = rbits ? (uint32_t)((nr * 8 + 15) & ~15) : 0u;
+                        mbar_arrive_expect_tx(full + slot, (uint32_t)stage_bytes + 2 * idb + bb);
                         const int64_t row0 = tl.base + r0;
                         for (int c = 0; c < nch; c++)
                             tma_load_2d(dst + (size_t)c * kTcRows * cw, &tm_ls, c * cw, (int)row0, full + slot);
                         tma_load_1d(dsid, ix.M_ls + row0, idb, full + slot);
                         tma_load_1d(dnorm, ix.xn_ls + row0, idb, full + slot);
+                        if (rbits) tma_load_1d(dbits, a.pool_bits + tl.bits_off + v0, bb, full + slot);
                     }
                     __syncwarp();
                 } else {
@@ -504,6 +511,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                     __syncwarp();
                     for (int q4 = lane; q4 < ng; q4 += 32) {
                         int32_t g4[4];
+                        unsigned long long b4[4] = {0, 0, 0, 0};
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const int r = min(q4 * 4 + j, nr - 1);
@@ -511,8 +519,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                                 int v = v0 + r, p = 0;
                                 while (v >= tl.piece_cnt[p]) { v -= tl.piece_cnt[p]; p++; }
                                 g4[j] = __ldg(a.pool + tl.piece_off[p] + v);
+                                b4[j] = __ldg(a.pool_bits + tl.piece_off[p] + v);
                             } else {
                                 g4[j] = __ldg(ix.M_hs + tl.base + r0 + r);
+                                if (rbits) b4[j] = __ldg(a.pool_bits + tl.bits_off + v0 + r);
                             }
                         }
                         for (int c = 0; c < nch; c++)
@@ -523,6 +533,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                             if (q4 * 4 + j < nr) {
                                 dsid[q4 * 4 + j] = g4[j];
                                 dnorm[q4 * 4 + j] = __ldg(ix.xn + g4[j]);
+                                dbits[q4 * 4 + j] = b4[j];
                             }
                         }
                     }
@@ -660,6 +671,9 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
             const bool valid = row < nr;
             const int32_t gid = sid[(size_t)slot * kTcRows + row];
             const int32_t xn = (int32_t)snorm[(size_t)slot * kTcRows + row];
+            // AND predicate: pass bits from the pre-filter (k_and_filter) when it ran on this tile
+            const bool use_bits = ti.n_pieces >= 0 || ti.bits_off >= 0;
+            const unsigned long long pbits = use_bits && valid ? sbits[(size_t)slot * kTcRows + row] : 0ull;
             Gd[row] = valid ? gid : -1;
             for (int c0 = 0; c0 < nq; c0 += 8) {
                 uint32_t v[8];
@@ -676,8 +690,9 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                         bool pass = valid && key < thrp[g];
                         if (pass) {
                             const TcQMeta &qq = qm[g];
-                            if ((qq.meta & META_PRED) && !verify_pred_ol(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label))
-                                pass = false;
+                            if (qq.meta & META_PRED)
+                                pass = use_bits ? ((pbits >> g) & 1ull) != 0
+                                                : verify_pred_ol(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label);
                         }
                         if (pass) D[(size_t)g * kTcRows + row] = bits;
                         const unsigned b = __ballot_sync(FULL, pass);

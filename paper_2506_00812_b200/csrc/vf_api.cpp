@@ -269,12 +269,13 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     VF_B(ix->pt_lab.ensure(plab.size() * 4));
     VF_B(cudaMemcpy(ix->pt_lab.p, plab.data(), plab.size() * 4, cudaMemcpyHostToDevice));
     // -- membership bitmaps of the largest labels (predicate fast path): labels with
-    // |C_l| >= N / VF_BITMAP_DENSITY (default 256: a bitmap is at most 8x its posting list), at most
-    // kMaxBitmaps of them, largest first. 0 disables them.
+    // |C_l| >= N / VF_BITMAP_DENSITY (default 1024: a bitmap is at most 32x its posting list), at most
+    // kMaxBitmaps of them, largest first. 0 disables them. HBM is plentiful (YFCC-shaped: ~860
+    // bitmaps, 1.1 GB); each turns a predicate check into one bit read (k_and_filter, verify_pred).
     int64_t n_bitmaps = 0, lbit_words = (N + 31) / 32;
     {
         const char *e = getenv("VF_BITMAP_DENSITY");
-        const int64_t dens = e ? atoll(e) : 256;
+        const int64_t dens = e ? atoll(e) : 1024;
         std::vector<int32_t> cand;
         if (dens > 0 && N > 0)
             for (int l = 0; l < L; l++)
@@ -553,10 +554,11 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.q8 = nullptr;
     a.q8_row_bytes = ix->enc8 ? ix->dev8.row_bytes : 0;
     a.gate = 0;
-    // AND items scanned on HS labels (f3 routing or exact mode) are pre-filtered for the
-    // tensor-core scan (k_hs_filter); the survivor pool is sized per search, overflow is exact
-    pl.filter = pl.tc && p->op == VF_AND && (p->exact || p->and_scan_threshold > 0 || p->scan_threshold > D.T);
+    // AND items are pre-filtered for the tensor-core scan (k_and_filter); the survivor
+    // pool is sized per search, overflow is exact (the scan then verifies by itself)
+    pl.filter = pl.tc && p->op == VF_AND;
     a.pool = nullptr;
+    a.pool_bits = nullptr;
     a.pool_cap = 0;
     a.n_slots = n_slots;
     a.max_nl = ix->world > 1 ? kRecLabels : kMaxQueryLabels;
@@ -581,7 +583,9 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
         int64_t cap = 16ll << 20;                       // 64 MB of survivor ids
         if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
         VF_CUDA(sc->pool.ensure((size_t)cap * 4));
+        VF_CUDA(sc->pool_bits.ensure((size_t)cap * 8));
         a.pool = sc->pool.as<int32_t>();
+        a.pool_bits = sc->pool_bits.as<unsigned long long>();
         a.pool_cap = (int32_t)cap;
     }
     if (ix->enc8) {
@@ -668,7 +672,7 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
         nl += launch_prepare(a, s);
     }
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
-    if (pl.filter) nl += launch_hs_filter(a, s);
+    if (pl.filter) nl += launch_and_filter(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     // scan and graph items are independent (Alg. 2 L418 / L428): the graph kernels run on a side

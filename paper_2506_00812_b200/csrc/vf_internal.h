@@ -8,7 +8,7 @@ namespace vf {
 
 constexpr int kMaxQueryLabels = 64;   // labels per query accepted by vf_search
 constexpr int kMaxK = 256;
-constexpr int kMaxBitmaps = 256;
+constexpr int kMaxBitmaps = 1024;
 // Graph items are claimed largest-label class first: an item's beam-search cost grows with log |C_l|
 // (oracle counters on SIFT-like: corr(log |C_l|, V) = 0.77), so long items start early and the
 // kernel's tail shrinks (longest-processing-time-first at class granularity).
@@ -102,7 +102,7 @@ struct Segment {
     int32_t pad[3];
 };
 
-constexpr int kMaxPieces = 6;        // survivor pieces of a pre-filtered HS tile (k_hs_filter)
+constexpr int kMaxPieces = 6;        // survivor pieces of a pre-filtered tile (k_and_filter)
 
 // A row tile of a segment: everything the scan producer needs in one record, so claiming a tile
 // costs one dependent load (written by k_segments; survivor pieces by k_hs_filter).
@@ -117,10 +117,13 @@ struct Tile {
     int32_t item_base;   // first entry of the segment in scan_slots / scan_q
     int32_t n_tiles;
     int32_t hs;          // 1: HS label scanned in exact mode (rows gathered through M_HS)
-    int32_t pad;
-    // AND pre-filter (HS tiles whose queries all carry a predicate): -1 = not filtered (every row
-    // of the range is scanned), else the rows passing some query's predicate, as pieces of the
-    // survivor pool -- the tensor-core scan gathers only those
+    // AND pre-filter (k_and_filter, "before distance"). A tile whose queries all carry a
+    // predicate is compacted: n_pieces >= 0 pieces of the survivor pool hold the rows passing some
+    // query's predicate (pool: global ids, pool_bits: per-query pass bits) and the tensor-core scan
+    // gathers only those. A tile mixing predicate and plain queries keeps every row and gets one
+    // pass-bit word per row at pool_bits[bits_off + row - row_begin]. -1 / -1: no pre-filter (the
+    // scan verifies the predicate itself).
+    int32_t bits_off;
     int32_t n_pieces;
     int32_t piece_off[kMaxPieces];
     int32_t piece_cnt[kMaxPieces];
@@ -209,7 +212,8 @@ struct SearchArgs {
     int32_t tc_parts;         // TC scan: split few-query tiles over several warps (VF_TC_PARTS=0 off)
     int32_t *tile_cls;        // [kTileClasses][max_tiles] tile indices by row-count class (tensor-core scan
                               // claims longest tiles first; nullptr = creation order)
-    int32_t *pool;            // AND pre-filter survivor ids (k_hs_filter)
+    int32_t *pool;            // AND pre-filter survivor ids (k_and_filter)
+    unsigned long long *pool_bits;  // ... and their per-query pass bits (bit g: query g of the tile)
     int32_t pool_cap;
     // device-side validation of caller offsets (device label arrays are not read by the host): a
     // query whose labels fall outside [0, n_slots) or number more than max_nl gets an empty row
@@ -230,7 +234,7 @@ int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg);
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // a2
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
-int launch_hs_filter(const SearchArgs &a, cudaStream_t s);  // AND pre-filter of HS scan tiles
+int launch_and_filter(const SearchArgs &a, cudaStream_t s);  // AND pre-filter of HS scan tiles
 // a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
 int scan_tc_qg(int row_bytes, int k);
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x);

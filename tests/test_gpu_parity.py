@@ -323,11 +323,11 @@ def test_scan_threshold_f2_bit_exact(vf, tiny, thr):
     assert (ids == oi).all() and (d == od.astype(np.float32)).all()
 
 
-@pytest.mark.parametrize("density", ["0", "4", "256"])
+@pytest.mark.parametrize("density", ["0", "4", "256", "1024"])
 def test_label_bitmaps_do_not_change_results(vf, tiny, density, monkeypatch):
     """Membership bitmaps of the largest labels (predicate fast path, read at build time): none
     (0), only labels with >= N/4 points (4: a mix of bitmap and label-list checks inside one query),
-    all labels with >= N/256 points (256, the default). AND / OR results and per-item counters
+    all labels with >= N/256 or N/1024 points (1024, the default). AND / OR results and per-item counters
     stay bit-identical to the oracle, which has no bitmaps."""
     from workload import gen
     monkeypatch.setenv("VF_BITMAP_DENSITY", density)

@@ -255,3 +255,57 @@ def test_small_query_groups_are_exact(vf, op):
         e, ed = (o.exact_knn(Q, qoff, qlab, k=10, op=op) if exact else
                  o.search(Q, qoff, qlab, k=10, itopk=32, op=op))
         assert (a == e).all() and (ad == ed.astype(np.float32)).all(), exact
+
+
+@pytest.mark.parametrize("cap", [None, "1", "700"])
+@pytest.mark.parametrize("exact", [False, True])
+def test_and_prefilter_mixed_and_compacted_tiles(vf, monkeypatch, cap, exact):
+    """k_and_filter (P:L559 'before distance'): tiles whose queries all carry an AND predicate are
+    compacted to the rows passing some query (pass bits per survivor); tiles mixing single-label
+    and AND queries keep every row with per-row pass bits; a full pool leaves the tile to the
+    scan's own verification. All three bit-exact vs the oracle, greedy and parallel policies."""
+    from workload import gen
+    if cap is None:
+        monkeypatch.delenv("VF_POOL_CAP", raising=False)
+    else:
+        monkeypatch.setenv("VF_POOL_CAP", cap)
+    cfg, X, off, ids, go, gi = small_random_index(seed=27, N=8000, D=64, L=10, F=3.0, T=700, R=8,
+                                                  dtype="u8")
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=400)
+    qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=400, mode="mix_and")
+    for mode in ("greedy", "parallel"):
+        a, ad = g.search(Q, qoff, qlab, k=10, itopk=32, op="and", recall_mode=mode, exact=exact)
+        if exact:
+            e, ed = o.exact_knn(Q, qoff, qlab, k=10, op="and")
+        else:
+            e, ed = o.search(Q, qoff, qlab, k=10, itopk=32, op="and", recall_mode=mode)
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), (mode, cap, exact)
+
+
+def test_and_prefilter_wide_label_union(vf):
+    """AND3 queries sharing their smallest label: one segment's other labels exceed the 64 bit
+    positions of the pre-filter's label union, which then verifies per query; results equal
+    Definition 1 (every label LS, so greedy AND is exact)."""
+    rng = np.random.default_rng(77)
+    N, dim = 6000, 64
+    X = rng.integers(0, 256, size=(N, dim), dtype=np.uint8)
+    lists = [np.sort(rng.choice(N, size=400, replace=False))]
+    lists += [np.sort(rng.choice(N, size=2500, replace=False)) for _ in range(120)]
+    off = np.zeros(len(lists) + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in lists])
+    ids = np.concatenate(lists).astype(np.int32)
+    T = 1 << 30
+    g = vf.Index(X, off, ids, T, 8)
+    o = oracle.Index(X, off, ids, T, 8)
+    n = 130                                          # > 64: the batched path (k_and_filter)
+    Q = rng.integers(0, 256, size=(n, dim), dtype=np.uint8)
+    labs = [np.array([0] + list(rng.choice(np.arange(1, 121), size=2, replace=False)), np.int32) for _ in range(n)]
+    qoff = np.zeros(n + 1, np.int64)
+    qoff[1:] = np.cumsum([len(x) for x in labs])
+    qlab = np.concatenate(labs)
+    for k in (1, 10):
+        a, ad = g.search(Q, qoff, qlab, k=k, itopk=16, op="and")
+        e, ed = o.exact_knn(Q, qoff, qlab, k=k, op="and")
+        assert (a == e).all() and (ad == ed.astype(np.float32)).all(), k
