@@ -424,7 +424,9 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                     if (s_np == kMaxPieces) {
                         s_bad = 1;
                     } else {
-                        const int off = atomicAdd(&a.ctr->pool_used, s_n);
+                        // even sizes keep every allocation 16-B aligned in pool_bits (the
+                        // per-row words of mixed tiles are read by bulk copies)
+                        const int off = atomicAdd(&a.ctr->pool_used, (s_n + 1) & ~1);
                         if ((int64_t)off + s_n > a.pool_cap) {
                             s_bad = 1;
                         } else {

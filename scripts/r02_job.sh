@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 export VF_GRAPH_CACHE=/tmp/vf_graph_cache
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${tag}_build.log 2>&1 || { echo "build failed"; tail -30 gpurun_out/${tag}_build.log; exit 1; }
 if [ "$pt" != "SKIP" ]; then
-  timeout 1500 python -m pytest tests -m gpu -x -q $pt > gpurun_out/${tag}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.log
+  timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scan_tc.py tests/test_gpu_small.py tests/test_gpu_fullsize.py -m gpu -x -q $pt > gpurun_out/${tag}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.log
   tail -n 5 gpurun_out/${tag}_pytest.log
 fi
 i=0
