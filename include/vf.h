@@ -131,6 +131,51 @@ typedef struct {
     int64_t n_query_labels;
 } vf_search_params;
 
+/*
+ * GPU construction of the per-label graphs ("we use CAGRA ...
+ * NN-descent + rank-based reordering", Alg. 1 L393 BuildGraph(C_l)) -- produces exactly the
+ * graph_row_offsets / graph_local_ids that vf_build_desc takes. For every label with
+ * |C_l| >= threshold_T:
+ *   kNN    the knn_k nearest other members of every point by (squared L2, row), computed on the
+ *          tensor cores (a u8 self-join); exact for labels of <= exact_max points, else IVF probing
+ *          (k-means cells of ~ivf_cell points, each joined against its ivf_probes nearest cells);
+ *   prune  CAGRA rank-based pruning to degree_R (fewest detours x -> z -> y with both ranks below
+ *          y's rank in x's list; ties by rank);
+ *   rows   the first R/2 pruned edges, then up to R/2 reverse edges (by position, then source),
+ *          then the remaining pruned edges; duplicates skipped; -1 padded.
+ * Vectors: u8, or fp32 holding integers in [0, 255] (else VF_ERR_INVALID_ARG). All host arrays;
+ * graph_row_offsets: [n_labels + 1] (written), graph_local_ids: caller-owned, capacity
+ * degree_R * sum of |C_l| over the labels with |C_l| >= threshold_T. Deterministic: the same
+ * inputs give the same graphs. Runs on `device`; uses up to ~ (rows of those labels) x
+ * (row bytes + 300) bytes of device memory, all freed on return.
+ */
+typedef struct {
+    int64_t n_points;
+    int32_t dim;
+    vf_dtype dtype;
+    const void *vectors;               /* host, row-major n_points * dim */
+    int32_t n_labels;
+    const int64_t *posting_offsets;    /* [n_labels + 1] */
+    const int32_t *posting_ids;        /* ascending per label */
+    int32_t threshold_T;               /* graphs for |C_l| >= T */
+    int32_t degree_R;                  /* even, 2..32 */
+    int32_t knn_k;                     /* kNN list length before pruning: 0 = min(32, 2R); <= 32, >= R */
+    int64_t exact_max;                 /* exact kNN up to this label size: 0 = 200000, < 0 = always */
+    int32_t ivf_cell;                  /* points per IVF cell: 0 = 2048 */
+    int32_t ivf_probes;                /* cells probed per cell (itself included): 0 = 16, <= 16 */
+    int32_t kmeans_iters;              /* Lloyd iterations: 0 = 4 */
+    int32_t device;
+} vf_graph_desc;
+
+typedef struct {
+    double ms_total, ms_upload, ms_knn_exact, ms_kmeans, ms_knn_ivf, ms_prune, ms_rows, ms_download;
+    int64_t n_graph_labels, n_exact_labels, n_ivf_labels, rows;
+    int64_t join_pairs;                /* (query, candidate) pairs the kNN joins evaluated */
+} vf_graph_report;
+
+vf_status vf_build_graphs(const vf_graph_desc *desc, int64_t *graph_row_offsets, int32_t *graph_local_ids,
+                          vf_graph_report *report /* may be NULL */);
+
 /* Build the index on the device (copies everything; see vf_build_desc). */
 vf_status vf_build_index(const vf_build_desc *desc, vf_index **out);
 

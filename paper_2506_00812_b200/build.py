@@ -11,9 +11,9 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libvecflow.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["route.cu", "scan.cu", "scan_tc.cu", "graph.cu", "merge.cu", "small.cu"]
+CU = ["route.cu", "scan.cu", "scan_tc.cu", "graph_build.cu", "graph.cu", "merge.cu", "small.cu"]
 CPP = ["vf_api.cpp", "shard.cpp", "serve.cpp"]
-HEADERS = ["vf_internal.h", "common.cuh", "host_internal.h", "graph_item.cuh", "small.h"]
+HEADERS = ["vf_internal.h", "common.cuh", "tc_common.cuh", "host_internal.h", "graph_item.cuh", "small.h"]
 
 
 def _sources():

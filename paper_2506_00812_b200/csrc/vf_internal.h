@@ -234,6 +234,7 @@ int launch_bucket(const SearchArgs &a, cudaStream_t s, int64_t n_slots, int qg);
 int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // a2
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
+bool encode_row_map(void *map, const void *base, int row_bytes, int64_t n_rows, int cw, int box_rows);
 int launch_and_filter(const SearchArgs &a, cudaStream_t s);  // AND pre-filter of HS scan tiles
 // a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
 int scan_tc_qg(int row_bytes, int k);
