@@ -86,7 +86,7 @@ def cpu_model():
 
 
 # ----------------------------------------------------------------------------- workload
-def make_inputs(config: str, device, query_stream: int = 0, n_queries=None):
+def make_inputs(config: str, device, query_stream: int = 0, n_queries=None, builder: str = "cuda"):
     from workload import gen, graphs
     t0 = time.time()
     w = gen.make_workload(config, n_queries=n_queries, query_stream=query_stream)
@@ -97,16 +97,25 @@ def make_inputs(config: str, device, query_stream: int = 0, n_queries=None):
     # VF_GRAPH_CACHE=<dir>: reuse the fixture graphs between bench processes of ONE job (profiling
     # runs several); nothing relies on it surviving the job
     cache = os.environ.get("VF_GRAPH_CACHE")
-    cpath = os.path.join(cache, f"graphs_{config}.npz") if cache else None
+    cpath = os.path.join(cache, f"graphs_{config}_{builder}.npz") if cache else None
+    rep = None
     if cpath and os.path.exists(cpath):
         z = np.load(cpath)
         go, gi = z["go"], z["gi"]
+    elif builder == "cuda" and device is not None:
+        # f4: the per-label graphs built on the GPU by the library (vf_build_graphs: tensor-core kNN
+        # + CAGRA-style pruning + reverse edges)
+        import paper_2506_00812_b200 as vf
+        go, gi, rep = vf.build_graphs(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R,
+                                      device=device.index or 0)
     else:
         go, gi = graphs.build_graphs(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, device=device)
-        if cpath:
-            os.makedirs(cache, exist_ok=True)
-            np.savez(cpath, go=go, gi=gi)
-    log(f"fixture graphs: {int((np.diff(go) > 0).sum())} HS labels, {int(go[-1])} rows ({time.time() - t0:.1f}s)")
+    if cpath and not os.path.exists(cpath):
+        os.makedirs(cache, exist_ok=True)
+        np.savez(cpath, go=go, gi=gi)
+    log(f"{builder} graphs: {int((np.diff(go) > 0).sum())} HS labels, {int(go[-1])} rows ({time.time() - t0:.1f}s)"
+        + (f" report {rep}" if rep else ""))
+    make_inputs.graph_report = rep
     return w, go, gi
 
 
@@ -228,7 +237,7 @@ def run_reference(args, config):
             dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
     except Exception:
         dev = None
-    w, go, gi = make_inputs(config, dev)
+    w, go, gi = make_inputs(config, dev, builder=args.graphs)
     c = w.cfg
     o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
     n = len(w.Q) if args.ref_sample < 0 and config != "yfcc" else min(len(w.Q), 5000 if args.ref_sample < 0 else args.ref_sample)
@@ -303,6 +312,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-paper-timing", action="store_true", help="skip timing the paper-routing operating points")
     ap.add_argument("--dump-stats", default=None)
+    ap.add_argument("--graphs", default="cuda", choices=["cuda", "fixture"],
+                    help="per-label graphs: the library's GPU builder (f4, vf_build_graphs) or the torch/numpy "
+                         "fixture builder (workload/graphs.py)")
     args = ap.parse_args()
 
     world_env = os.environ.get("WORLD_SIZE")
@@ -339,7 +351,7 @@ def main():
 
     # N > 1: the 1M-query batch of configs[4], split evenly (rank r draws its own slice's stream)
     nq_rank = SHARDED_QUERIES // world if world > 1 else None
-    w, go, gi = make_inputs(args.config, dev, query_stream=rank, n_queries=nq_rank)
+    w, go, gi = make_inputs(args.config, dev, query_stream=rank, n_queries=nq_rank, builder=args.graphs)
     c = w.cfg
     t0 = time.time()
     if world > 1:
@@ -650,7 +662,10 @@ def main():
                "sample": f"first {m} of the {n} queries x {passes} passes at the 0.90 operating point "
                          f"(itopk={itopk}, w={w_}, {mode}, f3={as_}), {threads} threads, {el:.1f}s",
                "one_thread": {"value": m1 / el1, "unit": "queries/s", "sample": f"first {m1} queries, 1 thread"},
-               "parity_vs_gpu": {"queries": m, "rows_ids_identical": same_ids, "rows_dists_identical": same_d}}
+               # consistency of the two arms on this run's inputs (the parity claims are tests/'s, on
+               # fixture graphs: an oracle input never comes from the CUDA path there)
+               "consistency_vs_gpu": {"queries": m, "rows_ids_identical": same_ids, "rows_dists_identical": same_d,
+                                      "graphs": args.graphs}}
         log(f"cpu baseline / parity: {cpu}")
 
     if rank != 0:
@@ -754,6 +769,7 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clocks,
         "index_bytes": info["bytes_total"],
+        "graphs": {"builder": args.graphs, "report": getattr(make_inputs, "graph_report", None)},
         "build": build_ids(),
     }
     if args.dump_stats:

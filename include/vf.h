@@ -165,12 +165,15 @@ typedef struct {
     int32_t ivf_probes;                /* cells probed per cell (itself included): 0 = 16, <= 16 */
     int32_t kmeans_iters;              /* Lloyd iterations: 0 = 4 */
     int32_t device;
+    int32_t *knn_lists;                /* optional (NULL): receives the kNN lists before pruning,
+                                          [rows][report.knn_k] local ids, rows in graph order */
 } vf_graph_desc;
 
 typedef struct {
     double ms_total, ms_upload, ms_knn_exact, ms_kmeans, ms_knn_ivf, ms_prune, ms_rows, ms_download;
     int64_t n_graph_labels, n_exact_labels, n_ivf_labels, rows;
     int64_t join_pairs;                /* (query, candidate) pairs the kNN joins evaluated */
+    int32_t knn_k;                     /* kNN list length used (knn_k rounded up to 16 or 32) */
 } vf_graph_report;
 
 vf_status vf_build_graphs(const vf_graph_desc *desc, int64_t *graph_row_offsets, int32_t *graph_local_ids,
@@ -276,6 +279,8 @@ typedef struct {
      * search and fail it with VF_ERR_INVALID_ARG instead): labels outside [0, n_query_labels) or
      * more labels than allowed (64; 16 on a label-sharded index). Their rows come out empty. */
     int64_t n_invalid_queries;
+    /* AND pre-filter (k_and_filter): survivor / pass-bit words used in its pool (diagnostics) */
+    int64_t prefilter_words;
 } vf_search_stats;
 
 vf_status vf_set_profiling(vf_index *index, int32_t enable);

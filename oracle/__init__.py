@@ -61,6 +61,10 @@ def lib():
                                 i32, u32, i32, p, p, p, i32, C.c_int, i32, i32]
         L.or_exact_knn.restype = C.c_int
         L.or_exact_knn.argtypes = [p, i64, p, p, p, C.c_int, i32, p, p, C.c_int]
+        L.or_label_knn.restype = C.c_int
+        L.or_label_knn.argtypes = [p, i32, C.c_int, p]
+        L.or_cagra_rows.restype = C.c_int
+        L.or_cagra_rows.argtypes = [i64, C.c_int, p, C.c_int, p, p]
         L.or_index_pt_off.restype = i64
         L.or_index_pt_off.argtypes = [p, i64]
         L.or_index_pt_lab.restype = p
@@ -151,6 +155,14 @@ class Index:
             raise ValueError("oracle: invalid query (SINGLE with more than one label)")
         return (ids, d, ctr) if counters else (ids, d)
 
+    def label_knn(self, label, K):
+        """f4: the K nearest other members of every point of `label` by (squared L2, local id),
+        exact (plain sort); [S][K] local ids, -1 padded."""
+        S = int(self.post_off[label + 1] - self.post_off[label])
+        out = np.empty((S, K), np.int32)
+        lib().or_label_knn(self._h, int(label), int(K), _ptr(out))
+        return out
+
     def exact_knn(self, Q, q_off, q_lab, k=10, op="single", nthreads=None):
         """Definition 1 ground truth by brute force over all N points."""
         Q = np.ascontiguousarray(Q, dtype=self.X.dtype)
@@ -196,6 +208,17 @@ def query_hash(q: np.ndarray) -> int:
 
 def entry_hash(seed: int, qh: int, label: int, i: int, S: int) -> int:
     return int(lib().or_entry_hash(seed & 0xFFFFFFFF, qh & 0xFFFFFFFF, label, i, S))
+
+
+def cagra_rows(knn, R):
+    """f4: CAGRA rank pruning + reverse edges + row assembly (oracle.c or_cagra_rows) on kNN lists
+    [S][K] of local ids; returns (pruned [S][R], rows [S][R])."""
+    knn = np.ascontiguousarray(knn, np.int32)
+    S, K = knn.shape
+    pruned = np.empty((S, R), np.int32)
+    rows = np.empty((S, R), np.int32)
+    lib().or_cagra_rows(S, K, _ptr(knn), int(R), _ptr(pruned), _ptr(rows))
+    return pruned, rows
 
 
 def merge(ids_lists, dists_lists, k):

@@ -620,3 +620,116 @@ double or_mem_hs_bytes(double N, double D, double F_HS, double Rp, double b) { r
 double or_mem_ls_bytes(double N, double D, double F_LS, double b) { return N * D * F_LS * b; }
 double or_mem_single_bytes(double N, double D, double R, double b) { return N * (D + R) * b; }
 double or_mem_map_bytes(double N, double F, double b) { return N * F * b; }
+
+/* ------------------------------------------------------------------ graph construction (f4)
+ * The builder's two deterministic steps, written out as plain loops (PAPER.md
+ * L348 "CAGRA ... rank-based reordering"; readings #45-#47).
+ *
+ * or_label_knn: for every member j of label l (local id j), the K nearest OTHER members by
+ *   (squared L2, local id) -- exact, by sorting all S-1 candidates. Output [S][K], -1 padded.
+ *
+ * or_cagra_rows: from kNN lists knn[S][K] (local ids, ascending by (d, id)):
+ *   detours(x, j) = #{ i < j : knn[x][j] occurs in knn[knn[x][i]] at a position < j }
+ *   pruned[x] = the R entries of knn[x] with the fewest detours, ties by position j (-1 last)
+ *   rev[y]    = the R/2 sources x with y in pruned[x], ordered by (position of y in pruned[x], x)
+ *   row[x]    = pruned[x][0..R/2) ++ rev[x] ++ pruned[x][R/2..R), duplicates and -1 skipped,
+ *               first R kept, -1 padded. */
+typedef struct { double d; int32_t id; } knn_c;
+static int cmp_knn_c(const void *a, const void *b)
+{
+    const knn_c *x = (const knn_c *)a, *y = (const knn_c *)b;
+    if (x->d < y->d) return -1;
+    if (x->d > y->d) return 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+int or_label_knn(const or_index *ix, int32_t l, int K, int32_t *out)
+{
+    const int64_t S = label_size(ix, l);
+    const int32_t *M = ix->post_ids + ix->post_off[l];
+    knn_c *c = (knn_c *)malloc(sizeof(knn_c) * (size_t)(S > 0 ? S : 1));
+    const size_t esz = ix->dtype == OR_U8 ? 1 : 4;
+    for (int64_t j = 0; j < S; j++) {
+        const void *q = (const uint8_t *)ix->X + (size_t)M[j] * ix->dim * esz;
+        int64_t n = 0;
+        for (int64_t t = 0; t < S; t++) {
+            if (t == j) continue;
+            c[n].d = dist_l2sq(ix->dtype, ix->dim, ix->X, M[t], q);
+            c[n].id = (int32_t)t;
+            n++;
+        }
+        qsort(c, (size_t)n, sizeof(knn_c), cmp_knn_c);
+        for (int t = 0; t < K; t++) out[j * K + t] = t < n ? c[t].id : -1;
+    }
+    free(c);
+    return 0;
+}
+
+typedef struct { int64_t a, b; int32_t v; } key3;
+static int cmp_key3(const void *p, const void *q)
+{
+    const key3 *x = (const key3 *)p, *y = (const key3 *)q;
+    if (x->a != y->a) return x->a < y->a ? -1 : 1;
+    if (x->b != y->b) return x->b < y->b ? -1 : 1;
+    return 0;
+}
+
+static int push_unique(int32_t *out, int no, int cap, int32_t v)
+{
+    if (v < 0 || no >= cap) return no;
+    for (int t = 0; t < no; t++)
+        if (out[t] == v) return no;
+    out[no] = v;
+    return no + 1;
+}
+
+int or_cagra_rows(int64_t S, int K, const int32_t *knn, int R, int32_t *pruned, int32_t *rows)
+{
+    const int h = R / 2;
+    key3 *ord = (key3 *)malloc(sizeof(key3) * (size_t)K);
+    for (int64_t x = 0; x < S; x++) {
+        for (int j = 0; j < K; j++) {
+            const int32_t y = knn[x * K + j];
+            int64_t det = 0;
+            if (y >= 0)
+                for (int i = 0; i < j; i++) {
+                    const int32_t z = knn[x * K + i];
+                    if (z < 0) continue;
+                    for (int t = 0; t < j; t++)
+                        if (knn[(int64_t)z * K + t] == y) { det++; break; }
+                }
+            ord[j].a = y < 0 ? INT64_MAX : det;
+            ord[j].b = j;
+            ord[j].v = y;
+        }
+        qsort(ord, (size_t)K, sizeof(key3), cmp_key3);
+        for (int t = 0; t < R; t++) pruned[x * R + t] = t < K && ord[t].a != INT64_MAX ? ord[t].v : -1;
+    }
+    free(ord);
+    /* reverse candidates (position, source) per target */
+    int64_t *cnt = (int64_t *)calloc((size_t)S + 1, sizeof(int64_t));
+    for (int64_t x = 0; x < S; x++)
+        for (int p = 0; p < R; p++)
+            if (pruned[x * R + p] >= 0) cnt[pruned[x * R + p] + 1]++;
+    for (int64_t y = 0; y < S; y++) cnt[y + 1] += cnt[y];
+    key3 *rv = (key3 *)malloc(sizeof(key3) * (size_t)(cnt[S] > 0 ? cnt[S] : 1));
+    int64_t *fill = (int64_t *)calloc((size_t)S, sizeof(int64_t));
+    for (int64_t x = 0; x < S; x++)
+        for (int p = 0; p < R; p++) {
+            const int32_t y = pruned[x * R + p];
+            if (y < 0) continue;
+            key3 *e = &rv[cnt[y] + fill[y]++];
+            e->a = p; e->b = x; e->v = (int32_t)x;
+        }
+    for (int64_t y = 0; y < S; y++) qsort(rv + cnt[y], (size_t)(cnt[y + 1] - cnt[y]), sizeof(key3), cmp_key3);
+    int32_t *out = (int32_t *)malloc(sizeof(int32_t) * (size_t)R);
+    for (int64_t x = 0; x < S; x++) {
+        int no = 0;
+        for (int t = 0; t < h; t++) no = push_unique(out, no, R, pruned[x * R + t]);
+        for (int64_t e = cnt[x]; e < cnt[x + 1] && e < cnt[x] + h; e++) no = push_unique(out, no, R, rv[e].v);
+        for (int t = h; t < R; t++) no = push_unique(out, no, R, pruned[x * R + t]);
+        for (int t = 0; t < R; t++) rows[x * R + t] = t < no ? out[t] : -1;
+    }
+    free(out); free(rv); free(fill); free(cnt);
+    return 0;
+}

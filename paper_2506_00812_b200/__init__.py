@@ -25,7 +25,7 @@ EXPORTED = ("vf_build_index", "vf_search", "vf_free", "vf_last_error", "vf_get_i
             "vf_serve_start", "vf_serve_submit", "vf_serve_wait", "vf_serve_stop", "vf_serve_info",
             "vf_serve_run", "vf_serve_stats",
             "vf_set_profiling", "vf_get_last_stats", "vf_get_last_items", "vf_build_index_virtual_shards",
-            "vf_partition_labels")
+            "vf_partition_labels", "vf_build_graphs")
 
 
 class VfError(RuntimeError):
@@ -42,6 +42,25 @@ class BuildDesc(C.Structure):
                 ("graph_row_offsets", C.c_void_p), ("graph_local_ids", C.c_void_p),
                 ("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("device", C.c_int32)]
+
+
+class GraphDesc(C.Structure):
+    _fields_ = [("n_points", C.c_int64), ("dim", C.c_int32), ("dtype", C.c_int32),
+                ("vectors", C.c_void_p), ("n_labels", C.c_int32),
+                ("posting_offsets", C.c_void_p), ("posting_ids", C.c_void_p),
+                ("threshold_T", C.c_int32), ("degree_R", C.c_int32), ("knn_k", C.c_int32),
+                ("exact_max", C.c_int64), ("ivf_cell", C.c_int32), ("ivf_probes", C.c_int32),
+                ("kmeans_iters", C.c_int32), ("device", C.c_int32), ("knn_lists", C.c_void_p)]
+
+
+class GraphReport(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("ms_total", "ms_upload", "ms_knn_exact", "ms_kmeans", "ms_knn_ivf",
+                                          "ms_prune", "ms_rows", "ms_download")] + \
+               [(n, C.c_int64) for n in ("n_graph_labels", "n_exact_labels", "n_ivf_labels", "rows", "join_pairs")] + \
+               [("knn_k", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class SearchParams(C.Structure):
@@ -71,7 +90,7 @@ class SearchStats(C.Structure):
                [("kernel_launches", C.c_int32), ("row_bytes", C.c_int32), ("n_profiled", C.c_int64)] + \
                [(n, C.c_double) for n in ("mean_ms_route", "mean_ms_scan", "mean_ms_graph", "mean_ms_merge",
                                           "mean_ms_copy", "mean_ms_total", "ms_scan_active", "ms_graph_active")] + \
-               [("n_invalid_queries", C.c_int64)]
+               [("n_invalid_queries", C.c_int64), ("prefilter_words", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -121,6 +140,8 @@ def lib():
         L.vf_serve_info.argtypes = [p, C.POINTER(i32), C.POINTER(i64)]
         L.vf_build_index_virtual_shards.restype = C.c_int
         L.vf_build_index_virtual_shards.argtypes = [C.POINTER(BuildDesc), i32, C.POINTER(p)]
+        L.vf_build_graphs.restype = C.c_int
+        L.vf_build_graphs.argtypes = [C.POINTER(GraphDesc), p, p, C.POINTER(GraphReport)]
         L.vf_partition_labels.restype = C.c_int
         L.vf_partition_labels.argtypes = [i32, p, i32, p]
         _lib = L
@@ -344,3 +365,30 @@ def nccl_unique_id():
     if h.ncclGetUniqueId(buf) != 0:
         raise VfError(VF_ERR_NCCL, "ncclGetUniqueId failed")
     return bytes(buf.raw)
+
+
+def build_graphs(X, post_off, post_ids, threshold_T, degree_R=16, knn_k=0, exact_max=0, ivf_cell=0, ivf_probes=0,
+                 kmeans_iters=0, device=0, return_knn=False):
+    """vf_build_graphs (f4): the per-label graphs built on the GPU. Returns (graph_off int64[L+1],
+    graph_ids int32[rows*R], report dict[, knn int32[rows][knn_k]])."""
+    X = np.ascontiguousarray(X)
+    post_off = np.ascontiguousarray(post_off, np.int64)
+    post_ids = np.ascontiguousarray(post_ids, np.int32)
+    L = len(post_off) - 1
+    sizes = np.diff(post_off)
+    rows = int(sizes[sizes >= threshold_T].sum())
+    goff = np.empty(L + 1, np.int64)
+    gids = np.empty(max(rows * degree_R, 1), np.int32)
+    kk = knn_k if knn_k > 0 else min(32, 2 * degree_R)
+    kk = 16 if kk <= 16 else 32
+    knn = np.empty((max(rows, 1), kk), np.int32) if return_knn else None
+    d = GraphDesc(X.shape[0], X.shape[1], _dtype_code(X), X.ctypes.data, L, post_off.ctypes.data,
+                  post_ids.ctypes.data if post_ids.size else None, int(threshold_T), int(degree_R), int(knn_k),
+                  int(exact_max), int(ivf_cell), int(ivf_probes), int(kmeans_iters), int(device),
+                  knn.ctypes.data if knn is not None else None)
+    rep = GraphReport()
+    _check(lib().vf_build_graphs(C.byref(d), goff.ctypes.data, gids.ctypes.data, C.byref(rep)))
+    gids = gids[:rows * degree_R]
+    if return_knn:
+        return goff, gids, rep.as_dict(), knn[:rows]
+    return goff, gids, rep.as_dict()

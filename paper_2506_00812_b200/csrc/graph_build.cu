@@ -611,8 +611,8 @@ extern "C" vf_status vf_build_graphs(const vf_graph_desc *d, int64_t *goff, int3
     auto T0 = std::chrono::steady_clock::now();
     if (!d || !goff || !d->vectors || !d->posting_offsets || (d->n_labels > 0 && !d->posting_ids))
         return fail(VF_ERR_INVALID_ARG, "NULL argument");
-    if (d->n_points < 1 || d->n_points >= (1ll << 31) || d->dim < 1 || d->n_labels < 0)
-        return fail(VF_ERR_INVALID_ARG, "bad n_points / dim / n_labels");
+    if (d->n_points < 1 || d->n_points >= (1ll << 31) || d->dim < 1 || d->dim > 256 || d->n_labels < 0)
+        return fail(VF_ERR_INVALID_ARG, "bad n_points / dim (1..256) / n_labels");
     const int R = d->degree_R;
     if (R < 2 || R > 32 || (R & 1)) return fail(VF_ERR_INVALID_ARG, "degree_R must be even, in [2, 32]");
     if (d->threshold_T < 1) return fail(VF_ERR_INVALID_ARG, "threshold_T must be >= 1");
@@ -628,6 +628,7 @@ extern "C" vf_status vf_build_graphs(const vf_graph_desc *d, int64_t *goff, int3
     const int64_t *po = d->posting_offsets;
     const int32_t *pi = d->posting_ids;
     vf_graph_report rp{};
+    rp.knn_k = 0;
 
     // ---- labels with graphs, their rows (label order), node -> label base
     std::vector<int32_t> glab;
@@ -737,14 +738,18 @@ extern "C" vf_status vf_build_graphs(const vf_graph_desc *d, int64_t *goff, int3
             while (gi < glab.size()) {
                 const int32_t l = glab[gi];
                 const int64_t S = po[l + 1] - po[l];
-                if (S > exact_max) { gi++; continue; }
+                if (S > exact_max) {                  // an IVF label ends the chunk (rows stay contiguous)
+                    gi++;
+                    if (chunk.empty()) continue;
+                    break;
+                }
                 if (!chunk.empty() && rows + S > kChunkRows) break;
                 chunk.push_back(l);
                 rows += S;
                 gi++;
             }
             if (chunk.empty()) continue;
-            // chunk rows [r0, r1) of XG (label order; IVF labels in between are skipped by the jobs)
+            // chunk rows [r0, r1) of XG: consecutive exact labels (label order)
             const int64_t r0 = goff[chunk.front()], r1 = goff[chunk.back() + 1];
             std::vector<int32_t> bysize(chunk);
             std::stable_sort(bysize.begin(), bysize.end(),
@@ -760,7 +765,7 @@ extern "C" vf_status vf_build_graphs(const vf_graph_desc *d, int64_t *goff, int3
             if ((size_t)(r1 - r0) * 2 * K * 8 > part.n) VF_CUDA(part.ensure((size_t)(r1 - r0) * 2 * K * 8));
             vf_status st = join_k(jv, rv, tm_xg, tm_xg, XGn.as<uint32_t>(), r0, 1);
             if (st != VF_OK) return st;
-            // merge every row of [r0, r1) that belongs to a chunk label (IVF rows are rewritten later)
+            // every row of [r0, r1): the two column halves -> K local ids
             st = merge(r1 - r0, nullptr, nbase.as<int64_t>() + r0, 0, nullptr, knn.as<int32_t>() + r0 * K);
             if (st != VF_OK) return st;
             rp.n_exact_labels += (int64_t)chunk.size();
@@ -872,6 +877,11 @@ extern "C" vf_status vf_build_graphs(const vf_graph_desc *d, int64_t *goff, int3
         rp.ms_knn_ivf += ms_since(tk);
     }
     rp.join_pairs = J.pairs;
+    rp.knn_k = K;
+    if (d->knn_lists) {
+        VF_CUDA(cudaMemcpyAsync(d->knn_lists, knn.p, (size_t)RT * K * 4, cudaMemcpyDeviceToHost, s));
+        VF_CUDA(cudaStreamSynchronize(s));
+    }
     part.release();
     XG.release();
     XGn.release();

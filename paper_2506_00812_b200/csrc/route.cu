@@ -237,8 +237,10 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
 //   * tile mixing predicate and plain queries: every row is kept, its pass bits go to pool_bits;
 //   * pool exhausted / piece list full: the tile keeps -1 and the scan verifies by itself (exact).
 // Membership: the segment's other labels (<= 64 distinct) become bit positions; a label with a
-// membership bitmap costs one bit read per row, the others one pass over the row's sorted labels;
-// query g passes iff its labels' mask is a subset of the row's.
+// membership bitmap costs one bit read per row (one sector), a label of this rank without one a
+// binary search of the row's id in the label's ascending posting list (M_LS / M_HS: small lists,
+// their upper levels stay in L1), and only a label owned by another rank (sharded index) one pass
+// over the row's sorted label list; query g passes iff its labels' mask is a subset of the row's.
 constexpr int kFiltThreads = 256;
 constexpr int kFiltBuf = 2048;
 constexpr int kFiltUnion = 64;
@@ -254,8 +256,10 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
     __shared__ int32_t s_u[kFiltUnion];           // union of the tile's other query labels, sorted
     __shared__ unsigned long long s_qm[kScanQG];  // per query: its labels' bits in s_u (0: no predicate)
     __shared__ unsigned long long s_plain;        // queries without a predicate (always pass)
-    __shared__ int16_t s_slot[kFiltUnion];        // membership bitmap of each s_u label
-    __shared__ int s_allbits;                     // every s_u label has a bitmap: no label-list reads
+    __shared__ int16_t s_slot[kFiltUnion];        // membership bitmap of each s_u label (-1: none)
+    __shared__ const int32_t *s_pl[kFiltUnion];   // ... else its posting list on this rank (ascending ids)
+    __shared__ int32_t s_pn[kFiltUnion];          // ... and its length (0: not on this rank -> label list)
+    __shared__ int s_allbits;                     // no s_u label needs the point's label list
     const int ntiles = a.ctr->n_tiles;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&a.ctr->filter_next, 1);
@@ -298,12 +302,20 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                     nu++;
                 }
             s_nu = nu;
-            int all = nu <= 64 && a.ix.lbit_slot != nullptr;
-            for (int j = 0; j < nu && all; j++) {
+            int all = nu <= 64;
+            for (int j = 0; j < nu && nu <= 64; j++) {
                 const int32_t l = s_u[j];
-                const int sl = (l >= 0 && l < a.ix.n_labels) ? a.ix.lbit_slot[l] : -1;
+                const bool known = l >= 0 && l < a.ix.n_labels;
+                const int sl = (known && a.ix.lbit_slot) ? a.ix.lbit_slot[l] : -1;
                 s_slot[j] = (int16_t)sl;
-                all = sl >= 0;
+                s_pn[j] = 0;
+                s_pl[j] = nullptr;
+                if (sl < 0 && known) {
+                    const LabelDir dl = a.ix.dir[l];
+                    s_pn[j] = dl.size;
+                    s_pl[j] = (dl.size >= a.ix.T ? a.ix.M_hs : a.ix.M_ls) + dl.base;
+                }
+                if (sl < 0 && s_pn[j] == 0) all = 0;  // not on this rank: the label list decides
             }
             s_allbits = all;
             if (!compact) {
@@ -355,13 +367,27 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
             } else {
                 unsigned long long lb[kFiltRows];
                 if (allbits) {
-                    // membership bitmaps: one bit read per (row, other label), independent loads
+                    // membership bitmaps (one bit read per (row, label), independent loads) and
+                    // binary searches in the short posting lists of labels without one
 #pragma unroll
                     for (int u = 0; u < kFiltRows; u++) {
                         lb[u] = 0;
                         if (gid[u] < 0) continue;
-                        for (int j = 0; j < nu; j++)
-                            if (has_label_bit(a.ix, s_slot[j], gid[u])) lb[u] |= 1ull << j;
+                        for (int j = 0; j < nu; j++) {
+                            bool in;
+                            if (s_slot[j] >= 0) {
+                                in = has_label_bit(a.ix, s_slot[j], gid[u]);
+                            } else {
+                                const int32_t *pl = s_pl[j];
+                                int lo = 0, hi = s_pn[j];
+                                while (lo < hi) {
+                                    const int mid = (lo + hi) >> 1;
+                                    if (__ldg(pl + mid) < gid[u]) lo = mid + 1; else hi = mid;
+                                }
+                                in = lo < s_pn[j] && __ldg(pl + lo) == gid[u];
+                            }
+                            if (in) lb[u] |= 1ull << j;
+                        }
                     }
                 } else {
                     int64_t lo[kFiltRows], hi[kFiltRows];

@@ -580,7 +580,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     bool fresh = false;
     VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
     if (pl.filter) {
-        int64_t cap = 16ll << 20;                       // 64 MB of survivor ids
+        int64_t cap = 64ll << 20;                       // 256 MB of survivor ids + 512 MB of pass bits
         if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
         VF_CUDA(sc->pool.ensure((size_t)cap * 4));
         VF_CUDA(sc->pool_bits.ensure((size_t)cap * 8));
@@ -978,6 +978,7 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->graph_iterations = (int64_t)c.graph_iters;
     st->graph_V_max = (int64_t)c.graph_V_max;
     st->n_invalid_queries = c.n_invalid;
+    st->prefilter_words = c.pool_used;
     st->kernel_launches = sc->last_launches;
     st->row_bytes = ix->enc8 && !c.exact_fallback ? ix->dev8.row_bytes : ix->dev.row_bytes;   // rows the kernels read
     auto span = [](unsigned long long t0_inv, unsigned long long t1) {

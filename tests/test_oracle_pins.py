@@ -364,3 +364,69 @@ def test_beam_multi_parent_trace():
         e = g[key]
         assert ids[0].tolist() == e["ids"] and d[0].tolist() == e["dists"], key
         assert int(ctr[0, 0, 2]) == e["V"] and int(ctr[0, 0, 3]) == e["E"], key
+
+
+# ----------------------------------------------------------------------------- graph builder (f4)
+def test_cagra_rows_hand_example():
+    """or_cagra_rows on the hand-derived example of tests/golden/cagra_prune.json."""
+    g = golden("cagra_prune.json")
+    pruned, rows = oracle.cagra_rows(np.array(g["knn"], np.int32), g["R"])
+    assert pruned.tolist() == g["pruned"]
+    assert rows.tolist() == g["rows"]
+
+
+def test_cagra_rows_special_cases_and_invariants():
+    rng = np.random.default_rng(3)
+    # no detours possible: every list points only at nodes whose lists point elsewhere -> pruned =
+    # the first R entries (a star: leaves list the centre first, the centre lists the leaves)
+    S, K, R = 9, 4, 2
+    knn = np.full((S, K), -1, np.int32)
+    knn[0] = [1, 2, 3, 4]
+    for x in range(1, S):
+        knn[x] = [0] + [-1] * (K - 1)
+    pruned, rows = oracle.cagra_rows(knn, R)
+    assert pruned[0].tolist() == [1, 2]
+    assert all(pruned[x].tolist() == [0, -1] for x in range(1, S))
+    # K == R keeps every entry (a permutation of the list)
+    for _ in range(20):
+        S, K = 30, 8
+        knn = np.stack([rng.choice(np.delete(np.arange(S), x), size=K, replace=False) for x in range(S)]).astype(np.int32)
+        pruned, rows = oracle.cagra_rows(knn, K)
+        assert all(sorted(pruned[x]) == sorted(knn[x]) for x in range(S))
+    # random lists: pruned is a subset of the list; rows hold no -1 before a valid entry, no
+    # duplicate, no self, and only ids of the forward list or of reverse sources
+    for _ in range(20):
+        S, K, R = 40, 12, 6
+        knn = np.stack([rng.choice(np.delete(np.arange(S), x), size=K, replace=False) for x in range(S)]).astype(np.int32)
+        pruned, rows = oracle.cagra_rows(knn, R)
+        for x in range(S):
+            assert set(pruned[x]) <= set(knn[x])
+            r = [v for v in rows[x] if v >= 0]
+            assert len(r) == len(set(r)) and x not in r
+            assert list(rows[x][:len(r)]) == r
+            src = {y for y in range(S) if x in pruned[y]}
+            assert set(r) <= set(pruned[x]) | src
+            assert list(pruned[x][:R // 2]) == r[:R // 2]     # the forward half comes first
+
+
+def test_label_knn_hand_and_bruteforce():
+    """or_label_knn: the App. B 1-D points (hand: ties broken by local id) and a numpy brute force
+    (int64 distances, lexsort by (distance, id)) on a random u8 label."""
+    pts = np.array([0, 2, 4, 6, 8, 10], np.float32)
+    X = np.zeros((6, 4), np.float32)
+    X[:, 0] = pts
+    o = oracle.Index(X, np.array([0, 6], np.int64), np.arange(6, dtype=np.int32), 10, 2)
+    assert o.label_knn(0, 2).tolist() == [[1, 2], [0, 2], [1, 3], [2, 4], [3, 5], [4, 3]]
+    assert o.label_knn(0, 6)[0].tolist() == [1, 2, 3, 4, 5, -1]          # S - 1 < K: -1 padded
+    rng = np.random.default_rng(5)
+    N, D = 300, 24
+    X = rng.integers(0, 256, size=(N, D), dtype=np.uint8)
+    ids = np.sort(rng.choice(N, size=120, replace=False)).astype(np.int32)
+    o = oracle.Index(X, np.array([0, len(ids)], np.int64), ids, 10, 8)
+    got = o.label_knn(0, 10)
+    Xl = X[ids].astype(np.int64)
+    d = ((Xl[:, None, :] - Xl[None, :, :]) ** 2).sum(-1)
+    for j in range(len(ids)):
+        cand = np.delete(np.arange(len(ids)), j)
+        order = np.lexsort((cand, d[j, cand]))
+        assert got[j].tolist() == cand[order][:10].tolist()
