@@ -549,7 +549,7 @@ JoinGeom join_geom(int rb) {
     g.kpad = (rb + g.cw - 1) / g.cw * g.cw;
     g.nch = g.kpad / g.cw;
     int nst = 8;
-    while (nst > 2 && join_layout(g.kpad, nst).total > 227 * 1024) nst--;
+    while (nst > 2 && join_layout(g.kpad, nst).total > 227 * 1024 - 256) nst--;   // + static smem
     g.nst = nst;
     g.smem = join_layout(g.kpad, nst).total;
     return g;
@@ -587,12 +587,7 @@ struct Joiner {
         A.cw = g.cw;
         A.kpad = g.kpad;
         A.nst = g.nst;
-        static bool attr[3] = {false, false, false};
-        const int ai = K == 1 ? 0 : K == 16 ? 1 : 2;
-        if (!attr[ai]) {
-            VF_CUDA(cudaFuncSetAttribute(k_join<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            attr[ai] = true;
-        }
+        VF_CUDA(cudaFuncSetAttribute(k_join<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
         const int grid = (int)std::min<size_t>(jv.size(), (size_t)nsm);
         k_join<K><<<grid, kJoinThreads, g.smem, s>>>(A, *reinterpret_cast<const CUtensorMap *>(tm_q),
                                                      *reinterpret_cast<const CUtensorMap *>(tm_c));
