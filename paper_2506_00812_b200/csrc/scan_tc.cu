@@ -305,10 +305,13 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
         int cum[kTileClasses + 1];
         cum[0] = 0;
         for (int c = 0; c < kTileClasses; c++) cum[c + 1] = cum[c] + (by_cls ? a.ctr->n_tile_cls[c] : 0);
+        TP_DECL
         for (;;) {
             const int tp = tc & 1;
+            TP_MARK(3)
             if (lane == 0) mbar_wait(qempty + tp, ((tc >> 1) & 1) ^ 1);
             __syncwarp();
+            TP_MARK(0)
             int t = 0;
             if (lane == 0) t = atomicAdd(&a.ctr->scan_next, 1);
             t = __shfl_sync(FULL, t, 0);
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                 break;
             }
             const Tile tl = a.tiles[t];
+            TP_MARK(1)
             const int nq = tl.nq;
             TcQMeta *qm = qmeta + (size_t)tp * qg;
             for (int g = lane; g < nq; g += 32) {
@@ -350,8 +354,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(tready + tp);
+            TP_MARK(2)
             tc++;
         }
+        TP_DUMP("sched(qempty,claim+tile,scanq,other)")
     } else if (warp == 0) {
         // ------------------------------------------------------------ producer
         uint32_t n = 0, tc = 0;

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="sift")
     ap.add_argument("--itopk", type=int, default=16)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--and-scan", type=int, default=0)
     a = ap.parse_args()
     from paper_2506_00812_b200 import build as B
     B.build(force=True)
@@ -30,7 +31,7 @@ def main():
     ix = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
     op = "and" if c.query_mode in ("and2", "mix_and") else "single"
     for _ in range(a.reps):
-        ix.search(w.Q, w.q_off, w.q_lab, k=c.k, itopk=a.itopk, search_width=2, op=op)
+        ix.search(w.Q, w.q_off, w.q_lab, k=c.k, itopk=a.itopk, search_width=2, op=op, and_scan_threshold=a.and_scan)
         torch.cuda.synchronize()
         print("----", ix.last_stats(), flush=True)
 
