@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
             }
             s_allbits = all;
             if (!compact) {
-                const int need = (nrows + 1) & ~1;        // even: 16-B aligned bulk copies of the words
+                const int need = (nrows + 3) & ~3;        // 16-B aligned bulk copies of the words
                 const int off = atomicAdd(&a.ctr->pool_used, need);
                 s_bits_off = (int64_t)off + need > a.pool_cap ? -1 : off;
             }
@@ -445,14 +445,17 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                 }
             __syncthreads();
             const bool last = r0 + kFiltThreads * kFiltRows >= tl.row_end;
-            if (s_n > kFiltBuf - kFiltThreads * kFiltRows || (last && s_n > 0)) {
+            // a tile of <= kFiltBuf rows flushes once: its survivors form ONE contiguous piece,
+            // which the scan's producer moves with bulk copies (ids, norms, pass bits)
+            const bool one_piece = nrows <= kFiltBuf;
+            if ((!one_piece && s_n > kFiltBuf - kFiltThreads * kFiltRows) || (last && s_n > 0)) {
                 if (threadIdx.x == 0) {
                     if (s_np == kMaxPieces) {
                         s_bad = 1;
                     } else {
-                        // even sizes keep every allocation 16-B aligned in pool_bits (the
-                        // per-row words of mixed tiles are read by bulk copies)
-                        const int off = atomicAdd(&a.ctr->pool_used, (s_n + 1) & ~1);
+                        // sizes rounded to 4 keep every allocation 16-B aligned in pool (ids,
+                        // norms) and pool_bits: the scan reads them with bulk copies
+                        const int off = atomicAdd(&a.ctr->pool_used, (s_n + 3) & ~3);
                         if ((int64_t)off + s_n > a.pool_cap) {
                             s_bad = 1;
                         } else {
@@ -468,6 +471,7 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                     for (int i = threadIdx.x; i < s_n; i += kFiltThreads) {
                         a.pool[s_flush_off + i] = buf[i];
                         a.pool_bits[s_flush_off + i] = bbuf[i];
+                        if (a.pool_norm) a.pool_norm[s_flush_off + i] = __ldg(a.ix.xn + buf[i]);
                     }
                 __syncthreads();
                 if (threadIdx.x == 0) s_n = 0;

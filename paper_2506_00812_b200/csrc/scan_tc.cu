@@ -424,6 +424,36 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                         if (rbits) tma_load_1d(dbits, a.pool_bits + tl.bits_off + v0, bb, full + slot);
                     }
                     __syncwarp();
+                } else if (filt && tl.n_pieces == 1 && a.pool_norm) {
+                    // compacted tile, one piece: ids by the lanes (one coalesced read, the only
+                    // wait), the rows by tile::gather4, and ids / norms / pass bits by bulk copies
+                    const int ng = (nr + 3) >> 2;
+                    const int64_t po = tl.piece_off[0] + v0;          // 16-B aligned (k_and_filter)
+                    const uint32_t b4n = (uint32_t)((nr * 4 + 15) & ~15), b8n = (uint32_t)((nr * 8 + 15) & ~15);
+                    if (lane == 0) {
+                        mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
+                        meta[slot] = make_int4(t, r0, nr, flags);
+                        mbar_arrive_expect_tx(full + slot, (uint32_t)(ng * 4 * kpad) + 2 * b4n + b8n);
+                        tma_load_1d(dsid, a.pool + po, b4n, full + slot);
+                        tma_load_1d(dnorm, a.pool_norm + po, b4n, full + slot);
+                        tma_load_1d(dbits, a.pool_bits + po, b8n, full + slot);
+                    }
+                    __syncwarp();
+                    for (int q4 = lane; q4 < ng; q4 += 32) {
+                        const int rr = q4 * 4;
+                        int32_t g4[4];
+                        if (rr + 3 < nr) {
+                            const int4 v4 = __ldg(reinterpret_cast<const int4 *>(a.pool + po) + q4);
+                            g4[0] = v4.x; g4[1] = v4.y; g4[2] = v4.z; g4[3] = v4.w;
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; j++) g4[j] = __ldg(a.pool + po + min(rr + j, nr - 1));
+                        }
+                        for (int c = 0; c < nch; c++)
+                            tma_gather4(dst + (size_t)c * kTcRows * cw + (size_t)q4 * 4 * cw, &tm_x, c * cw, g4,
+                                        full + slot);
+                    }
+                    __syncwarp();
                 } else {
                     // HS label (exact mode / f3): gather rows of X through M_HS, 4 rows per TMA
                     // tile::gather4 per K chunk (a short group repeats its last row; ignored)

@@ -559,6 +559,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     pl.filter = pl.tc && p->op == VF_AND;
     a.pool = nullptr;
     a.pool_bits = nullptr;
+    a.pool_norm = nullptr;
     a.pool_cap = 0;
     a.n_slots = n_slots;
     a.max_nl = ix->world > 1 ? kRecLabels : kMaxQueryLabels;
@@ -584,8 +585,10 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
         if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
         VF_CUDA(sc->pool.ensure((size_t)cap * 4));
         VF_CUDA(sc->pool_bits.ensure((size_t)cap * 8));
+        VF_CUDA(sc->pool_norm.ensure((size_t)cap * 4));
         a.pool = sc->pool.as<int32_t>();
         a.pool_bits = sc->pool_bits.as<unsigned long long>();
+        a.pool_norm = D.xn ? sc->pool_norm.as<uint32_t>() : nullptr;
         a.pool_cap = (int32_t)cap;
     }
     if (ix->enc8) {

@@ -214,6 +214,7 @@ struct SearchArgs {
                               // claims longest tiles first; nullptr = creation order)
     int32_t *pool;            // AND pre-filter survivor ids (k_and_filter)
     unsigned long long *pool_bits;  // ... and their per-query pass bits (bit g: query g of the tile)
+    uint32_t *pool_norm;      // ... and their ||x||^2 (tensor-core scan; nullptr: none)
     int32_t pool_cap;
     // device-side validation of caller offsets (device label arrays are not read by the host): a
     // query whose labels fall outside [0, n_slots) or number more than max_nl gets an empty row
