@@ -63,8 +63,12 @@ struct JoinArgs {
 };
 
 struct JoinLayout {
-    size_t off_bar, off_meta, off_a, off_st, st_bytes, total;
+    size_t off_bar, off_meta, off_a, off_st, st_bytes, off_lists, total;
 };
+
+// per epilogue thread, a running top-K list in shared memory ([K][256] keys: entry i of thread t at
+// i * 256 + t); insertion shifts only the tail it displaces (new keys land near the end)
+constexpr int kJoinListK = 32;
 
 __host__ __device__ static JoinLayout join_layout(int kpad, int nst) {
     JoinLayout L{};
@@ -81,6 +85,8 @@ __host__ __device__ static JoinLayout join_layout(int kpad, int nst) {
     o = (o + 1023) / 1024 * 1024;
     L.off_st = o;
     o += L.st_bytes * nst;
+    L.off_lists = o;
+    o += (size_t)kJoinListK * 32 * kJoinEpiW * 8;
     L.total = o + 1024;
     return L;
 }
@@ -98,12 +104,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
 }
 
-// insert `key` into the ascending register list L[0..K) (L[K-1] is dropped)
+// insert `key` (< Ls[K-1]) into the ascending shared-memory list Ls[i * S] (i < K); returns the
+// new K-th key
 template <int K>
-__device__ __forceinline__ void list_insert(ull (&L)[K], ull key) {
-#pragma unroll
-    for (int i = K - 1; i > 0; i--) L[i] = key < L[i - 1] ? L[i - 1] : (key < L[i] ? key : L[i]);
-    L[0] = key < L[0] ? key : L[0];
+__device__ __noinline__ ull list_insert_s(ull *Ls, ull key) {
+    constexpr int S = 32 * kJoinEpiW;
+    int i = K - 1;
+    while (i > 0) {
+        const ull prev = Ls[(i - 1) * S];
+        if (!(key < prev)) break;
+        Ls[i * S] = prev;
+        i--;
+    }
+    Ls[i * S] = key;
+    return Ls[(K - 1) * S];
 }
 
 // Stage meta (32 B): q_row, nq, flags | abuf << 8 | (job parity) << 9, candidate row0, ncols
@@ -115,6 +129,7 @@ struct JMeta {
 template <int K>
 __global__ void __launch_bounds__(kJoinThreads, 1)
     k_join(JoinArgs A, const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c) {
+    static_assert(K <= kJoinListK, "list capacity");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     const int nst = A.nst, nch = A.nch, cw = A.cw, kpad = A.kpad;
@@ -248,9 +263,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
         // ------------------------------------------------------------ epilogue (8 warps)
         const int quarter = warp & 3, half = (warp - 2) >> 2;
         const int r = quarter * 32 + lane;                 // query of this thread (TMEM lane)
-        ull L[K];
-#pragma unroll
-        for (int i = 0; i < K; i++) L[i] = KEY_INF;
+        ull *Ls = reinterpret_cast<ull *>(smem + SL.off_lists) + (threadIdx.x - 64);
+        constexpr int LS = 32 * kJoinEpiW;
+        for (int i = 0; i < K; i++) Ls[i * LS] = KEY_INF;
+        ull kth = KEY_INF;
         uint32_t n = 0;
         for (;;) {
             const int slot = n % nst, buf = n & 1;
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
             const uint32_t *scn = reinterpret_cast<const uint32_t *>(st + (size_t)slot * SL.st_bytes + (size_t)kJoinN * kpad);
             const bool valid = r < m.nq;
             const int64_t qrow = m.q_row + r;
-            uint32_t thr = (uint32_t)(L[K - 1] >> 32);
+            uint32_t thr = (uint32_t)(kth >> 32);
             const int c_lo = half * (kJoinN / 2);
 #pragma unroll 1
             for (int c0 = c_lo; c0 < c_lo + kJoinN / 2; c0 += 32) {
@@ -283,9 +299,9 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                             const int64_t crow = (int64_t)m.row0 + col;
                             if (!(A.exclude_self && crow == qrow)) {
                                 const ull key = ((ull)key32 << 32) | (uint32_t)crow;
-                                if (key < L[K - 1]) {
-                                    list_insert<K>(L, key);
-                                    thr = (uint32_t)(L[K - 1] >> 32);
+                                if (key < kth) {
+                                    kth = list_insert_s<K>(Ls, key);
+                                    thr = (uint32_t)(kth >> 32);
                                 }
                             }
                         }
@@ -301,11 +317,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
             if (m.flags & JF_LAST) {
                 if (valid) {
                     ull *o = A.out + ((qrow - A.out_base) * 2 + half) * K;
-#pragma unroll
-                    for (int i = 0; i < K; i++) o[i] = L[i];
+                    for (int i = 0; i < K; i++) o[i] = Ls[i * LS];
                 }
-#pragma unroll
-                for (int i = 0; i < K; i++) L[i] = KEY_INF;
+                for (int i = 0; i < K; i++) Ls[i * LS] = KEY_INF;
+                kth = KEY_INF;
             }
             n++;
         }

@@ -67,6 +67,10 @@ struct Scratch {
     // scan / graph overlap: the graph kernels run on a side stream forked after routing
     cudaStream_t side = nullptr, side_hi = nullptr;   // graph kernels; scan kernels (high priority)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+    // label sharding: the exchange stream, its events and the pinned copy of the routed counters
+    cudaStream_t xs = nullptr;
+    cudaEvent_t ev_routed = nullptr, ev_cnt = nullptr, ev_xdone = nullptr;
+    Counters *hctr = nullptr;
     size_t gtab_slots = 0, gtab_warps = 0;
     // profiled searches record their phase events into a ring: ev points at the current set, so
     // the mean over every search since profiling was enabled (<= kProfRing of them) is readable
@@ -92,6 +96,11 @@ struct Scratch {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (ev_join2) cudaEventDestroy(ev_join2);
+        if (xs) cudaStreamDestroy(xs);
+        if (ev_routed) cudaEventDestroy(ev_routed);
+        if (ev_cnt) cudaEventDestroy(ev_cnt);
+        if (ev_xdone) cudaEventDestroy(ev_xdone);
+        if (hctr) cudaFreeHost(hctr);
     }
 };
 
@@ -148,9 +157,13 @@ struct Plan {
 // (queries, labels and outputs are bound by the caller).
 vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, const vf_search_params *p,
                       cudaStream_t s, Plan *out);
-// route (k_prepare) or unpack received items, then bucket, scan and graph for the local items.
+// route (k_prepare) or unpack received items, then bucket, scan and graph for the local items
+// (= run_route + run_compute).
 vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
                     int rec_bytes, int *launches);
+vf_status run_route(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
+                    int rec_bytes, int *launches);
+vf_status run_compute(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, int *launches);
 
 // Label sharding entry points (shard.cpp).
 vf_status shard_partition(int32_t n_labels, const int64_t *sizes, int32_t world, int32_t *owner);

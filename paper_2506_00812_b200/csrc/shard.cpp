@@ -166,6 +166,22 @@ struct ShardJob {
     int64_t n_send = 0, n_recv = 0;
 };
 
+// The exchange runs on a second stream of the origin scratch (xs) so that the local items' scan /
+// graph kernels (on the caller's stream) overlap it: the only host waits are for the routed
+// per-owner counts (they size the exchange) and the count exchange itself, both right after
+// routing; the item records, the owners' searches and the results travel while the local
+// kernels run, and the caller's stream joins the exchange stream only for the final merge.
+static vf_status exchange_stream(Scratch *sc) {
+    if (!sc->xs) {
+        VF_CUDA(cudaStreamCreateWithFlags(&sc->xs, cudaStreamNonBlocking));
+        VF_CUDA(cudaEventCreateWithFlags(&sc->ev_routed, cudaEventDisableTiming));
+        VF_CUDA(cudaEventCreateWithFlags(&sc->ev_cnt, cudaEventDisableTiming));
+        VF_CUDA(cudaEventCreateWithFlags(&sc->ev_xdone, cudaEventDisableTiming));
+        VF_CUDA(cudaHostAlloc((void **)&sc->hctr, sizeof(Counters), cudaHostAllocDefault));
+    }
+    return VF_OK;
+}
+
 vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void *> &queries,
                          std::vector<int64_t> &nq, std::vector<const int64_t *> &qoff,
                          std::vector<const int32_t *> &qlab, const vf_search_params *p,
@@ -179,8 +195,9 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
     const int rec_bytes = (int)sizeof(ItemRecord) + D0.row_bytes;
     if (!tr) return fail(VF_ERR_INTERNAL, "sharded index without transport");
     std::vector<ShardJob> jobs(J);
+    bool any_host_out = false;
 
-    // ---- phase 1: every origin routes its queries and runs the items it owns
+    // ---- phase 1: every origin routes its queries; local items start on s, counts go to the host
     for (int j = 0; j < J; j++) {
         ShardJob &jb = jobs[j];
         vf_index *ix = shards[j];
@@ -189,25 +206,30 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         jb.own = get_scratch(ix, s, 0);
         jb.exec = get_scratch(ix, s, 1);
         VF_CUDA(cudaSetDevice(ix->device));
+        vf_status st = exchange_stream(jb.own);
+        if (st != VF_OK) return st;
         const bool q_dev = is_device_ptr(queries[j]), off_dev = is_device_ptr(qoff[j]);
         const bool lab_dev = is_device_ptr(qlab[j]);
         jb.out_dev = is_device_ptr(out_ids[j]);
+        any_host_out |= !jb.out_dev;
         jb.out_ids = out_ids[j];
         jb.out_dists = out_dists[j];
         int64_t lo = 0, hi = 0;
         if (jb.n > 0) {
-            if (off_dev) {
+            if (!off_dev) {
+                lo = qoff[j][0];
+                hi = qoff[j][jb.n];
+            } else if (J == 1 && p->n_query_labels > 0) {
+                hi = p->n_query_labels;        // device offsets of the caller's batch: qoff[0] == 0
+            } else {
                 VF_CUDA(cudaMemcpyAsync(&lo, qoff[j], 8, cudaMemcpyDeviceToHost, s));
                 VF_CUDA(cudaMemcpyAsync(&hi, qoff[j] + jb.n, 8, cudaMemcpyDeviceToHost, s));
                 VF_CUDA(cudaStreamSynchronize(s));
-            } else {
-                lo = qoff[j][0];
-                hi = qoff[j][jb.n];
             }
         }
         jb.n_slots = hi - lo;
         Scratch *sc = jb.own;
-        vf_status st = plan_search(ix, sc, jb.n, jb.n_slots, p, s, &jb.po);
+        st = plan_search(ix, sc, jb.n, jb.n_slots, p, s, &jb.po);
         if (st != VF_OK) return st;
         SearchArgs &a = jb.po.a;
         VF_CUDA(sc->raw.ensure((size_t)std::max<int64_t>(jb.n, 1) * raw_bytes));
@@ -216,12 +238,16 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         if (jb.n > 0) {
             VF_CUDA(cudaMemcpyAsync(sc->raw.p, queries[j], (size_t)jb.n * raw_bytes,
                                     q_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-            // offsets rebased to this chunk's first label
-            std::vector<int64_t> ho(jb.n + 1);
-            if (off_dev) VF_CUDA(cudaMemcpy(ho.data(), qoff[j], (jb.n + 1) * 8, cudaMemcpyDeviceToHost));
-            else std::memcpy(ho.data(), qoff[j], (jb.n + 1) * 8);
-            for (auto &v : ho) v -= lo;
-            VF_CUDA(cudaMemcpy(sc->qoff.p, ho.data(), (jb.n + 1) * 8, cudaMemcpyHostToDevice));
+            if (off_dev && lo == 0) {
+                VF_CUDA(cudaMemcpyAsync(sc->qoff.p, qoff[j], (jb.n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+            } else {
+                // offsets rebased to this chunk's first label
+                std::vector<int64_t> ho(jb.n + 1);
+                if (off_dev) VF_CUDA(cudaMemcpy(ho.data(), qoff[j], (jb.n + 1) * 8, cudaMemcpyDeviceToHost));
+                else std::memcpy(ho.data(), qoff[j], (jb.n + 1) * 8);
+                for (auto &v : ho) v -= lo;
+                VF_CUDA(cudaMemcpy(sc->qoff.p, ho.data(), (jb.n + 1) * 8, cudaMemcpyHostToDevice));
+            }
             if (jb.n_slots > 0)
                 VF_CUDA(cudaMemcpyAsync(sc->qlab.p, qlab[j] + lo, (size_t)jb.n_slots * 4,
                                         lab_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
@@ -231,15 +257,22 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         a.out_dists = sc->out_dists.as<float>();
         int launches = 0;
         if (ix->profiling) VF_CUDA(cudaEventRecord(sc->ev[0], s));
-        st = run_local(ix, sc, jb.po, s, nullptr, 0, 0, &launches);
+        st = run_route(ix, sc, jb.po, s, nullptr, 0, 0, &launches);
+        if (st != VF_OK) return st;
+        VF_CUDA(cudaEventRecord(sc->ev_routed, s));
+        VF_CUDA(cudaStreamWaitEvent(sc->xs, sc->ev_routed, 0));
+        VF_CUDA(cudaMemcpyAsync(sc->hctr, sc->ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, sc->xs));
+        VF_CUDA(cudaEventRecord(sc->ev_cnt, sc->xs));
+        st = run_compute(ix, sc, jb.po, s, &launches);       // local items, overlapping the exchange
         if (st != VF_OK) return st;
         sc->last_launches = launches;
-        Counters c;
-        VF_CUDA(cudaMemcpyAsync(&c, sc->ctr.p, sizeof(c), cudaMemcpyDeviceToHost, s));
-        VF_CUDA(cudaStreamSynchronize(s));
-        jb.send_cnt.assign(W, 0);
-        for (int r = 0; r < W; r++) jb.send_cnt[r] = c.remote[r];
     }
+    for (auto &jb : jobs) {
+        VF_CUDA(cudaEventSynchronize(jb.own->ev_cnt));
+        jb.send_cnt.assign(W, 0);
+        for (int r = 0; r < W; r++) jb.send_cnt[r] = jb.own->hctr->remote[r];
+    }
+    cudaStream_t xs = jobs[0].own->xs;       // one stream carries the exchange (per process)
 
     // ---- phase 2: exchange the per-destination counts
     for (int j = 0; j < J; j++) jobs[j].recv_cnt.assign(W, 0);
@@ -247,7 +280,7 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         for (int src = 0; src < J; src++)
             for (int dst = 0; dst < J; dst++) jobs[dst].recv_cnt[src] = jobs[src].send_cnt[dst];
     } else {
-        vf_status st = tr->exchange_counts(jobs[0].send_cnt.data(), jobs[0].recv_cnt.data(), W, shards[0]->rank, s);
+        vf_status st = tr->exchange_counts(jobs[0].send_cnt.data(), jobs[0].recv_cnt.data(), W, shards[0]->rank, xs);
         if (st != VF_OK) return st;
     }
     for (auto &jb : jobs) {
@@ -261,15 +294,19 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         jb.n_recv = jb.recv_off[W];
     }
 
-    // ---- phase 3: pack the remote items and ship them to their owners
+    // ---- phase 3: pack the remote items and ship them to their owners (exchange stream)
     for (auto &jb : jobs) {
         Scratch *sc = jb.own;
         VF_CUDA(cudaSetDevice(jb.ix->device));
+        if (jb.own->xs != xs) {           // loopback shards: every shard's exchange work on xs
+            VF_CUDA(cudaEventRecord(jb.own->ev_routed, s));
+            VF_CUDA(cudaStreamWaitEvent(xs, jb.own->ev_routed, 0));
+        }
         VF_CUDA(sc->send.ensure((size_t)std::max<int64_t>(jb.n_send, 1) * rec_bytes));
         VF_CUDA(sc->sent_slots.ensure((size_t)std::max<int64_t>(jb.n_send, 1) * 4));
         VF_CUDA(sc->dst_off.ensure((size_t)(W + 1) * 8));
-        VF_CUDA(cudaMemcpyAsync(sc->dst_off.p, jb.send_off.data(), (W + 1) * 8, cudaMemcpyHostToDevice, s));
-        launch_pack_remote(jb.po.a, s, jb.n_slots, sc->send.as<uint8_t>(), sc->dst_off.as<int64_t>(),
+        VF_CUDA(cudaMemcpyAsync(sc->dst_off.p, jb.send_off.data(), (W + 1) * 8, cudaMemcpyHostToDevice, xs));
+        launch_pack_remote(jb.po.a, xs, jb.n_slots, sc->send.as<uint8_t>(), sc->dst_off.as<int64_t>(),
                            sc->sent_slots.as<int32_t>(), rec_bytes);
         VF_CUDA(jb.exec->recv.ensure((size_t)std::max<int64_t>(jb.n_recv, 1) * rec_bytes));
     }
@@ -294,7 +331,7 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
                     if (cnt == 0) continue;
                     const uint8_t *from = forward ? sbuf(a_) + a_.send_off[dst] * unit : sbuf(b_) + b_.recv_off[src] * unit;
                     uint8_t *to = forward ? rbuf(b_) + b_.recv_off[src] * unit : rbuf(a_) + a_.send_off[dst] * unit;
-                    VF_CUDA(cudaMemcpyAsync(to, from, cnt * unit, cudaMemcpyDeviceToDevice, s));
+                    VF_CUDA(cudaMemcpyAsync(to, from, cnt * unit, cudaMemcpyDeviceToDevice, xs));
                 }
             return VF_OK;
         }
@@ -310,7 +347,7 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
             }
         }
         return tr->alltoallv(sbuf(jb), soff.data(), sb.data(), rbuf(jb), roff.data(), rb.data(), W,
-                             jb.ix->rank, s);
+                             jb.ix->rank, xs);
     };
     vf_status st = exchange(true, 0);
     if (st != VF_OK) return st;
@@ -319,7 +356,7 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
     for (auto &jb : jobs) {
         vf_index *ix = jb.ix;
         Scratch *sc = jb.exec;
-        st = plan_search(ix, sc, jb.n_recv, jb.n_recv, p, s, &jb.pe);
+        st = plan_search(ix, sc, jb.n_recv, jb.n_recv, p, xs, &jb.pe);
         if (st != VF_OK) return st;
         VF_CUDA(sc->qlab.ensure((size_t)std::max<int64_t>(jb.n_recv, 1) * kRecLabels * 4));
         VF_CUDA(sc->res_ids.ensure((size_t)std::max<int64_t>(jb.n_recv, 1) * k * 4));
@@ -329,7 +366,7 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         a.out_ids = sc->res_ids.as<int32_t>();
         a.out_dists = sc->res_dists.as<float>();
         int launches = 0;
-        st = run_local(ix, sc, jb.pe, s, sc->recv.as<uint8_t>(), jb.n_recv, rec_bytes, &launches);
+        st = run_local(ix, sc, jb.pe, xs, sc->recv.as<uint8_t>(), jb.n_recv, rec_bytes, &launches);
         if (st != VF_OK) return st;
         jb.own->last_launches += launches;
         VF_CUDA(jb.own->back_ids.ensure((size_t)std::max<int64_t>(jb.n_send, 1) * k * 4));
@@ -341,6 +378,8 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
     if (st != VF_OK) return st;
     st = exchange(false, 1);
     if (st != VF_OK) return st;
+    VF_CUDA(cudaEventRecord(jobs[0].own->ev_xdone, xs));
+    VF_CUDA(cudaStreamWaitEvent(s, jobs[0].own->ev_xdone, 0));
 
     // ---- phase 6: origins merge local and returned lists per query (a5)
     for (auto &jb : jobs) {
@@ -364,7 +403,9 @@ vf_status sharded_search(std::vector<vf_index *> &shards, std::vector<const void
         sc->has_last = true;
     }
     VF_CUDA(cudaGetLastError());
-    VF_CUDA(cudaStreamSynchronize(s));
+    // host outputs or no stream: the results must be there on return (device outputs with a
+    // stream: asynchronous like vf_search)
+    if (any_host_out || s == nullptr) VF_CUDA(cudaStreamSynchronize(s));
     return VF_OK;
 }
 

@@ -663,6 +663,14 @@ static inline int D_dtype(const vf_index *ix) { return ix->dev.dtype; }
 
 vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
                     int rec_bytes, int *launches) {
+    vf_status st = run_route(ix, sc, pl, s, recv, n_recv, rec_bytes, launches);
+    if (st != VF_OK) return st;
+    return run_compute(ix, sc, pl, s, launches);
+}
+
+// a1 (+ the AND pre-filter): everything up to the scan / graph fork
+vf_status run_route(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
+                    int rec_bytes, int *launches) {
     SearchArgs &a = pl.a;
     const bool prof = ix->profiling;
     VF_CUDA(cudaMemsetAsync(sc->ctr.p, 0, sizeof(Counters), s));
@@ -677,6 +685,16 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
     if (pl.filter) nl += launch_and_filter(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
+    VF_CUDA(cudaGetLastError());
+    *launches += nl;
+    return VF_OK;
+}
+
+// a2 / a3: the scan and graph kernels of the routed items (concurrently, on forked streams)
+vf_status run_compute(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, int *launches) {
+    SearchArgs &a = pl.a;
+    const bool prof = ix->profiling;
+    int nl = 0;
     const int tb = (int)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     // scan and graph items are independent (Alg. 2 L418 / L428): the graph kernels run on a side
     // stream concurrently with the scan; graph CTAs take whatever each SM has left and pull items

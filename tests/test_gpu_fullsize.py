@@ -6,8 +6,8 @@ in ONE vf_search, device buffers, the 0.90 / 0.99 operating points) and a YFCC-s
 mixed single / AND2 batch, f3 routing off and on): the GPU answers the whole batch;
 a seeded sample of queries is answered one by one by the CPU oracle on the same arrays and must
 match bit-exactly (ids, distances, per-item V / E). Exact mode (T = infinity) is checked against the
-oracle's brute-force Definition 1 on a sample. The full 10M-point YFCC-shaped index needs ~6 min of
-fixture-graph building and is exercised by bench.py, not here."""
+oracle's brute-force Definition 1 on a sample. The full 10M-point YFCC-shaped index (configs[2] at
+its size; ~6 min of fixture-graph building) is checked the same way in the `slow` test at the end."""
 import numpy as np
 import pytest
 
@@ -93,12 +93,39 @@ def test_sift_full_batch_exact_mode_is_definition1(vf, sift):
         assert (ids[i] == gt[0]).all() and (d[i] == gd[0].astype(np.float32)).all(), i
 
 
-def test_yfcc_shaped_1m_sampled_parity(vf):
-    w, go, gi = _build("yfcc", n_points=1_000_000, n_queries=20_000)
+@pytest.fixture(scope="module")
+def yfcc1m():
+    return _build("yfcc", n_points=1_000_000, n_queries=20_000)
+
+
+# the bench's operating-point families on the YFCC-shaped mix: paper routing (greedy / parallel),
+# f3 at the 0.90 point, and the 0.99 point (itopk 192-384, w = 4: two 32-child batches per
+# iteration, 64 entry samples), each in one batched vf_search
+@pytest.mark.parametrize("itopk,w_,mode,thr", [(48, 2, "greedy", 0), (48, 2, "greedy", 2000), (32, 2, "parallel", 0),
+                                               (192, 2, "greedy", 50000), (384, 4, "greedy", 50000)])
+def test_yfcc_shaped_1m_sampled_parity(vf, yfcc1m, itopk, w_, mode, thr):
+    w, go, gi = yfcc1m
     c = w.cfg
     g = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
     o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
-    for thr in (0, 2000):
-        ids, d, recs = _gpu_batch(vf, g, w, itopk=48, search_width=2, op="and", and_scan_threshold=thr)
-        sample = np.random.default_rng(9 + thr).choice(len(w.Q), SAMPLE, replace=False)
-        _sample_check(o, w, ids, d, recs, sample, itopk=48, search_width=2, op="and", and_scan_threshold=thr)
+    kw = dict(itopk=itopk, search_width=w_, op="and", recall_mode=mode, and_scan_threshold=thr)
+    ids, d, recs = _gpu_batch(vf, g, w, **kw)
+    sample = np.random.default_rng(9 + thr + itopk).choice(len(w.Q), SAMPLE, replace=False)
+    _sample_check(o, w, ids, d, recs, sample, **kw)
+    g.close()
+
+
+@pytest.mark.slow
+def test_yfcc_10m_sampled_parity(vf):
+    """BASELINE.json configs[2] at its full size (10M x 192 u8, 200,386 labels, the 100K mixed
+    batch in one vf_search) with fixture graphs (an oracle input never comes from the CUDA path):
+    48 sampled queries bit-exact vs the oracle at the 0.90 (f3) and 0.99 operating points."""
+    w, go, gi = _build("yfcc")
+    c = w.cfg
+    g = vf.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
+    o = oracle.Index(w.X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi)
+    for itopk, w_, thr in ((48, 2, 2000), (192, 2, 50000)):
+        kw = dict(itopk=itopk, search_width=w_, op="and", and_scan_threshold=thr)
+        ids, d, recs = _gpu_batch(vf, g, w, **kw)
+        sample = np.random.default_rng(31 + itopk).choice(len(w.Q), SAMPLE, replace=False)
+        _sample_check(o, w, ids, d, recs, sample, **kw)
