@@ -564,7 +564,7 @@ JoinGeom join_geom(int rb) {
     g.kpad = (rb + g.cw - 1) / g.cw * g.cw;
     g.nch = g.kpad / g.cw;
     int nst = 8;
-    while (nst > 2 && join_layout(g.kpad, nst).total > 227 * 1024 - 256) nst--;   // + static smem
+    while (nst > 1 && join_layout(g.kpad, nst).total > 227 * 1024 - 256) nst--;   // + static smem
     g.nst = nst;
     g.smem = join_layout(g.kpad, nst).total;
     return g;

@@ -191,7 +191,9 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
                 tl.bits_off = -1;
                 tl.n_pieces = -1;
                 a.tiles[tb + t] = tl;
-                if (a.tile_cls) {
+                if (a.pack_list && ntile == 1 && !tl.hs && sg.n_items <= a.pack_max_nq) {
+                    a.pack_list[atomicAdd(&a.ctr->n_pack, 1)] = tb + t;     // packed by k_pack
+                } else if (a.tile_cls) {
                     const int c = tile_class(tl.row_end - tl.row_begin);
                     a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = tb + t;
                 }
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                     for (int i = threadIdx.x; i < s_n; i += kFiltThreads) {
                         a.pool[s_flush_off + i] = buf[i];
                         a.pool_bits[s_flush_off + i] = bbuf[i];
-                        if (a.pool_norm) a.pool_norm[s_flush_off + i] = __ldg(a.ix.xn + buf[i]);
+                        if (a.pool_norm) a.pool_norm[s_flush_off + i] = __ldg(a.tc_xn + buf[i]);
                     }
                 __syncthreads();
                 if (threadIdx.x == 0) s_n = 0;
@@ -493,6 +495,139 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------- tile packing
+// The YFCC-shaped batch holds ~36K scan segments of ~1.4 queries and a few hundred rows: one tile
+// each, the tensor-core scan's per-tile chain (claim, query load, B operand, thresholds, results)
+// dominated its time. pack_group such segments become ONE tile: its queries are the segments'
+// queries side by side (<= 64), its rows the segments' rows (after the AND pre-filter), each row
+// carrying the pass bits of exactly its own segment's queries -- every other (row, query) pair of
+// the packed tile is masked in the scan's epilogue, so each query still sees exactly its label's
+// rows (reading #50). One CTA per group.
+constexpr int kPackThreads = 256;
+constexpr int kPackMaxGroup = 16;
+
+__global__ void __launch_bounds__(kPackThreads) k_pack(SearchArgs a) {
+    __shared__ Tile st[kPackMaxGroup];
+    __shared__ int s_q0[kPackMaxGroup + 1], s_r0[kPackMaxGroup + 1];
+    __shared__ int s_off, s_cnt, s_pq, s_ok;
+    const int n_pack = a.ctr->n_pack;
+    const int G = a.pack_group;
+    const int n_groups = (n_pack + G - 1) / G;
+    for (int gidx = blockIdx.x; gidx < n_groups; gidx += gridDim.x) {
+        const int i0 = gidx * G, ng = min(G, n_pack - i0);
+        if (threadIdx.x < ng) st[threadIdx.x] = a.tiles[a.pack_list[i0 + threadIdx.x]];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int q = 0, r = 0;
+            for (int s = 0; s < ng; s++) {
+                s_q0[s] = q;
+                s_r0[s] = r;
+                q += st[s].nq;
+                int rows = st[s].row_end - st[s].row_begin;
+                if (st[s].n_pieces >= 0) {
+                    rows = 0;
+                    for (int p = 0; p < st[s].n_pieces; p++) rows += st[s].piece_cnt[p];
+                }
+                r += rows;
+            }
+            s_q0[ng] = q;
+            s_r0[ng] = r;
+            const int off = atomicAdd(&a.ctr->pool_used, (r + 3) & ~3);
+            s_ok = q <= 64 && (int64_t)off + r <= a.pool_cap;
+            s_off = off;
+            s_cnt = 0;
+            s_pq = s_ok ? atomicAdd(&a.ctr->packq_used, q) : 0;
+        }
+        __syncthreads();
+        if (!s_ok) {
+            // no room: the segments stay tiles of their own (claimed like any other)
+            if (threadIdx.x < ng) {
+                const int t = a.pack_list[i0 + threadIdx.x];
+                const int c = tile_class(st[threadIdx.x].row_end - st[threadIdx.x].row_begin);
+                a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = t;
+            }
+            __syncthreads();
+            continue;
+        }
+        // query records side by side
+        for (int s = 0; s < ng; s++)
+            for (int g = threadIdx.x; g < st[s].nq; g += kPackThreads)
+                a.scan_q[a.packq_base + s_pq + s_q0[s] + g] = a.scan_q[st[s].item_base + g];
+        // rows: compacted survivors, or every row of the label (with per-row AND bits if any)
+        const int off = s_off;
+        for (int s = 0; s < ng; s++) {
+            const Tile &T = st[s];
+            const int q0 = s_q0[s];
+            const unsigned long long mine = (T.nq >= 64 ? ~0ull : ((1ull << T.nq) - 1)) << q0;
+            const int nrows = s_r0[s + 1] - s_r0[s];
+            for (int i0r = 0; i0r < nrows; i0r += kPackThreads) {
+                const int i = i0r + threadIdx.x;
+                int32_t gid = -1;
+                uint32_t nrm = 0;
+                unsigned long long bits = 0;
+                if (i < nrows) {
+                    if (T.n_pieces >= 0) {
+                        int v = i, p = 0;
+                        while (v >= T.piece_cnt[p]) { v -= T.piece_cnt[p]; p++; }
+                        const int64_t e = T.piece_off[p] + v;
+                        gid = __ldg(a.pool + e);
+                        nrm = __ldg(a.pool_norm + e);
+                        bits = __ldg(a.pool_bits + e) << q0;
+                    } else {
+                        const int64_t r = T.base + T.row_begin + i;
+                        gid = __ldg(a.ix.M_ls + r);
+                        nrm = __ldg(a.tc_xn_ls + r);
+                        bits = T.bits_off >= 0 ? (__ldg(a.pool_bits + T.bits_off + i) << q0) : mine;
+                    }
+                }
+                const bool keep = bits != 0;
+                const unsigned m = __ballot_sync(FULL, keep);
+                int base = 0;
+                if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+                base = __shfl_sync(FULL, base, 0);
+                if (keep) {
+                    const int o = off + base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+                    a.pool[o] = gid;
+                    a.pool_norm[o] = nrm;
+                    a.pool_bits[o] = bits;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int pi = atomicAdd(&a.ctr->n_packed, 1);
+            Tile P;
+            P.base = 0;
+            P.seg = -1;
+            P.row_begin = 0;
+            P.row_end = s_cnt;
+            P.tile_in_seg = 0;
+            P.label = -1;
+            P.nq = s_q0[ng];
+            P.item_base = (int32_t)(a.packq_base + s_pq);
+            P.n_tiles = 1;
+            P.hs = 0;
+            P.bits_off = -1;
+            P.n_pieces = 1;
+            P.piece_off[0] = off;
+            P.piece_cnt[0] = s_cnt;
+            for (int i = 1; i < kMaxPieces; i++) { P.piece_off[i] = 0; P.piece_cnt[i] = 0; }
+            P.pad2[0] = P.pad2[1] = P.pad2[2] = 0;
+            const int t = a.max_tiles + pi;
+            a.tiles[t] = P;
+            const int c = tile_class(s_cnt);
+            a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = t;
+        }
+        __syncthreads();
+    }
+}
+
+int launch_pack(const SearchArgs &a, cudaStream_t s) {
+    if (!a.pack_list) return 0;
+    k_pack<<<148 * 4, kPackThreads, 0, s>>>(a);
+    return 1;
 }
 
 int launch_and_filter(const SearchArgs &a, cudaStream_t s) {

@@ -300,11 +300,13 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
         // the tile slot of its parity ahead of the producer, so no dependent global round trip sits
         // between one tile's last row stage and the next tile's first.
         uint32_t tc = 0;
-        const int ntiles = a.ctr->n_tiles;
         const bool by_cls = a.tile_cls != nullptr;          // longest tiles first (row-count classes)
         int cum[kTileClasses + 1];
         cum[0] = 0;
         for (int c = 0; c < kTileClasses; c++) cum[c + 1] = cum[c] + (by_cls ? a.ctr->n_tile_cls[c] : 0);
+        // with the claim lists every claimable tile is listed there (packed segments are not,
+        // their packed tile is)
+        const int ntiles = by_cls ? cum[kTileClasses] : a.ctr->n_tiles;
         TP_DECL
         for (;;) {
             const int tp = tc & 1;
@@ -434,9 +436,11 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                         mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
                         meta[slot] = make_int4(t, r0, nr, flags);
                         mbar_arrive_expect_tx(full + slot, (uint32_t)(ng * 4 * kpad) + 2 * b4n + b8n);
-                        tma_load_1d(dsid, a.pool + po, b4n, full + slot);
-                        tma_load_1d(dnorm, a.pool_norm + po, b4n, full + slot);
-                        tma_load_1d(dbits, a.pool_bits + po, b8n, full + slot);
+                        if (nr > 0) {
+                            tma_load_1d(dsid, a.pool + po, b4n, full + slot);
+                            tma_load_1d(dnorm, a.pool_norm + po, b4n, full + slot);
+                            tma_load_1d(dbits, a.pool_bits + po, b8n, full + slot);
+                        }
                     }
                     __syncwarp();
                     for (int q4 = lane; q4 < ng; q4 += 32) {
@@ -644,10 +648,11 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                         const ull key = ((ull)bits << 32) | (uint32_t)gid;
                         bool pass = valid && key < thrp[g];
                         if (pass) {
-                            const TcQMeta &qq = qm[g];
-                            if (qq.meta & META_PRED)
-                                pass = use_bits ? ((pbits >> g) & 1ull) != 0
-                                                : verify_pred_ol(ix, gid, a.qlab + qq.p_off, qq.nl, ti.label);
+                            // pass bits (pre-filter / packed tile: the row's own segment's queries
+                            // and their AND predicates), else the scan verifies the predicate itself
+                            if (use_bits) pass = ((pbits >> g) & 1ull) != 0;
+                            else if (qm[g].meta & META_PRED)
+                                pass = verify_pred_ol(ix, gid, a.qlab + qm[g].p_off, qm[g].nl, ti.label);
                         }
                         if (pass) D[(size_t)g * kTcRows + row] = bits;
                         const unsigned b = __ballot_sync(FULL, pass);

@@ -490,6 +490,11 @@ void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slo
     *gslots = pow2ceil((uint64_t)(2 * v_bound + 64));
 }
 
+static bool getenv_pack() {          // read per search (A/B tests toggle it)
+    const char *e = getenv("VF_PACK");
+    return e ? atoi(e) != 0 : true;
+}
+
 vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, const vf_search_params *p,
                       cudaStream_t s, Plan *out) {
     const DevIndex &D = ix->dev;
@@ -560,9 +565,15 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.pool = nullptr;
     a.pool_bits = nullptr;
     a.pool_norm = nullptr;
+    a.tc_xn = F.xn;
+    a.tc_xn_ls = F.xn_ls;
     a.pool_cap = 0;
     a.n_slots = n_slots;
     a.max_nl = ix->world > 1 ? kRecLabels : kMaxQueryLabels;
+    a.pack_list = nullptr;
+    a.pack_max_nq = 0;
+    a.pack_group = 0;
+    a.packq_base = 0;
     {
         const char *e = getenv("VF_TC_PARTS");
         a.tc_parts = e ? atoi(e) : 1;
@@ -580,7 +591,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
 
     bool fresh = false;
     VF_CUDA(sc->Qp.ensure((size_t)std::max<int64_t>(n, 1) * D.row_bytes));
-    if (pl.filter) {
+    if (pl.filter || (pl.tc && getenv_pack())) {
         int64_t cap = 64ll << 20;                       // 256 MB of survivor ids + 512 MB of pass bits
         if (const char *e = getenv("VF_POOL_CAP")) cap = std::max<int64_t>(1, atoll(e));   // overflow tests
         VF_CUDA(sc->pool.ensure((size_t)cap * 4));
@@ -588,7 +599,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
         VF_CUDA(sc->pool_norm.ensure((size_t)cap * 4));
         a.pool = sc->pool.as<int32_t>();
         a.pool_bits = sc->pool_bits.as<unsigned long long>();
-        a.pool_norm = D.xn ? sc->pool_norm.as<uint32_t>() : nullptr;
+        a.pool_norm = F.xn ? sc->pool_norm.as<uint32_t>() : nullptr;
         a.pool_cap = (int32_t)cap;
     }
     if (ix->enc8) {
@@ -602,9 +613,18 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     VF_CUDA(sc->item_ctr.ensure((size_t)slots * 12));
     VF_CUDA(sc->graph_list.ensure((size_t)slots * kGraphClasses * 4));
     VF_CUDA(sc->scan_slots.ensure((size_t)slots * 4));
-    VF_CUDA(sc->scan_q.ensure((size_t)slots * sizeof(ScanQuery)));
+    // tile packing (k_pack; VF_PACK=0 off): small single-tile segments of the tensor-core scan
+    pl.pack = pl.tc && getenv_pack() && pl.a.pool != nullptr;
+    VF_CUDA(sc->scan_q.ensure((size_t)slots * (pl.pack ? 2 : 1) * sizeof(ScanQuery)));
     VF_CUDA(sc->segs.ensure((size_t)slots * sizeof(Segment)));
-    VF_CUDA(sc->tiles.ensure((size_t)pl.max_tiles * sizeof(Tile)));
+    VF_CUDA(sc->tiles.ensure((size_t)(pl.max_tiles + (pl.pack ? slots : 0)) * sizeof(Tile)));
+    if (pl.pack) {
+        VF_CUDA(sc->pack_list.ensure((size_t)slots * 4));
+        a.pack_list = sc->pack_list.as<int32_t>();
+        a.pack_max_nq = std::max(1, pl.qg / 8);
+        a.pack_group = std::min(16, pl.qg / a.pack_max_nq);
+        a.packq_base = slots;
+    }
     VF_CUDA(sc->item_seg.ensure((size_t)slots * 4));
     VF_CUDA(sc->item_res.ensure((size_t)slots * k * 8));
     if (pl.multi) VF_CUDA(sc->partials.ensure((size_t)slots * a.max_tiles_per_label * k * 8));
@@ -684,6 +704,7 @@ vf_status run_route(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     }
     nl += launch_bucket(a, s, pl.n_slots, pl.qg);
     if (pl.filter) nl += launch_and_filter(a, s);
+    if (pl.pack) nl += launch_pack(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     VF_CUDA(cudaGetLastError());
     *launches += nl;

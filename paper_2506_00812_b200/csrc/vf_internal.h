@@ -153,6 +153,9 @@ struct Counters {
     int32_t filter_next;     // k_hs_filter tile cursor
     int32_t n_tile_cls[4];        // scan tiles per row-count class (kTileClasses; longest first)
     int32_t pool_used;       // survivor pool bump allocator
+    int32_t n_pack;          // small single-tile segments queued for packing (k_pack)
+    int32_t n_packed;        // packed tiles made
+    int32_t packq_used;      // query records copied for packed tiles
     int32_t n_invalid;       // queries rejected by the device-side offset / label-count check
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
@@ -215,12 +218,21 @@ struct SearchArgs {
     int32_t *pool;            // AND pre-filter survivor ids (k_and_filter)
     unsigned long long *pool_bits;  // ... and their per-query pass bits (bit g: query g of the tile)
     uint32_t *pool_norm;      // ... and their ||x||^2 (tensor-core scan; nullptr: none)
+    const uint32_t *tc_xn, *tc_xn_ls;   // ||x||^2 per point / X_LS row of the tensor-core scan's view
     int32_t pool_cap;
     // device-side validation of caller offsets (device label arrays are not read by the host): a
     // query whose labels fall outside [0, n_slots) or number more than max_nl gets an empty row
     // and is counted in ctr->n_invalid (vf_search_stats.n_invalid_queries)
     int64_t n_slots;
     int32_t max_nl;
+    // tile packing (k_pack): single-tile LS segments of <= pack_max_nq queries are queued in
+    // pack_list (instead of the claim lists) and packed pack_group at a time into one tile whose
+    // rows (ids, norms, per-query pass bits = "row belongs to my segment" & the AND pre-filter) are
+    // materialised in the pool; packed tiles live at tiles[max_tiles + i], their query records at
+    // scan_q[packq_base + j]. pack_list == nullptr: off.
+    int32_t *pack_list;
+    int32_t pack_max_nq, pack_group;
+    int64_t packq_base;
 };
 
 __device__ __forceinline__ bool gate_skip(const SearchArgs &a) {
@@ -236,6 +248,7 @@ int launch_scan(const SearchArgs &a, cudaStream_t s, int max_tiles_bound);   // 
 int launch_graph(const SearchArgs &a, cudaStream_t s, int graph_items_bound, int grid_ctas); // a3
 int launch_merge(const SearchArgs &a, cudaStream_t s);     // a5
 bool encode_row_map(void *map, const void *base, int row_bytes, int64_t n_rows, int cw, int box_rows);
+int launch_pack(const SearchArgs &a, cudaStream_t s);   // pack small scan segments (k_pack)
 int launch_and_filter(const SearchArgs &a, cudaStream_t s);  // AND pre-filter of HS scan tiles
 // a2 on tcgen05 (scan_tc.cu): u8 indexes; tensor maps encoded once per index
 int scan_tc_qg(int row_bytes, int k);

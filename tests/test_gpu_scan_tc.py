@@ -309,3 +309,24 @@ def test_and_prefilter_wide_label_union(vf):
         a, ad = g.search(Q, qoff, qlab, k=k, itopk=16, op="and")
         e, ed = o.exact_knn(Q, qoff, qlab, k=k, op="and")
         assert (a == e).all() and (ad == ed.astype(np.float32)).all(), k
+
+
+@pytest.mark.parametrize("mode", ["single", "mix_and", "and2"])
+def test_tile_packing_is_exact(vf, monkeypatch, mode):
+    """k_pack: small single-tile segments share one tensor-core tile (rows carry their own
+    segment's pass bits). Results bit-identical with packing off and on, and to the oracle."""
+    from workload import gen
+    cfg, X, off, ids, go, gi = small_random_index(seed=51, N=20000, D=192, L=60, F=4.0, T=1500, R=8, dtype="u8")
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=600)
+    qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=600, mode=mode)
+    op = "single" if mode == "single" else "and"
+    res = {}
+    for pack in ("0", "1"):
+        monkeypatch.setenv("VF_PACK", pack)
+        res[pack] = g.search(Q, qoff, qlab, k=10, itopk=32, op=op)
+        assert g.last_stats()["n_scan_items"] > 100
+    assert (res["0"][0] == res["1"][0]).all() and (res["0"][1] == res["1"][1]).all()
+    e, ed = o.search(Q, qoff, qlab, k=10, itopk=32, op=op)
+    assert (res["1"][0] == e).all() and (res["1"][1] == ed.astype(np.float32)).all()
