@@ -507,61 +507,81 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
 // rows (reading #50). One CTA per group.
 constexpr int kPackThreads = 256;
 constexpr int kPackMaxGroup = 16;
+constexpr int kPackRows = 1024;      // a segment with more rows (after the pre-filter) stays alone;
+                                     // a packed tile closes once it holds this many rows
+
+// rows of a (pre-filtered) tile
+__device__ __forceinline__ int tile_rows_now(const Tile &T) {
+    if (T.n_pieces < 0) return T.row_end - T.row_begin;
+    int r = 0;
+    for (int p = 0; p < T.n_pieces; p++) r += T.piece_cnt[p];
+    return r;
+}
+
+__device__ __forceinline__ void list_tile(const SearchArgs &a, int t, int rows) {
+    const int c = tile_class(rows);
+    a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = t;
+}
 
 __global__ void __launch_bounds__(kPackThreads) k_pack(SearchArgs a) {
     __shared__ Tile st[kPackMaxGroup];
+    __shared__ int s_idx[kPackMaxGroup], s_rows[kPackMaxGroup];
     __shared__ int s_q0[kPackMaxGroup + 1], s_r0[kPackMaxGroup + 1];
-    __shared__ int s_off, s_cnt, s_pq, s_ok;
+    __shared__ int s_pack[kPackMaxGroup];        // packed tile (0..) of each sub, -1 alone
+    __shared__ int s_off[kPackMaxGroup], s_cnt[kPackMaxGroup], s_pq[kPackMaxGroup], s_nq[kPackMaxGroup];
+    __shared__ int s_npk;
     const int n_pack = a.ctr->n_pack;
     const int G = a.pack_group;
     const int n_groups = (n_pack + G - 1) / G;
     for (int gidx = blockIdx.x; gidx < n_groups; gidx += gridDim.x) {
         const int i0 = gidx * G, ng = min(G, n_pack - i0);
-        if (threadIdx.x < ng) st[threadIdx.x] = a.tiles[a.pack_list[i0 + threadIdx.x]];
+        if (threadIdx.x < ng) {
+            s_idx[threadIdx.x] = a.pack_list[i0 + threadIdx.x];
+            st[threadIdx.x] = a.tiles[s_idx[threadIdx.x]];
+            s_rows[threadIdx.x] = tile_rows_now(st[threadIdx.x]);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            int q = 0, r = 0;
+            // consecutive subs of <= kPackRows rows fill packed tiles up to kPackRows rows and the
+            // scan's query capacity; bigger subs stay tiles of their own
+            int npk = 0, q = 0, r = 0;
             for (int s = 0; s < ng; s++) {
+                if (s_rows[s] > kPackRows) { s_pack[s] = -1; continue; }
+                if (npk == 0 || q + st[s].nq > a.pack_max_nq * G || r >= kPackRows) {
+                    if (npk > 0) { s_nq[npk - 1] = q; s_cnt[npk - 1] = r; }
+                    npk++; q = 0; r = 0;
+                }
+                s_pack[s] = npk - 1;
                 s_q0[s] = q;
                 s_r0[s] = r;
                 q += st[s].nq;
-                int rows = st[s].row_end - st[s].row_begin;
-                if (st[s].n_pieces >= 0) {
-                    rows = 0;
-                    for (int p = 0; p < st[s].n_pieces; p++) rows += st[s].piece_cnt[p];
-                }
-                r += rows;
+                r += s_rows[s];
             }
-            s_q0[ng] = q;
-            s_r0[ng] = r;
-            const int off = atomicAdd(&a.ctr->pool_used, (r + 3) & ~3);
-            s_ok = q <= 64 && (int64_t)off + r <= a.pool_cap;
-            s_off = off;
-            s_cnt = 0;
-            s_pq = s_ok ? atomicAdd(&a.ctr->packq_used, q) : 0;
+            if (npk > 0) { s_nq[npk - 1] = q; s_cnt[npk - 1] = r; }
+            for (int p2 = 0; p2 < npk; p2++) {
+                const int off = atomicAdd(&a.ctr->pool_used, (s_cnt[p2] + 3) & ~3);
+                const bool ok = s_nq[p2] <= 64 && (int64_t)off + s_cnt[p2] <= a.pool_cap;
+                s_off[p2] = ok ? off : -1;
+                s_pq[p2] = ok ? atomicAdd(&a.ctr->packq_used, s_nq[p2]) : 0;
+                s_cnt[p2] = 0;                                  // rows written so far
+            }
+            for (int s = 0; s < ng; s++)                        // alone, or no room: its own tile
+                if (s_pack[s] < 0 || s_off[s_pack[s]] < 0) {
+                    list_tile(a, s_idx[s], s_rows[s]);
+                    s_pack[s] = -1;
+                }
+            s_npk = npk;
         }
         __syncthreads();
-        if (!s_ok) {
-            // no room: the segments stay tiles of their own (claimed like any other)
-            if (threadIdx.x < ng) {
-                const int t = a.pack_list[i0 + threadIdx.x];
-                const int c = tile_class(st[threadIdx.x].row_end - st[threadIdx.x].row_begin);
-                a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = t;
-            }
-            __syncthreads();
-            continue;
-        }
-        // query records side by side
-        for (int s = 0; s < ng; s++)
-            for (int g = threadIdx.x; g < st[s].nq; g += kPackThreads)
-                a.scan_q[a.packq_base + s_pq + s_q0[s] + g] = a.scan_q[st[s].item_base + g];
-        // rows: compacted survivors, or every row of the label (with per-row AND bits if any)
-        const int off = s_off;
         for (int s = 0; s < ng; s++) {
+            const int pk = s_pack[s];
+            if (pk < 0) continue;
             const Tile &T = st[s];
             const int q0 = s_q0[s];
+            for (int g = threadIdx.x; g < T.nq; g += kPackThreads)        // query records side by side
+                a.scan_q[a.packq_base + s_pq[pk] + q0 + g] = a.scan_q[T.item_base + g];
             const unsigned long long mine = (T.nq >= 64 ? ~0ull : ((1ull << T.nq) - 1)) << q0;
-            const int nrows = s_r0[s + 1] - s_r0[s];
+            const int nrows = s_rows[s];
             for (int i0r = 0; i0r < nrows; i0r += kPackThreads) {
                 const int i = i0r + threadIdx.x;
                 int32_t gid = -1;
@@ -585,10 +605,10 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(SearchArgs a) {
                 const bool keep = bits != 0;
                 const unsigned m = __ballot_sync(FULL, keep);
                 int base = 0;
-                if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+                if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&s_cnt[pk], __popc(m));
                 base = __shfl_sync(FULL, base, 0);
                 if (keep) {
-                    const int o = off + base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+                    const int o = s_off[pk] + base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
                     a.pool[o] = gid;
                     a.pool_norm[o] = nrm;
                     a.pool_bits[o] = bits;
@@ -596,29 +616,29 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(SearchArgs a) {
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x < s_npk && s_off[threadIdx.x] >= 0) {
+            const int pk = threadIdx.x;
             const int pi = atomicAdd(&a.ctr->n_packed, 1);
             Tile P;
             P.base = 0;
             P.seg = -1;
             P.row_begin = 0;
-            P.row_end = s_cnt;
+            P.row_end = s_cnt[pk];
             P.tile_in_seg = 0;
             P.label = -1;
-            P.nq = s_q0[ng];
-            P.item_base = (int32_t)(a.packq_base + s_pq);
+            P.nq = s_nq[pk];
+            P.item_base = (int32_t)(a.packq_base + s_pq[pk]);
             P.n_tiles = 1;
             P.hs = 0;
             P.bits_off = -1;
             P.n_pieces = 1;
-            P.piece_off[0] = off;
-            P.piece_cnt[0] = s_cnt;
+            P.piece_off[0] = s_off[pk];
+            P.piece_cnt[0] = s_cnt[pk];
             for (int i = 1; i < kMaxPieces; i++) { P.piece_off[i] = 0; P.piece_cnt[i] = 0; }
             P.pad2[0] = P.pad2[1] = P.pad2[2] = 0;
             const int t = a.max_tiles + pi;
             a.tiles[t] = P;
-            const int c = tile_class(s_cnt);
-            a.tile_cls[(int64_t)c * a.max_tiles + atomicAdd(&a.ctr->n_tile_cls[c], 1)] = t;
+            list_tile(a, t, s_cnt[pk]);
         }
         __syncthreads();
     }

@@ -621,8 +621,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     if (pl.pack) {
         VF_CUDA(sc->pack_list.ensure((size_t)slots * 4));
         a.pack_list = sc->pack_list.as<int32_t>();
-        a.pack_max_nq = std::max(1, pl.qg / 8);
-        a.pack_group = std::min(16, pl.qg / a.pack_max_nq);
+        a.pack_max_nq = std::max(1, pl.qg / 8);                 // segments of <= qg/8 queries
+        a.pack_group = std::min(16, pl.qg / a.pack_max_nq);     // <= qg queries per packed tile
         a.packq_base = slots;
     }
     VF_CUDA(sc->item_seg.ensure((size_t)slots * 4));
