@@ -264,6 +264,9 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
     const size_t stage_bytes = (size_t)kTcRows * kpad;
     if (gate_skip(a)) return;     // a batch outside the exact range runs k_scan instead
     if (threadIdx.x == 0) atomicMax(&a.ctr->scan_t0_inv, ~gtimer());
+#ifdef VF_TC_PROF
+    const unsigned long long cta_t0 = gtimer();
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < nst; i++) {
@@ -859,6 +862,9 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(SL.tmem_cols));
     }
     if (threadIdx.x == 0) atomicMax(&a.ctr->scan_t1, gtimer());
+#ifdef VF_TC_PROF
+    if (threadIdx.x == 0) printf("TCCTA %d start %llu end %llu\n", blockIdx.x, cta_t0, gtimer());
+#endif
 }
 
 // ---------------------------------------------------------------- row norms (build time)
