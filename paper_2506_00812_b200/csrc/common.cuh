@@ -112,8 +112,29 @@ static __device__ __noinline__ bool verify_pred_x(const int64_t *__restrict__ pt
     return true;
 }
 
+// 8-byte load that asks L2 to keep the line (the signatures are re-read by every AND item)
+__device__ __forceinline__ unsigned long long ld_keep(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile(
+        "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+        "ld.global.nc.L2::cache_hint.u64 %0, [%1], pol;\n}\n"
+        : "=l"(v) : "l"(p));
+    return v;
+}
+
+// the labels' signature bits all set in the point's signature (else: certainly not a member)
+__device__ __forceinline__ bool sig_may_have(unsigned long long sig, unsigned long long need) {
+    return (sig & need) == need;
+}
+
 __device__ __forceinline__ bool verify_pred(const DevIndex &ix, int32_t gid, const int32_t *P, int np,
                                             int32_t excl) {
+    if (ix.lsig) {
+        unsigned long long need = 0;
+        for (int t = 0; t < np; t++)
+            if (P[t] != excl) need |= label_sig_bits(P[t]);
+        if (!sig_may_have(ld_keep(ix.lsig + gid), need)) return false;
+    }
     return verify_pred_x(ix.pt_off, ix.pt_lab, ix.lbits, ix.lbit_slot, ix.lbit_words, ix.n_labels, gid, P, np, excl);
 }
 

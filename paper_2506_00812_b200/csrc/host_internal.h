@@ -112,7 +112,7 @@ struct vf_index_impl;
 struct vf_index {
     vf::DevIndex dev{};
     int device = 0;
-    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev, xn, xn_ls, X8, Xls8, lbits, lbit_slot;
+    vf::DevBuf X, dir, G, M_hs, Xls, M_ls, pt_off, pt_lab, owner_dev, xn, xn_ls, X8, Xls8, lbits, lbit_slot, lsig;
     bool enc8 = false;                          // lossless u8 row store of integer-valued fp32 rows
     vf::DevIndex dev8{};                        // ... and the u8 view the fast kernels read
     alignas(64) unsigned char tm_ls[128];       // CUtensorMap of X_LS (tensor-core scan)

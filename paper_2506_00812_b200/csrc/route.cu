@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
     __shared__ const int32_t *s_pl[kFiltUnion];   // ... else its posting list on this rank (ascending ids)
     __shared__ int32_t s_pn[kFiltUnion];          // ... and its length (0: not on this rank -> label list)
     __shared__ int s_allbits;                     // no s_u label needs the point's label list
+    __shared__ unsigned long long s_sig[kFiltUnion];   // signature bits of each s_u label
     const int ntiles = a.ctr->n_tiles;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&a.ctr->filter_next, 1);
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                 const bool known = l >= 0 && l < a.ix.n_labels;
                 const int sl = (known && a.ix.lbit_slot) ? a.ix.lbit_slot[l] : -1;
                 s_slot[j] = (int16_t)sl;
+                s_sig[j] = label_sig_bits(l);
                 s_pn[j] = 0;
                 s_pl[j] = nullptr;
                 if (sl < 0 && known) {
@@ -371,13 +373,18 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                 if (allbits) {
                     // membership bitmaps (one bit read per (row, label), independent loads) and
                     // binary searches in the short posting lists of labels without one
+                    unsigned long long sg[kFiltRows];
+#pragma unroll
+                    for (int u = 0; u < kFiltRows; u++) sg[u] = gid[u] >= 0 && a.ix.lsig ? ld_keep(a.ix.lsig + gid[u]) : ~0ull;
 #pragma unroll
                     for (int u = 0; u < kFiltRows; u++) {
                         lb[u] = 0;
                         if (gid[u] < 0) continue;
                         for (int j = 0; j < nu; j++) {
                             bool in;
-                            if (s_slot[j] >= 0) {
+                            if (!sig_may_have(sg[u], s_sig[j])) {
+                                in = false;                 // the signature rules the label out
+                            } else if (s_slot[j] >= 0) {
                                 in = has_label_bit(a.ix, s_slot[j], gid[u]);
                             } else {
                                 const int32_t *pl = s_pl[j];

@@ -402,6 +402,12 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                 for (int i = 0; i < tl.n_pieces; i++) total += tl.piece_cnt[i];
             }
             const int nstage = max(1, (total + kTcRows - 1) / kTcRows);
+#ifdef VF_TC_PROF
+            if (lane == 0 && nstage > 40)
+                printf("TCBIG blk %d tile %d stages %d rows %d..%d pieces %d bits %d hs %d nq %d label %d ntiles %d\n",
+                       blockIdx.x, t, nstage, tl.row_begin, tl.row_end, tl.n_pieces, tl.bits_off, tl.hs, nq, tl.label,
+                       tl.n_tiles);
+#endif
             for (int si = 0; si < nstage; si++) {
                 const int v0 = si * kTcRows;
                 const int r0 = tl.row_begin + v0;

@@ -268,6 +268,14 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     VF_B(cudaMemcpy(ix->pt_off.p, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice));
     VF_B(ix->pt_lab.ensure(plab.size() * 4));
     VF_B(cudaMemcpy(ix->pt_lab.p, plab.data(), plab.size() * 4, cudaMemcpyHostToDevice));
+    {
+        // per-point label signatures (the predicate's negative fast path, DevIndex::lsig)
+        std::vector<unsigned long long> sig((size_t)std::max<int64_t>(N, 1), 0ull);
+        for (int64_t i = 0; i < N; i++)
+            for (int64_t e = poff[i]; e < poff[i + 1]; e++) sig[(size_t)i] |= label_sig_bits(plab[e]);
+        VF_B(ix->lsig.ensure(sig.size() * 8));
+        VF_B(cudaMemcpy(ix->lsig.p, sig.data(), sig.size() * 8, cudaMemcpyHostToDevice));
+    }
     // -- membership bitmaps of the largest labels (predicate fast path): labels with
     // |C_l| >= N / VF_BITMAP_DENSITY (default 1024: a bitmap is at most 32x its posting list), at most
     // kMaxBitmaps of them, largest first. 0 disables them. HBM is plentiful (YFCC-shaped: ~860
@@ -326,6 +334,7 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     D.lbits = n_bitmaps ? ix->lbits.as<uint32_t>() : nullptr;
     D.lbit_slot = n_bitmaps ? ix->lbit_slot.as<int16_t>() : nullptr;
     D.lbit_words = lbit_words;
+    D.lsig = ix->lsig.as<unsigned long long>();
     D.owner = owner.empty() ? nullptr : ix->owner_dev.as<int32_t>();
     D.rank = rank;
     D.world = world;
@@ -364,7 +373,8 @@ static vf_status build_one(const vf_build_desc *d, int world, int rank, const st
     I.bytes_map_hs = hs_rows * 4;
     I.bytes_ls_vectors = ls_rows_pad * row_bytes;
     I.bytes_map_ls = (ls_rows_pad + 4) * 4;
-    I.bytes_predicate = (N + 1) * 8 + n_entries * 4 + (n_bitmaps ? n_bitmaps * lbit_words * 4 + (int64_t)L * 2 : 0);
+    I.bytes_predicate = (N + 1) * 8 + n_entries * 4 + (n_bitmaps ? n_bitmaps * lbit_words * 4 + (int64_t)L * 2 : 0) +
+                        N * 8;   // + label signatures
     I.bytes_directory = (int64_t)L * sizeof(LabelDir) + (owner.empty() ? 0 : (int64_t)L * 4);
     I.bytes_norms = tc_rows ? (N + (int64_t)m_ls.size()) * 4 : 0;
     I.bytes_u8_store = enc8 ? (N + ls_rows_pad) * row_bytes8 : 0;

@@ -57,6 +57,10 @@ struct DevIndex {
                            // fast path: P ⊆ L_x tested bit by bit; identical answers to pt_lab)
     const int16_t *lbit_slot;  // [n_labels] bitmap of a label, -1 = none
     int64_t lbit_words;
+    // [n_points] 64-bit label signature of each point: bits h1(l), h2(l) of every label l of the
+    // point (label_sig_bits). A label whose bits are not all set is certainly not a label of the
+    // point: the predicate's negative fast path (one 8-B read, kept in L2), exact checks after it
+    const unsigned long long *lsig;
     const int32_t *owner;  // [n_labels] owning rank of each label (label sharding, §8(e)); NULL = all local
     const uint32_t *xn;    // [n_points] ||x||^2 (u8: exact int32) for the tensor-core scan's expansion
     const uint32_t *xn_ls; // [ls_rows_pad + 4] ||x||^2 of the X_LS rows
@@ -138,6 +142,13 @@ struct ScanQuery {
     int32_t nl;
     int32_t pad[2];
 };
+
+// The two signature bits of a label (vf_build_index builds the per-point signatures with it).
+__host__ __device__ __forceinline__ unsigned long long label_sig_bits(int32_t l) {
+    uint32_t h = (uint32_t)l * 0x9E3779B1u;
+    h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+    return (1ull << (h & 63)) | (1ull << ((h >> 8) & 63));
+}
 
 // Device counters, zeroed at the start of every search.
 struct Counters {
