@@ -4,6 +4,7 @@
 // step of the search runs in the CUDA kernels of this directory. Label sharding (§8(e)) is in
 // shard.cpp.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -511,8 +512,16 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     const int R = D.R, k = p->k;
     const int w = p->search_width < 1 ? 1 : p->search_width;
     // labels the scan may stream: LS lists, or every list in exact mode / with f3 AND routing
-    const int scan_max = (p->exact || p->and_scan_threshold > 0 || p->scan_threshold > D.T) ? ix->max_label_size
-                                                                                           : ix->max_ls_size;
+    // labels the scan may stream: LS lists; every list in exact mode / with T' > T; with f3 AND
+    // routing an HS l* whose AND set is estimated below the threshold: est >= |C_l*|^2 / N (the
+    // other labels are at least as large), so |C_l*| < sqrt(threshold * N) bounds those lists
+    int scan_max = ix->max_ls_size;
+    if (p->exact || p->scan_threshold > D.T) {
+        scan_max = ix->max_label_size;
+    } else if (p->and_scan_threshold > 0) {
+        const double b = std::ceil(std::sqrt((double)p->and_scan_threshold * (double)D.n_points)) + 1.0;
+        scan_max = std::max(scan_max, (int)std::min<double>(ix->max_label_size, b));
+    }
     // row tiles: small in the normal path (load balance across SMs; a label split over several
     // tiles is finalised in-kernel), large in exact mode (<= 256 tiles per label)
     // (the tensor-core scan finalises a label split over tiles with a grid-wide fence and a merge,
