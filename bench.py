@@ -759,7 +759,7 @@ def main():
                      "note": ("kernel_ms_per_launch: CUDA events of the kernel's phase on its stream, mean of the K "
                               "timed steps (scan and graph overlap, so it includes waiting for SMs); "
                               "kernel_active_ms: %globaltimer span of the kernel's CTAs in the last step")},
-        "phases_ms": {**{p: s0[f"mean_ms_{p}"] for p in ("route", "scan", "graph", "merge", "copy", "total")},
+        "phases_ms": {**{p: s0[f"mean_ms_{p}"] for p in ("route", "filter", "scan", "graph", "merge", "copy", "total")},
                       "steps_averaged": s0["n_profiled"]},
         "work": {kk: s0[kk] for kk in ("n_items", "n_scan_items", "n_graph_items", "n_segments",
                                        "scan_rows", "graph_V", "graph_E", "graph_iterations", "graph_V_max")},

@@ -281,6 +281,9 @@ typedef struct {
     int64_t n_invalid_queries;
     /* AND pre-filter (k_and_filter): survivor / pass-bit words used in its pool (diagnostics) */
     int64_t prefilter_words;
+    /* scan items' bucketing + AND pre-filter + tile packing (k_segments .. k_pack), between routing
+     * (ms_route = k_prepare) and the scan kernels (ms_scan); last search and mean */
+    double ms_filter, mean_ms_filter;
 } vf_search_stats;
 
 vf_status vf_set_profiling(vf_index *index, int32_t enable);

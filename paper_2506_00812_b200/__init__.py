@@ -90,7 +90,8 @@ class SearchStats(C.Structure):
                [("kernel_launches", C.c_int32), ("row_bytes", C.c_int32), ("n_profiled", C.c_int64)] + \
                [(n, C.c_double) for n in ("mean_ms_route", "mean_ms_scan", "mean_ms_graph", "mean_ms_merge",
                                           "mean_ms_copy", "mean_ms_total", "ms_scan_active", "ms_graph_active")] + \
-               [("n_invalid_queries", C.c_int64), ("prefilter_words", C.c_int64)]
+               [("n_invalid_queries", C.c_int64), ("prefilter_words", C.c_int64)] + \
+               [("ms_filter", C.c_double), ("mean_ms_filter", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

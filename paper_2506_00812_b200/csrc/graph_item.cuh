@@ -189,11 +189,10 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
         __syncwarp();
         if (nc > RP * GROUP) {
             // more rows than one load group: put every row's 128-byte lines in flight to L2 now,
-            // so the later groups do not each pay a full DRAM round trip
-            const int lines = (row_bytes + 127) >> 7;
-            for (int e = lane; e < nc * lines; e += 32) {
-                const int r = e / lines, l = e - r * lines;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ix.X + (int64_t)fgid[r] * row_bytes + l * 128));
+            // so the later groups do not each pay a full DRAM round trip (one row per lane)
+            if (lane < nc) {
+                const uint8_t *rp = ix.X + (int64_t)fgid[lane] * row_bytes;
+                for (int l = 0; l < row_bytes; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + l));
             }
         }
         for (int p0 = 0; p0 < nc; p0 += RP * GROUP) {
@@ -298,10 +297,35 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
             __syncwarp();
             return;
         }
-        if (ns == 1) {
-            ck = __shfl_sync(FULL, ck, __ffs(sm) - 1);
-            if (lane == 0) cbuf[0] = ck;
-        } else {
+        if (ns <= 4) {
+            // few survivors into a long Top: insert each in place -- its position by ballots over
+            // the sorted list, then only the tail behind it moves up one slot (top chunk first)
+            unsigned rem = sm;
+            while (rem) {
+                const ull kk = __shfl_sync(FULL, ck, __ffs(rem) - 1);
+                rem &= rem - 1;
+                int pos = 0;
+                for (int b = 0; b < ntop; b += 32) {
+                    const unsigned lt = __ballot_sync(FULL, b + lane < ntop && cur[b + lane] < kk);
+                    pos += __popc(lt);
+                    if (lt != FULL) break;                  // the rest of the sorted list is larger
+                }
+                if (pos >= M) continue;                      // beaten by earlier insertions
+                const int last = min(ntop, M - 1);           // [pos, last) -> [pos + 1, last + 1)
+                for (int hi = last; hi > pos; hi -= 32) {
+                    const int i = max(pos, hi - 32) + lane;
+                    const ull v = i < hi ? cur[i] : 0ull;
+                    __syncwarp();
+                    if (i < hi) cur[i + 1] = v;
+                    __syncwarp();
+                }
+                if (lane == 0) cur[pos] = kk;
+                ntop = min(M, ntop + 1);
+                __syncwarp();
+            }
+            return;
+        }
+        {
             ck = warp_sort32(ck, lane);
             cbuf[lane] = ck;
         }

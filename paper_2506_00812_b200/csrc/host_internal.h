@@ -76,7 +76,7 @@ struct Scratch {
     // the mean over every search since profiling was enabled (<= kProfRing of them) is readable
     // without a host sync between searches
     static constexpr int kProfRing = 64;
-    cudaEvent_t evs[kProfRing][8];
+    cudaEvent_t evs[kProfRing][9];
     cudaEvent_t *ev = evs[0];
     int64_t prof_n = 0, prof_first = 0;
     bool ev_ok = false;

@@ -707,7 +707,8 @@ vf_status run_local(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
     return run_compute(ix, sc, pl, s, launches);
 }
 
-// a1 (+ the AND pre-filter): everything up to the scan / graph fork
+// a1: routing (items, graph lists); the bucketing and pre-filter of the scan items run in
+// run_compute, concurrently with the graph kernels
 vf_status run_route(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const uint8_t *recv, int64_t n_recv,
                     int rec_bytes, int *launches) {
     SearchArgs &a = pl.a;
@@ -721,9 +722,6 @@ vf_status run_route(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, const u
         if (pl.clear_items && pl.n_slots > 0) VF_CUDA(cudaMemsetAsync(a.items, 0, (size_t)pl.n_slots * sizeof(Item), s));
         nl += launch_prepare(a, s);
     }
-    nl += launch_bucket(a, s, pl.n_slots, pl.qg);
-    if (pl.filter) nl += launch_and_filter(a, s);
-    if (pl.pack) nl += launch_pack(a, s);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[2], s));
     VF_CUDA(cudaGetLastError());
     *launches += nl;
@@ -773,8 +771,10 @@ vf_status run_compute(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, int *
     }
     fast.gate = pl.checked ? 1 : 0;
     slow.gate = 2;
-    static const int graph_first_env = [] { const char *e = getenv("VF_GRAPH_FIRST"); return e ? atoi(e) : 0; }();
-    static const int graph_per_sm_env = [] { const char *e = getenv("VF_GRAPH_PER_SM"); return e ? atoi(e) : 0; }();
+    // read per search (A/B: scripts/ab_env.py)
+    const char *gf_e = getenv("VF_GRAPH_FIRST"), *gps_e = getenv("VF_GRAPH_PER_SM");
+    const int graph_first_env = gf_e ? atoi(gf_e) : 0;
+    const int graph_per_sm_env = gps_e ? atoi(gps_e) : 0;
     auto launch_scans = [&]() -> int {
         int sl = pl.tc ? launch_scan_tc(fast, ss, tb, ix->tm_ls, ix->tm_x, overlap ? tc_ctas_env : 0)
                        : launch_scan(fast, ss, tb);
@@ -799,11 +799,17 @@ vf_status run_compute(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, int *
         }
         return gl;
     };
+    // the scan items' bucketing, AND pre-filter and packing run on the scan stream: with overlap
+    // they proceed while the graph kernels (launched first when VF_GRAPH_FIRST=1) search
     int gl = 0;
     if (overlap && graph_first_env) {
         gl = launch_graphs();
         if (gl < 0) return fail(VF_ERR_INTERNAL, "graph kernel dispatch failed");
     }
+    nl += launch_bucket(a, ss, pl.n_slots, pl.qg);
+    if (pl.filter) nl += launch_and_filter(a, ss);
+    if (pl.pack) nl += launch_pack(a, ss);
+    if (prof) VF_CUDA(cudaEventRecord(sc->ev[8], ss));
     const int sl = launch_scans();
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
@@ -978,6 +984,7 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
         if (prof) {
             VF_CUDA(cudaEventRecord(sc->ev[1], s));
             VF_CUDA(cudaEventRecord(sc->ev[2], s));
+            VF_CUDA(cudaEventRecord(sc->ev[8], s));
             VF_CUDA(cudaEventRecord(sc->ev[3], s));
         }
         // a small batch spreads each query over several CTAs (scan items split by rows, graph items
@@ -1049,10 +1056,12 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
     st->ms_scan_active = span(c.scan_t0_inv, c.scan_t1);
     st->ms_graph_active = span(c.graph_t0_inv, c.graph_t1);
     // with scan / graph overlap the graph phase runs from the fork (ev[2]) to its own end (ev[7])
+    // route = k_prepare; filter = bucket + AND pre-filter + packing; scan = the scan kernels
     auto phases = [](cudaEvent_t *e, bool ov, double *out) {
         float t;
         cudaEventElapsedTime(&t, e[1], e[2]); out[0] = t;
-        cudaEventElapsedTime(&t, e[2], e[3]); out[1] = t;
+        cudaEventElapsedTime(&t, e[8], e[3]); out[1] = t;
+        cudaEventElapsedTime(&t, e[2], e[8]); out[6] = t;
         cudaEventElapsedTime(&t, ov ? e[2] : e[3], ov ? e[7] : e[4]); out[2] = t;
         cudaEventElapsedTime(&t, e[4], e[5]); out[3] = t;
         float c0, c1;
@@ -1062,21 +1071,22 @@ extern "C" vf_status vf_get_last_stats(vf_index *ix, void *cuda_stream, vf_searc
         cudaEventElapsedTime(&t, e[0], e[6]); out[5] = t;
     };
     if (sc->profiled && sc->prof_n > 0) {
-        double v[6];
+        double v[7];
         phases(sc->evs[(sc->prof_n - 1) % Scratch::kProfRing], sc->evov[(sc->prof_n - 1) % Scratch::kProfRing], v);
         st->ms_route = v[0]; st->ms_scan = v[1]; st->ms_graph = v[2];
-        st->ms_merge = v[3]; st->ms_copy = v[4]; st->ms_total = v[5];
+        st->ms_merge = v[3]; st->ms_copy = v[4]; st->ms_total = v[5]; st->ms_filter = v[6];
         const int64_t lo = std::max(sc->prof_first, sc->prof_n - Scratch::kProfRing);
-        double sum[6] = {0, 0, 0, 0, 0, 0};
+        double sum[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int64_t i = lo; i < sc->prof_n; i++) {
             phases(sc->evs[i % Scratch::kProfRing], sc->evov[i % Scratch::kProfRing], v);
-            for (int j = 0; j < 6; j++) sum[j] += v[j];
+            for (int j = 0; j < 7; j++) sum[j] += v[j];
         }
         const int64_t m = sc->prof_n - lo;
         st->n_profiled = m;
         if (m > 0) {
             st->mean_ms_route = sum[0] / m; st->mean_ms_scan = sum[1] / m; st->mean_ms_graph = sum[2] / m;
             st->mean_ms_merge = sum[3] / m; st->mean_ms_copy = sum[4] / m; st->mean_ms_total = sum[5] / m;
+            st->mean_ms_filter = sum[6] / m;
         }
     }
     return VF_OK;

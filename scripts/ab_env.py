@@ -45,8 +45,9 @@ def main():
     kw = dict(k=c.k, itopk=a.itopk, search_width=a.w, op=op, and_scan_threshold=a.and_scan, stream=s,
               n_query_labels=int(w.q_off[-1]))
     for setting in a.settings:
-        name, val = setting.split("=")
-        os.environ[name] = val
+        pairs = [kv.split("=") for kv in setting.split(",")]      # NAME=V[,NAME=V...]
+        for name, val in pairs:
+            os.environ[name] = val
         for _ in range(a.warmup):
             ix.search_into(Q, qo, ql, ids, dd, **kw)
         evs = []
@@ -61,9 +62,11 @@ def main():
         st = ix.last_stats(s)
         ms = float(np.median([e0.elapsed_time(e1) for e0, e1 in evs]))
         chk = int(ids.sum().item())
-        print(f"{setting:22s} step {ms:8.3f} ms  QPS {n / ms * 1e3 / 1e6:7.2f}M  route {st['ms_route']:.3f} "
-              f"scan {st['ms_scan']:.3f} graph {st['ms_graph']:.3f}  checksum {chk}", flush=True)
-        del os.environ[name]
+        print(f"{setting:40s} step {ms:8.3f} ms  QPS {n / ms * 1e3 / 1e6:7.2f}M  route {st['ms_route']:.3f} "
+              f"filter {st['ms_filter']:.3f} scan {st['ms_scan']:.3f} graph {st['ms_graph']:.3f}  checksum {chk}",
+              flush=True)
+        for name, _ in pairs:
+            del os.environ[name]
 
 
 if __name__ == "__main__":
