@@ -37,7 +37,8 @@ struct vf_server {
 
 namespace vf {
 // visited-set geometry of one beam search (the same sizing as plan_search)
-void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slots, uint64_t *gslots);
+void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slots, uint64_t *gslots,
+                int warp_bytes);
 }
 
 using namespace vf;
@@ -86,7 +87,7 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
     a.and_scan_thr = p->and_scan_threshold;
     a.scan_thr = std::max(ix->dev.T, p->scan_threshold);
     uint64_t gslots = 0;
-    beam_sizes(p->itopk, w, ix->dev.R, a.n_init, a.max_iter, &a.hash_slots, &gslots);
+    beam_sizes(p->itopk, w, ix->dev.R, a.n_init, a.max_iter, &a.hash_slots, &gslots, 7168);
     a.gtab_slots = (int64_t)gslots;
     a.chk_lo = ix->chk_lo;
     a.chk_hi = ix->chk_hi;

@@ -492,9 +492,10 @@ namespace vf {
 
 // Visited-set geometry of one beam search: a shared-memory table within ~7 KB per warp and an exact
 // global overflow table large enough for every vertex the search can visit.
-void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slots, uint64_t *gslots) {
+void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slots, uint64_t *gslots,
+                int warp_bytes) {
     int hs = 1024;
-    const int64_t budget = 7168 - 16ll * itopk - 1024;
+    const int64_t budget = (int64_t)warp_bytes - 16ll * itopk - 1024;
     while (hs < 64 * itopk && hs < 8192 && (int64_t)hs * 2 * 4 <= budget) hs <<= 1;
     const int64_t v_bound = (int64_t)n_init + (int64_t)max_iter * w * R + 32;
     *hash_slots = hs;
@@ -505,6 +506,8 @@ static bool getenv_pack() {          // read per search (A/B tests toggle it)
     const char *e = getenv("VF_PACK");
     return e ? atoi(e) != 0 : true;
 }
+
+int graph_warp_kb_default(int itopk) { return itopk >= 128 ? 7 : 7; }
 
 vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, const vf_search_params *p,
                       cudaStream_t s, Plan *out) {
@@ -552,7 +555,12 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     const int max_iter = p->max_iterations > 0 ? p->max_iterations : 2 * ((p->itopk + w - 1) / w) + 16;
     int hs = 0;
     uint64_t gslots = 0;
-    beam_sizes(p->itopk, w, R, n_init, max_iter, &hs, &gslots);
+    // per-warp shared memory of the batched graph kernel: the visited table takes what the Top
+    // buffers leave; more bytes per warp = fewer visited ids spilling to the global table (long
+    // searches) but fewer resident warps (VF_GRAPH_WARP_KB, read per search)
+    const char *wk = getenv("VF_GRAPH_WARP_KB");
+    const int warp_kb = wk ? std::max(4, atoi(wk)) : graph_warp_kb_default(p->itopk);
+    beam_sizes(p->itopk, w, R, n_init, max_iter, &hs, &gslots, warp_kb * 1024);
 
     SearchArgs &a = pl.a;
     a.ix = D;
@@ -979,6 +987,10 @@ extern "C" vf_status vf_search(vf_index *ix, const void *queries, int64_t n, con
     if (small_path) {
         SearchArgs f = a;
         if (ix->enc8) f.ix = ix->dev8;
+        {   // the per-query path keeps the default 7 KB per warp (its CTAs also hold row stages)
+            uint64_t gs_ = 0;
+            beam_sizes(p->itopk, f.w, D.R, f.n_init, f.max_iter, &f.hash_slots, &gs_, 7168);
+        }
         if (lab_dev) f.qlab = const_cast<int32_t *>(qlab);
         VF_CUDA(cudaMemsetAsync(sc->ctr.p, 0, sizeof(Counters), s));
         if (prof) {
