@@ -325,7 +325,7 @@ def main():
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.and_scan is None:
-        args.and_scan = "0,2000,50000" if args.config == "yfcc" else "0"
+        args.and_scan = "0,1000,2000,5000,10000,20000,50000" if args.config == "yfcc" else "0"
     if args.modes is None:
         args.modes = "greedy,parallel" if args.config == "yfcc" else "greedy"
     if args.scan_thr is None:

@@ -190,9 +190,13 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
         if (nc > RP * GROUP) {
             // more rows than one load group: put every row's 128-byte lines in flight to L2 now,
             // so the later groups do not each pay a full DRAM round trip (one row per lane)
-            if (lane < nc) {
+            const int pf = (a.knobs & KNOB_PF_MASK) >> KNOB_PF_SHIFT;
+            if (lane < nc && pf != 2) {
                 const uint8_t *rp = ix.X + (int64_t)fgid[lane] * row_bytes;
-                for (int l = 0; l < row_bytes; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + l));
+                if (pf == 1)      // exactly the row's bytes (rows are 16-B aligned and padded)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp), "r"(row_bytes) : "memory");
+                else
+                    for (int l = 0; l < row_bytes; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + l));
             }
         }
         for (int p0 = 0; p0 < nc; p0 += RP * GROUP) {
@@ -231,7 +235,7 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
 #if VF_PREFETCH_ADJ
         // a child entering Top is a future parent: start its adjacency row on its way to L2 now, so
         // the expansion's dependent load hits L2 instead of DRAM
-        if (ck != KEY_INF)
+        if (ck != KEY_INF && !(a.knobs & KNOB_NO_ADJ_PF))
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ix.G + (base + (int64_t)((uint32_t)ck >> 1)) * R));
 #endif
         if (M <= 32) {

@@ -57,7 +57,7 @@ struct DevBuf {
 
 // Per-stream (and per role) scratch of a search.
 struct Scratch {
-    DevBuf raw, Qp, Q8, pool, pool_bits, pool_norm, pack_list, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
+    DevBuf raw, Qp, Q8, pool, pool_bits, pool_norm, filt_list, pack_list, qoff, qlab, qinfo, items, item_ctr, graph_list, scan_slots, scan_q, segs, tiles, item_seg,
         item_res, partials, ctr, out_ids, out_dists, ls_count, ls_segbase, ls_itembase, gtab;
     // label sharding: item records out / in, returned results, slots of the sent items
     DevBuf send, recv, res_ids, res_dists, back_ids, back_dists, sent_slots, dst_off;

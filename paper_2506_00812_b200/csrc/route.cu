@@ -159,7 +159,7 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
         const LabelDir d = a.ix.dir[it.label];
         const int count = a.ls_count[d.bslot];
         const int nseg = (count + qg - 1) / qg;
-        const int tr = a.tile_rows;
+        const int tr = (!a.exact && d.size >= a.scan_thr) ? a.tile_rows_f3 : a.tile_rows;
         const int ntile = (d.size + tr - 1) / tr;
         const int total = nseg * ntile;
         const int seg0 = atomicAdd(&a.ctr->n_segs, nseg);
@@ -174,7 +174,9 @@ __global__ void k_segments(SearchArgs a, int64_t n_slots, int qg) {
             sg.n_items = min(qg, count - g * qg);
             sg.tile_base = tb;
             sg.n_tiles = ntile;
-            sg.pad[0] = sg.pad[1] = sg.pad[2] = 0;
+            sg.listed = 0;
+            sg.done = 0;
+            sg.pad = 0;
             a.segs[seg0 + g] = sg;
             for (int t = 0; t < ntile; t++) {
                 Tile tl;
@@ -213,6 +215,12 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
         a.scan_slots[a.ls_itembase[d.bslot] + it.rank] = (int32_t)s;
         a.item_seg[s] = seg;
         const int ntile = a.segs[seg].n_tiles;     // written by k_segments
+        if ((it.meta & META_PRED) && a.filt_list && atomicExch(&a.segs[seg].listed, 1) == 0) {
+            // the segment's first predicate item lists its tiles for the AND pre-filter
+            const int tb = a.segs[seg].tile_base;
+            const int f0 = atomicAdd(&a.ctr->n_filt_tiles, ntile);
+            for (int t = 0; t < ntile; t++) a.filt_list[f0 + t] = tb + t;
+        }
         if (ntile > 1) {
             it.meta |= META_MULTI;       // finalised in the scan kernel (last tile done)
             a.items[s] = it;
@@ -248,80 +256,82 @@ constexpr int kFiltBuf = 2048;
 constexpr int kFiltUnion = 64;
 constexpr int kFiltRows = 4;          // rows per thread per round
 
-__global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a) {
     __shared__ int32_t buf[kFiltBuf];
     __shared__ unsigned long long bbuf[kFiltBuf];
     __shared__ int64_t q_off[kScanQG];
     __shared__ int32_t q_nl[kScanQG];
     __shared__ int32_t p_off[kMaxPieces], p_cnt[kMaxPieces];
-    __shared__ int s_tile, s_npred, s_n, s_np, s_bad, s_flush_off, s_nu, s_bits_off;
+    __shared__ int s_tile, s_npred, s_n, s_np, s_bad, s_flush_off, s_nu, s_bits_off, s_ns;
     __shared__ int32_t s_u[kFiltUnion];           // union of the tile's other query labels, sorted
     __shared__ unsigned long long s_qm[kScanQG];  // per query: its labels' bits in s_u (0: no predicate)
     __shared__ unsigned long long s_plain;        // queries without a predicate (always pass)
+    __shared__ unsigned long long s_one[kFiltUnion];   // queries whose mask is exactly bit j
+    __shared__ unsigned long long s_multi;        // predicate queries with >= 2 mask bits (checked one by one)
     __shared__ int16_t s_slot[kFiltUnion];        // membership bitmap of each s_u label (-1: none)
     __shared__ const int32_t *s_pl[kFiltUnion];   // ... else its posting list on this rank (ascending ids)
     __shared__ int32_t s_pn[kFiltUnion];          // ... and its length (0: not on this rank -> label list)
-    __shared__ int s_allbits;                     // no s_u label needs the point's label list
     __shared__ unsigned long long s_sig[kFiltUnion];   // signature bits of each s_u label
-    const int ntiles = a.ctr->n_tiles;
+    __shared__ uint8_t s_first[kFiltThreads];     // staged pair i holds the first copy of its label
+    // only tiles holding a predicate query are listed (k_scatter), so none is visited for nothing
+    const int ntiles = a.ctr->n_filt_tiles;
     for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&a.ctr->filter_next, 1);
+        if (threadIdx.x == 0) {
+            const int i = atomicAdd(&a.ctr->filter_next, 1);
+            s_tile = i < ntiles ? a.filt_list[i] : -1;
+            s_npred = 0; s_n = 0; s_np = 0; s_bad = 0; s_plain = 0; s_bits_off = -1; s_ns = 0; s_multi = 0;
+        }
+        if (threadIdx.x < kFiltUnion) s_one[threadIdx.x] = 0;
         __syncthreads();
         const int t = s_tile;
-        if (t >= ntiles) break;
+        if (t < 0) break;
         const Tile tl = a.tiles[t];
         const int nq = tl.nq;
-        if (threadIdx.x == 0) { s_npred = 0; s_n = 0; s_np = 0; s_bad = 0; s_plain = 0; s_bits_off = -1; }
-        __syncthreads();
         if (threadIdx.x < nq) {
             const ScanQuery sq = a.scan_q[tl.item_base + threadIdx.x];
             q_off[threadIdx.x] = sq.p_off;
             q_nl[threadIdx.x] = (sq.meta & META_PRED) ? sq.nl : 0;
             if (sq.meta & META_PRED) atomicAdd(&s_npred, 1);
             else atomicOr(&s_plain, 1ull << threadIdx.x);
+            s_qm[threadIdx.x] = 0;
         }
         __syncthreads();
         const int npred = s_npred;
-        if (npred == 0) {
-            __syncthreads();
-            continue;
-        }
         const bool compact = npred == nq;
         const int nrows = tl.row_end - tl.row_begin;
-        // the tile's other labels -> bit positions (one thread; <= 64 distinct, else per-query
-        // verification); a mixed tile also reserves one pass-bit word per row
-        if (threadIdx.x == 0) {
-            int nu = 0;
-            for (int g = 0; g < nq && nu <= 64; g++)
-                for (int i = 0; i < q_nl[g] && nu <= 64; i++) {
-                    const int32_t l = a.qlab[q_off[g] + i];
-                    if (l == tl.label) continue;
-                    int j = nu;
-                    while (j > 0 && s_u[j - 1] > l) j--;
-                    if (j > 0 && s_u[j - 1] == l) continue;
-                    if (nu == kFiltUnion) { nu = 65; break; }
-                    for (int m = nu; m > j; m--) s_u[m] = s_u[m - 1];
-                    s_u[j] = l;
-                    nu++;
-                }
-            s_nu = nu;
-            int all = nu <= 64;
-            for (int j = 0; j < nu && nu <= 64; j++) {
-                const int32_t l = s_u[j];
-                const bool known = l >= 0 && l < a.ix.n_labels;
-                const int sl = (known && a.ix.lbit_slot) ? a.ix.lbit_slot[l] : -1;
-                s_slot[j] = (int16_t)sl;
-                s_sig[j] = label_sig_bits(l);
-                s_pn[j] = 0;
-                s_pl[j] = nullptr;
-                if (sl < 0 && known) {
-                    const LabelDir dl = a.ix.dir[l];
-                    s_pn[j] = dl.size;
-                    s_pl[j] = (dl.size >= a.ix.T ? a.ix.M_hs : a.ix.M_ls) + dl.base;
-                }
-                if (sl < 0 && s_pn[j] == 0) all = 0;  // not on this rank: the label list decides
+        // the tile's other labels -> bit positions (<= 64 distinct, else per-query verification),
+        // in parallel: every (query, label) pair is staged (label in buf, query in bbuf), the
+        // distinct labels ranked, and each label's membership structure looked up by its own thread
+        if (threadIdx.x < nq) {
+            const int g = threadIdx.x;
+            for (int i = 0; i < q_nl[g]; i++) {
+                const int32_t l = a.qlab[q_off[g] + i];
+                if (l == tl.label) continue;
+                const int p = atomicAdd(&s_ns, 1);
+                if (p < kFiltThreads) { buf[p] = l; bbuf[p] = (unsigned long long)g; }
             }
-            s_allbits = all;
+        }
+        __syncthreads();
+        const int ns = s_ns;
+        bool first = false;
+        int32_t myl = 0;
+        if (ns <= kFiltThreads && threadIdx.x < ns) {
+            myl = buf[threadIdx.x];
+            first = true;
+            for (int j = 0; j < threadIdx.x; j++)
+                if (buf[j] == myl) { first = false; break; }
+            s_first[threadIdx.x] = first;
+        }
+        // number of distinct labels, and each distinct label's rank among them
+        const int nd = ns <= kFiltThreads ? __syncthreads_count(first) : kFiltUnion + 1;
+        if (first && nd <= kFiltUnion) {
+            int r = 0;
+            for (int j = 0; j < ns; j++) r += s_first[j] && buf[j] < myl;
+            s_u[r] = myl;
+        }
+        if (threadIdx.x == 0) {
+            s_nu = nd <= kFiltUnion ? nd : kFiltUnion + 1;
             if (!compact) {
                 const int need = (nrows + 3) & ~3;        // 16-B aligned bulk copies of the words
                 const int off = atomicAdd(&a.ctr->pool_used, need);
@@ -330,23 +340,52 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
         }
         __syncthreads();
         const int nu = s_nu;
-        const bool allbits = s_allbits != 0;
+        int lab_ok = 1, lab_nobm = 0;
+        if (nu <= kFiltUnion && threadIdx.x < nu) {
+            const int j = threadIdx.x;
+            const int32_t l = s_u[j];
+            const bool known = l >= 0 && l < a.ix.n_labels;
+            const int sl = (known && a.ix.lbit_slot) ? a.ix.lbit_slot[l] : -1;
+            s_slot[j] = (int16_t)sl;
+            s_sig[j] = label_sig_bits(l);
+            int pn = 0;
+            const int32_t *pl = nullptr;
+            if (sl < 0 && known) {
+                const LabelDir dl = a.ix.dir[l];
+                pn = dl.size;
+                pl = (dl.size >= a.ix.T ? a.ix.M_hs : a.ix.M_ls) + dl.base;
+            }
+            s_pn[j] = pn;
+            s_pl[j] = pl;
+            lab_ok = !(sl < 0 && pn == 0);           // not on this rank: the label list decides
+            lab_nobm = sl < 0;
+        }
+        if (nu <= kFiltUnion && threadIdx.x < ns) {   // each staged pair sets its query's mask bit
+            int lo = 0, hi = nu - 1;
+            const int32_t l = buf[threadIdx.x];
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_u[mid] < l) lo = mid + 1; else hi = mid; }
+            atomicOr(&s_qm[(int)bbuf[threadIdx.x]], 1ull << lo);
+        }
+        const bool allbits = nu <= kFiltUnion && __syncthreads_and(lab_ok);
+        // a bitmap label costs one sector per row, as does the signature (a random 8-B read): with
+        // every label on a bitmap the signature only adds a sector (VF_KNOBS bit 0)
+        const bool needsig = !(a.knobs & KNOB_FILT_SIG_AUTO) || __syncthreads_or(lab_nobm);
         const int bits_off = s_bits_off;
         if (!compact && bits_off < 0) {          // pool exhausted: the scan verifies this tile
             __syncthreads();
             continue;
         }
-        if (nu <= 64 && threadIdx.x < nq) {
-            unsigned long long qm = 0;
-            for (int i = 0; i < q_nl[threadIdx.x]; i++) {
-                const int32_t l = a.qlab[q_off[threadIdx.x] + i];
-                for (int j = 0; j < nu; j++)
-                    if (s_u[j] == l) qm |= 1ull << j;
-            }
-            s_qm[threadIdx.x] = qm;
+        // pass bits of a row = plain | OR of s_one[j] over its set label bits | multi-bit queries
+        // whose whole mask is set
+        if (nu <= kFiltUnion && threadIdx.x < nq && q_nl[threadIdx.x]) {
+            const unsigned long long qm = s_qm[threadIdx.x];
+            if (qm == 0) atomicOr(&s_plain, 1ull << threadIdx.x);        // its labels are all the tile's
+            else if ((qm & (qm - 1)) == 0) atomicOr(&s_one[__ffsll((long long)qm) - 1], 1ull << threadIdx.x);
+            else atomicOr(&s_multi, 1ull << threadIdx.x);
         }
         __syncthreads();
         const unsigned long long plain = s_plain;
+        const unsigned long long multi = s_multi;
         const int32_t *rowid = tl.hs ? a.ix.M_hs + tl.base : a.ix.M_ls + tl.base;
         for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads * kFiltRows) {
             // kFiltRows rows per thread, their dependent chains (id -> label offsets -> labels)
@@ -375,7 +414,8 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                     // binary searches in the short posting lists of labels without one
                     unsigned long long sg[kFiltRows];
 #pragma unroll
-                    for (int u = 0; u < kFiltRows; u++) sg[u] = gid[u] >= 0 && a.ix.lsig ? ld_keep(a.ix.lsig + gid[u]) : ~0ull;
+                    for (int u = 0; u < kFiltRows; u++)
+                        sg[u] = gid[u] >= 0 && a.ix.lsig && needsig ? ld_keep(a.ix.lsig + gid[u]) : ~0ull;
 #pragma unroll
                     for (int u = 0; u < kFiltRows; u++) {
                         lb[u] = 0;
@@ -432,8 +472,11 @@ __global__ void __launch_bounds__(kFiltThreads) k_and_filter(SearchArgs a) {
                 for (int u = 0; u < kFiltRows; u++) {
                     if (gid[u] < 0) continue;
                     unsigned long long b = plain;
-                    for (int g = 0; g < nq; g++)
-                        if (q_nl[g] && (lb[u] & s_qm[g]) == s_qm[g]) b |= 1ull << g;
+                    for (unsigned long long m = lb[u]; m; m &= m - 1) b |= s_one[__ffsll((long long)m) - 1];
+                    for (unsigned long long m = multi; m; m &= m - 1) {
+                        const int g = __ffsll((long long)m) - 1;
+                        if ((lb[u] & s_qm[g]) == s_qm[g]) b |= 1ull << g;
+                    }
                     pb[u] = b;
                 }
             }
@@ -658,8 +701,10 @@ int launch_pack(const SearchArgs &a, cudaStream_t s) {
 }
 
 int launch_and_filter(const SearchArgs &a, cudaStream_t s) {
-    if (!a.pool || a.pool_cap <= 0) return 0;
-    k_and_filter<<<148 * 8, kFiltThreads, 0, s>>>(a);
+    if (!a.pool || a.pool_cap <= 0 || !a.filt_list) return 0;
+    // VF_KNOBS bit 4: 6 resident CTAs per SM (<= 40 registers) instead of 4 (64 registers)
+    if (a.knobs & KNOB_FILT_OCC6) k_and_filter<6><<<148 * 6, kFiltThreads, 0, s>>>(a);
+    else k_and_filter<4><<<148 * 4, kFiltThreads, 0, s>>>(a);
     return 1;
 }
 

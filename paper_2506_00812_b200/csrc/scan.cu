@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(SearchArgs a, ScanLayo
                 // last-block-done: the CTA completing the segment's last tile merges the partials
                 __threadfence();
                 named_bar_sync(1, 32 * kScanConsumers);
-                if (ct == 0) flag[0] = atomicAdd(&a.segs[ti.seg].pad[0], 1) == ti.n_tiles - 1;
+                if (ct == 0) flag[0] = atomicAdd(&a.segs[ti.seg].done, 1) == ti.n_tiles - 1;
                 named_bar_sync(1, 32 * kScanConsumers);
                 if (flag[0]) {
                     __threadfence();

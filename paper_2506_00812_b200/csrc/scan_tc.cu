@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                     // last-block-done: the CTA completing the segment's last tile merges the partials
                     __threadfence();
                     named_bar_sync(3, 32 * kTcSelW);
-                    if (sw == 0 && lane == 0) misc[2] = atomicAdd(&a.segs[ti.seg].pad[0], 1) == ti.n_tiles - 1;
+                    if (sw == 0 && lane == 0) misc[2] = atomicAdd(&a.segs[ti.seg].done, 1) == ti.n_tiles - 1;
                     named_bar_sync(3, 32 * kTcSelW);
                     if (misc[2]) {
                         __threadfence();

@@ -81,6 +81,7 @@ extern "C" vf_status vf_serve_start(vf_index *ix, const vf_search_params *p, int
     a.n_init = p->n_init > 0 ? p->n_init : ix->dev.R * w;
     a.max_iter = p->max_iterations > 0 ? p->max_iterations : 2 * ((p->itopk + w - 1) / w) + 16;
     a.seed = p->seed;
+    a.knobs = vf::kDefaultKnobs;
     a.op = p->op;
     a.recall_mode = p->recall_mode;
     a.exact = p->exact ? 1 : 0;

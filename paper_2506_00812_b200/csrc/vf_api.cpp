@@ -577,6 +577,12 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.and_scan_thr = p->and_scan_threshold;
     a.scan_thr = std::max(D.T, p->scan_threshold);
     a.tile_rows = tile_rows;
+    {
+        // f3-only segments (every tile pre-filtered): VF_F3_TILE rows per tile (read per search)
+        const char *e = getenv("VF_F3_TILE");
+        const int f3t = e ? atoi(e) : kF3TileRows;
+        a.tile_rows_f3 = std::max(tile_rows, f3t >= 64 ? (f3t & ~63) : tile_rows);
+    }
     a.max_tiles_per_label = mtpl;
     a.max_tiles = (int32_t)std::min<int64_t>(pl.max_tiles, INT32_MAX);
     a.hash_slots = hs;
@@ -595,6 +601,7 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     a.tc_xn = F.xn;
     a.tc_xn_ls = F.xn_ls;
     a.pool_cap = 0;
+    a.filt_list = nullptr;
     a.n_slots = n_slots;
     a.max_nl = ix->world > 1 ? kRecLabels : kMaxQueryLabels;
     a.pack_list = nullptr;
@@ -604,6 +611,8 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
     {
         const char *e = getenv("VF_TC_PARTS");
         a.tc_parts = e ? atoi(e) : 1;
+        const char *kn = getenv("VF_KNOBS");
+        a.knobs = kn ? (int32_t)strtol(kn, nullptr, 0) : kDefaultKnobs;
     }
     pl.graph_ctas = graph_max_ctas(a);
     if (pl.graph_ctas <= 0) return fail(VF_ERR_INTERNAL, "no graph kernel for this row size");
@@ -628,6 +637,10 @@ vf_status plan_search(vf_index *ix, Scratch *sc, int64_t n, int64_t n_slots, con
         a.pool_bits = sc->pool_bits.as<unsigned long long>();
         a.pool_norm = F.xn ? sc->pool_norm.as<uint32_t>() : nullptr;
         a.pool_cap = (int32_t)cap;
+        if (pl.filter) {
+            VF_CUDA(sc->filt_list.ensure((size_t)std::max<int64_t>(pl.max_tiles, 1) * 4));
+            a.filt_list = sc->filt_list.as<int32_t>();
+        }
     }
     if (ix->enc8) {
         VF_CUDA(sc->Q8.ensure((size_t)std::max<int64_t>(n, 1) * ix->dev8.row_bytes));

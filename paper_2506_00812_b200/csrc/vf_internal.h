@@ -22,6 +22,7 @@ __host__ __device__ __forceinline__ int graph_class(int32_t size) {
 }      // membership bitmaps of the largest labels (predicate fast path)
 constexpr int kMaxItopk = 1024;
 constexpr int kScanQG = 64;           // queries per scan segment (query group)
+constexpr int kF3TileRows = 8192;     // rows per tile of f3-only (fully pre-filtered) segments
 constexpr int kWarpsPerGraphCta = 4;
 
 enum Path : uint32_t { PATH_NONE = 0, PATH_SCAN = 1, PATH_GRAPH = 2 };
@@ -103,10 +104,12 @@ struct Segment {
     int32_t n_items;
     int32_t tile_base;   // first tile of this segment
     int32_t n_tiles;
-    int32_t pad[3];
+    int32_t listed;      // 1 once k_scatter listed the segment's tiles for the AND pre-filter
+    int32_t done;        // tiles of a multi-tile segment finished (the last one merges the partials)
+    int32_t pad;
 };
 
-constexpr int kMaxPieces = 6;        // survivor pieces of a pre-filtered tile (k_and_filter)
+constexpr int kMaxPieces = 8;        // survivor pieces of a pre-filtered tile (k_and_filter)
 
 // A row tile of a segment: everything the scan producer needs in one record, so claiming a tile
 // costs one dependent load (written by k_segments; survivor pieces by k_hs_filter).
@@ -161,13 +164,15 @@ struct Counters {
     int32_t graph_next;
     int32_t n_items;
     int32_t exact_fallback;  // a query of this batch is outside the fast path's exact range (gate)
-    int32_t filter_next;     // k_hs_filter tile cursor
+    int32_t filter_next;     // k_and_filter cursor over filt_list
     int32_t n_tile_cls[4];        // scan tiles per row-count class (kTileClasses; longest first)
     int32_t pool_used;       // survivor pool bump allocator
     int32_t n_pack;          // small single-tile segments queued for packing (k_pack)
     int32_t n_packed;        // packed tiles made
     int32_t packq_used;      // query records copied for packed tiles
     int32_t n_invalid;       // queries rejected by the device-side offset / label-count check
+    int32_t n_filt_tiles;    // tiles holding a predicate query (k_scatter -> filt_list, k_and_filter)
+    int32_t pad_ctr;
     unsigned long long graph_V, graph_E, graph_iters, scan_rows, scan_qrows;
     unsigned long long graph_V_max;
     // device-clock activity spans of the dominant kernels (globaltimer ns; first CTA start stored
@@ -210,6 +215,9 @@ struct SearchArgs {
     int32_t and_scan_thr;
     int32_t scan_thr;      // effective specificity threshold of this search: max(T, scan_threshold) (f2)     // selectivity-aware AND routing (f3), 0 = off
     int32_t tile_rows;
+    int32_t tile_rows_f3;     // rows per tile of a segment scanned only through f3 AND routing (|C_l| >=
+                              // scan_thr, not exact): every one of its tiles is compacted by the AND
+                              // pre-filter, so large tiles cost the scan nothing and save tile chains
     int32_t max_tiles_per_label;
     int32_t max_tiles;
     int32_t hash_slots;       // smem visited table size (power of two)
@@ -231,6 +239,7 @@ struct SearchArgs {
     uint32_t *pool_norm;      // ... and their ||x||^2 (tensor-core scan; nullptr: none)
     const uint32_t *tc_xn, *tc_xn_ls;   // ||x||^2 per point / X_LS row of the tensor-core scan's view
     int32_t pool_cap;
+    int32_t *filt_list;       // [max_tiles] the tiles k_and_filter visits (those with a predicate query)
     // device-side validation of caller offsets (device label arrays are not read by the host): a
     // query whose labels fall outside [0, n_slots) or number more than max_nl gets an empty row
     // and is counted in ctr->n_invalid (vf_search_stats.n_invalid_queries)
@@ -244,7 +253,16 @@ struct SearchArgs {
     int32_t *pack_list;
     int32_t pack_max_nq, pack_group;
     int64_t packq_base;
+    // implementation switches of equal-result variants (VF_KNOBS, read per search; A/B tooling):
+    // bit 0 the AND pre-filter reads the point's label signature only when some label of the tile
+    // has no membership bitmap; bits 1-2 graph row prefetch into L2 (0 per 128-B line, 1 one bulk
+    // prefetch of the row's exact bytes, 2 none); bit 3 no L2 prefetch of adjacency rows; bit 4 the
+    // AND pre-filter at 6 CTAs per SM
+    int32_t knobs;
 };
+enum : int32_t { KNOB_FILT_SIG_AUTO = 1, KNOB_PF_SHIFT = 1, KNOB_PF_MASK = 3 << 1, KNOB_NO_ADJ_PF = 1 << 3,
+                 KNOB_FILT_OCC6 = 1 << 4 };
+constexpr int32_t kDefaultKnobs = KNOB_FILT_SIG_AUTO | (1 << KNOB_PF_SHIFT) | KNOB_NO_ADJ_PF;   // r02t A/B
 
 __device__ __forceinline__ bool gate_skip(const SearchArgs &a) {
     if (a.gate == 0) return false;

@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """A small end-to-end run of every product kernel family on tiny inputs, for compute-sanitizer:
    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python scripts/sanitize.py
-batched path (route, AND pre-filter, tensor-core scan, graph, merge; single / AND / OR; exact mode),
+batched path (route, AND pre-filter incl. large f3 tiles, tensor-core scan, graph, merge; single / AND / OR;
+exact mode),
 the per-query path (k_small), label sharding over virtual shards, and the graph builder (k_join, pruning).
 The persistent serving kernel is left out: it polls host memory the sanitizer serialises."""
 import os
@@ -30,6 +31,8 @@ for mode in ("single", "and2", "or2"):
     ix.search(Q[:20], qo[:21], ql[:qo[20]], k=10, itopk=32, op=op)            # per-query path
     if op == "and":
         ix.search(Q, qo, ql, k=10, itopk=32, op=op, recall_mode="parallel", and_scan_threshold=400)
+        # f3 routing of every HS l*: large pre-filtered tiles with several survivor pieces
+        ix.search(Q, qo, ql, k=10, itopk=32, op=op, and_scan_threshold=10 ** 7)
 print("search ok")
 sh = vf.Index(X, w.post_off, w.post_ids, c.threshold_T, c.degree_R, go, gi, virtual_shards=2)
 sh.search(Q, w.q_off, w.q_lab, k=10, itopk=32)

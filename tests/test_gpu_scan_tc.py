@@ -330,3 +330,38 @@ def test_tile_packing_is_exact(vf, monkeypatch, mode):
     assert (res["0"][0] == res["1"][0]).all() and (res["0"][1] == res["1"][1]).all()
     e, ed = o.search(Q, qoff, qlab, k=10, itopk=32, op=op)
     assert (res["1"][0] == e).all() and (res["1"][1] == ed.astype(np.float32)).all()
+
+
+
+@pytest.mark.parametrize("cap", [None, "6000"])
+def test_f3_tile_sizes_are_exact(vf, monkeypatch, cap):
+    """Segments scanned only through f3 AND routing (every tile compacted by the AND pre-filter)
+    use large tiles (VF_F3_TILE rows): a tile's survivors come in up to kMaxPieces pieces, more
+    survivors than that leave the tile to the scan's own verification, and a small survivor pool
+    leaves tiles uncompacted. Results bit-identical across tile sizes, and to the oracle (greedy
+    AND with f3 routing; Definition 1 in exact mode, where tiles keep the normal size)."""
+    from workload import gen
+    if cap is None:
+        monkeypatch.delenv("VF_POOL_CAP", raising=False)
+    else:
+        monkeypatch.setenv("VF_POOL_CAP", cap)
+    cfg, X, off, ids, go, gi = small_random_index(seed=61, N=40000, D=64, L=12, F=3.0, T=1500, R=8,
+                                                  dtype="u8")
+    assert np.diff(off).max() > 4 * 4096           # multi-tile segments at every tile size
+    g = vf.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    o = oracle.Index(X, off, ids, cfg.threshold_T, cfg.degree_R, go, gi)
+    Q = gen.gen_query_vectors(cfg, n=500)
+    qoff, qlab = gen.gen_query_labels(cfg, off, ids, n=500, mode="mix_and")
+    thr = 10 ** 7                                      # every greedy AND item with an HS l* is scanned
+    for exact in (False, True):
+        res = {}
+        for rows in ("2048", "8192", "32768"):
+            monkeypatch.setenv("VF_F3_TILE", rows)
+            res[rows] = g.search(Q, qoff, qlab, k=10, itopk=32, op="and", exact=exact, and_scan_threshold=thr)
+        for rows in ("8192", "32768"):
+            assert (res[rows][0] == res["2048"][0]).all() and (res[rows][1] == res["2048"][1]).all(), (exact, rows)
+        if exact:
+            e, ed = o.exact_knn(Q, qoff, qlab, k=10, op="and")
+        else:
+            e, ed = o.search(Q, qoff, qlab, k=10, itopk=32, op="and", and_scan_threshold=thr)
+        assert (res["8192"][0] == e).all() and (res["8192"][1] == ed.astype(np.float32)).all(), (exact, cap)
