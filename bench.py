@@ -699,8 +699,10 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(args.config)
+        storage = "u8" if (c.dtype == "u8" or info["bytes_u8_store"] > 0) else "f32"
         if tj and f"k_{dom}" in tj and (tj["itopk"], tj["search_width"], tj["and_scan_threshold"],
-                                        tj["scan_threshold"], tj.get("recall_mode", "greedy")) == (itopk, w_, as_, st_, mode):
+                                        tj["scan_threshold"], tj.get("recall_mode", "greedy"),
+                                        tj.get("storage", "u8")) == (itopk, w_, as_, st_, mode, storage):
             traffic = int(tj[f"k_{dom}"]["bytes"])
     except (OSError, ValueError, KeyError):
         traffic = None
