@@ -6,7 +6,7 @@
 #include "graph_item.cuh"
 
 #ifndef VF_GRAPH_MINB
-#define VF_GRAPH_MINB 8      // CTAs per SM the register budget is sized for (8: 64 registers)
+#define VF_GRAPH_MINB 7      // CTAs per SM the register budget is sized for (7: 72 registers; r02aa A/B)
 #endif
 
 namespace vf {

@@ -156,24 +156,44 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
     // Process one batch of candidate local ids (one per lane, -1 = none): visited-set
     // check/insert, M_HS mapping, predicate, distances, merge into Top.
     auto process = [&](int32_t c, int32_t gid) {
-        bool v = c >= 0;
-        const unsigned same = __match_any_sync(FULL, v ? c : -1 - lane);
-        if (v && (__ffs(same) - 1) != lane) v = false;          // duplicate within the batch
-        bool found = false;
-        if (v) {
-            found = smem_find(htab, hmask, c);
-            if (!found && g_used) found = gtab_find(gtab, gmask, epoch, c);
+        bool isnew;
+        int nnew;
+        if (!g_used && 2 * (n_smem + 32) <= H && !(a.knobs & KNOB_VIS_2PHASE)) {
+            // the whole batch fits the shared table and nothing has spilled: one insert-if-absent
+            // probe per lane (atomicCAS; of duplicate ids within the batch exactly one lane inserts,
+            // and which one does not matter -- keys are ordered by (distance, id) only)
+            isnew = false;
+            if (c >= 0) {
+                uint32_t h = vis_hash(c) & hmask;
+                for (;;) {
+                    const int32_t old = atomicCAS(htab + h, -1, c);
+                    if (old == -1) { isnew = true; break; }
+                    if (old == c) break;
+                    h = (h + 1) & hmask;
+                }
+            }
+            nnew = __popc(__ballot_sync(FULL, isnew));
+            n_smem += nnew;
+        } else {
+            bool v = c >= 0;
+            const unsigned same = __match_any_sync(FULL, v ? c : -1 - lane);
+            if (v && (__ffs(same) - 1) != lane) v = false;      // duplicate within the batch
+            bool found = false;
+            if (v) {
+                found = smem_find(htab, hmask, c);
+                if (!found && g_used) found = gtab_find(gtab, gmask, epoch, c);
+            }
+            isnew = v && !found;
+            const unsigned nm = __ballot_sync(FULL, isnew);
+            nnew = __popc(nm);
+            const bool use_smem = 2 * (n_smem + nnew) <= H;
+            __syncwarp();
+            if (isnew) {
+                if (use_smem) smem_insert(htab, hmask, c);
+                else gtab_insert(gtab, gmask, epoch, c);
+            }
+            if (nnew) { if (use_smem) n_smem += nnew; else g_used = true; }
         }
-        const bool isnew = v && !found;
-        const unsigned nm = __ballot_sync(FULL, isnew);
-        const int nnew = __popc(nm);
-        const bool use_smem = 2 * (n_smem + nnew) <= H;
-        __syncwarp();
-        if (isnew) {
-            if (use_smem) smem_insert(htab, hmask, c);
-            else gtab_insert(gtab, gmask, epoch, c);
-        }
-        if (nnew) { if (use_smem) n_smem += nnew; else g_used = true; }
         nvis += nnew;
         if (isnew && gid < 0) gid = __ldg(ix.M_hs + base + c);   // entry samples only
         bool pass = isnew;

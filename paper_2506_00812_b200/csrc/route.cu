@@ -369,7 +369,8 @@ __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a)
         const bool allbits = nu <= kFiltUnion && __syncthreads_and(lab_ok);
         // a bitmap label costs one sector per row, as does the signature (a random 8-B read): with
         // every label on a bitmap the signature only adds a sector (VF_KNOBS bit 0)
-        const bool needsig = !(a.knobs & KNOB_FILT_SIG_AUTO) || __syncthreads_or(lab_nobm);
+        const bool anynobm = __syncthreads_or(lab_nobm);
+        const bool needsig = !(a.knobs & KNOB_FILT_SIG_AUTO) || anynobm;
         const int bits_off = s_bits_off;
         if (!compact && bits_off < 0) {          // pool exhausted: the scan verifies this tile
             __syncthreads();
@@ -387,6 +388,44 @@ __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a)
         const unsigned long long plain = s_plain;
         const unsigned long long multi = s_multi;
         const int32_t *rowid = tl.hs ? a.ix.M_hs + tl.base : a.ix.M_ls + tl.base;
+        // survivors in buf -> one pool piece (ids, pass bits, norms); pieces are 16-B aligned
+        // survivors in buf -> one pool piece (ids, pass bits, norms). Every piece but a tile's last
+        // holds a multiple of 4 rows (up to 3 survivors wait in buf for the next piece) and every
+        // allocation is rounded to 4 rows, so each piece starts 16-B aligned in pool, pool_norm and
+        // pool_bits AND at a 4-row boundary of the tile: the scan moves any piece with bulk copies.
+        auto flush = [&](bool final_piece) {
+            const int n = final_piece ? s_n : (s_n & ~3);
+            if (threadIdx.x == 0 && n > 0) {
+                if (s_np == kMaxPieces) {
+                    s_bad = 1;
+                } else {
+                    const int off = atomicAdd(&a.ctr->pool_used, (n + 3) & ~3);
+                    if ((int64_t)off + n > a.pool_cap) {
+                        s_bad = 1;
+                    } else {
+                        p_off[s_np] = off;
+                        p_cnt[s_np] = n;
+                        s_np++;
+                        s_flush_off = off;
+                    }
+                }
+            }
+            __syncthreads();
+            if (!s_bad && n > 0)
+                for (int i = threadIdx.x; i < n; i += kFiltThreads) {
+                    a.pool[s_flush_off + i] = buf[i];
+                    a.pool_bits[s_flush_off + i] = bbuf[i];
+                    if (a.pool_norm) a.pool_norm[s_flush_off + i] = __ldg(a.tc_xn + buf[i]);
+                }
+            __syncthreads();
+            if (threadIdx.x < s_n - n) {          // the <= 3 survivors left over move to the front
+                buf[threadIdx.x] = buf[n + threadIdx.x];
+                bbuf[threadIdx.x] = bbuf[n + threadIdx.x];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_n -= n;
+            __syncthreads();
+        };
         for (int r0 = tl.row_begin; r0 < tl.row_end; r0 += kFiltThreads * kFiltRows) {
             // kFiltRows rows per thread, their dependent chains (id -> label offsets -> labels)
             // interleaved so several memory latencies overlap
@@ -500,35 +539,8 @@ __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a)
             // a tile of <= kFiltBuf rows flushes once: its survivors form ONE contiguous piece,
             // which the scan's producer moves with bulk copies (ids, norms, pass bits)
             const bool one_piece = nrows <= kFiltBuf;
-            if ((!one_piece && s_n > kFiltBuf - kFiltThreads * kFiltRows) || (last && s_n > 0)) {
-                if (threadIdx.x == 0) {
-                    if (s_np == kMaxPieces) {
-                        s_bad = 1;
-                    } else {
-                        // sizes rounded to 4 keep every allocation 16-B aligned in pool (ids,
-                        // norms) and pool_bits: the scan reads them with bulk copies
-                        const int off = atomicAdd(&a.ctr->pool_used, (s_n + 3) & ~3);
-                        if ((int64_t)off + s_n > a.pool_cap) {
-                            s_bad = 1;
-                        } else {
-                            p_off[s_np] = off;
-                            p_cnt[s_np] = s_n;
-                            s_np++;
-                            s_flush_off = off;
-                        }
-                    }
-                }
-                __syncthreads();
-                if (!s_bad)
-                    for (int i = threadIdx.x; i < s_n; i += kFiltThreads) {
-                        a.pool[s_flush_off + i] = buf[i];
-                        a.pool_bits[s_flush_off + i] = bbuf[i];
-                        if (a.pool_norm) a.pool_norm[s_flush_off + i] = __ldg(a.tc_xn + buf[i]);
-                    }
-                __syncthreads();
-                if (threadIdx.x == 0) s_n = 0;
-                __syncthreads();
-            }
+            if (last && s_n > 0) flush(true);
+            else if (!one_piece && s_n > kFiltBuf - kFiltThreads * kFiltRows) flush(false);
             if (s_bad) break;
         }
         __syncthreads();

@@ -435,32 +435,44 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtasPerSm)
                         if (rbits) tma_load_1d(dbits, a.pool_bits + tl.bits_off + v0, bb, full + slot);
                     }
                     __syncwarp();
-                } else if (filt && tl.n_pieces == 1 && a.pool_norm) {
-                    // compacted tile, one piece: ids by the lanes (one coalesced read, the only
-                    // wait), the rows by tile::gather4, and ids / norms / pass bits by bulk copies
+                } else if (filt && a.pool_norm) {
+                    // compacted tile: its pieces start at 4-row boundaries, 16-B aligned (k_and_filter),
+                    // so per piece overlapping this stage ids / norms / pass bits move by bulk copies
+                    // and the lanes read the ids (coalesced int4, the only wait) for tile::gather4
                     const int ng = (nr + 3) >> 2;
-                    const int64_t po = tl.piece_off[0] + v0;          // 16-B aligned (k_and_filter)
                     const uint32_t b4n = (uint32_t)((nr * 4 + 15) & ~15), b8n = (uint32_t)((nr * 8 + 15) & ~15);
                     if (lane == 0) {
                         mbar_wait(empty + slot, ((n / nst) & 1) ^ 1);
                         meta[slot] = make_int4(t, r0, nr, flags);
                         mbar_arrive_expect_tx(full + slot, (uint32_t)(ng * 4 * kpad) + 2 * b4n + b8n);
-                        if (nr > 0) {
-                            tma_load_1d(dsid, a.pool + po, b4n, full + slot);
-                            tma_load_1d(dnorm, a.pool_norm + po, b4n, full + slot);
-                            tma_load_1d(dbits, a.pool_bits + po, b8n, full + slot);
+                        int ps = 0;                                       // first row of piece p
+                        for (int p = 0; p < tl.n_pieces && nr > 0; p++) {
+                            const int pc = tl.piece_cnt[p];
+                            const int lo = max(ps, v0), hi = min(ps + pc, v0 + nr);
+                            if (lo < hi) {
+                                const int64_t po = tl.piece_off[p] + (lo - ps);
+                                const int d = lo - v0, len = hi - lo;
+                                tma_load_1d(dsid + d, a.pool + po, (uint32_t)((len * 4 + 15) & ~15), full + slot);
+                                tma_load_1d(dnorm + d, a.pool_norm + po, (uint32_t)((len * 4 + 15) & ~15), full + slot);
+                                tma_load_1d(dbits + d, a.pool_bits + po, (uint32_t)((len * 8 + 15) & ~15), full + slot);
+                            }
+                            ps += pc;
                         }
                     }
                     __syncwarp();
                     for (int q4 = lane; q4 < ng; q4 += 32) {
-                        const int rr = q4 * 4;
+                        const int rr = q4 * 4, v = v0 + rr;
+                        int p = 0, ps = 0;
+                        while (p + 1 < tl.n_pieces && v >= ps + tl.piece_cnt[p]) { ps += tl.piece_cnt[p]; p++; }
+                        const int64_t po = tl.piece_off[p] + (v - ps);
+                        const int cnt = min(4, ps + tl.piece_cnt[p] - v);   // rows of this group in the piece
                         int32_t g4[4];
-                        if (rr + 3 < nr) {
-                            const int4 v4 = __ldg(reinterpret_cast<const int4 *>(a.pool + po) + q4);
+                        if (cnt == 4) {
+                            const int4 v4 = __ldg(reinterpret_cast<const int4 *>(a.pool + po));
                             g4[0] = v4.x; g4[1] = v4.y; g4[2] = v4.z; g4[3] = v4.w;
                         } else {
 #pragma unroll
-                            for (int j = 0; j < 4; j++) g4[j] = __ldg(a.pool + po + min(rr + j, nr - 1));
+                            for (int j = 0; j < 4; j++) g4[j] = __ldg(a.pool + po + min(j, cnt - 1));
                         }
                         for (int c = 0; c < nch; c++)
                             tma_gather4(dst + (size_t)c * kTcRows * cw + (size_t)q4 * 4 * cw, &tm_x, c * cw, g4,
