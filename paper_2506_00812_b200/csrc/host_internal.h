@@ -66,7 +66,7 @@ struct Scratch {
     DevBuf tile_cls;            // scan tiles by row-count class (claim order of the tensor-core scan)
     // scan / graph overlap: the graph kernels run on a side stream forked after routing
     cudaStream_t side = nullptr, side_hi = nullptr;   // graph kernels; scan kernels (high priority)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_filt = nullptr;
     // label sharding: the exchange stream, its events and the pinned copy of the routed counters
     cudaStream_t xs = nullptr;
     cudaEvent_t ev_routed = nullptr, ev_cnt = nullptr, ev_xdone = nullptr;
@@ -96,6 +96,7 @@ struct Scratch {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (ev_join2) cudaEventDestroy(ev_join2);
+        if (ev_filt) cudaEventDestroy(ev_filt);
         if (xs) cudaStreamDestroy(xs);
         if (ev_routed) cudaEventDestroy(ev_routed);
         if (ev_cnt) cudaEventDestroy(ev_cnt);

@@ -68,12 +68,23 @@ struct TcLayout {
 
 constexpr int kTcCtasPerSm = 2;       // up to two independent pipelines per SM (latency-bound chains)
 
+// K chunk (swizzle width) of the row tiles: the largest of 128 / 64 / 32 B dividing the row, or with
+// VF_TC_CW=128 always 128 B (rows padded to a multiple of 128 in shared memory: the TMA fills the
+// bytes past the row with zeros without reading them, so a 192-B row costs 2 tile::gather4 requests
+// per 4 rows instead of 3; the zero columns add nothing to the dot products). Read once per process:
+// the tensor maps (index build) and the layout (each search) must agree.
+static int tc_chunk_bytes(int row_bytes) {
+    static const int force = [] { const char *e = getenv("VF_TC_CW"); return e ? atoi(e) : 0; }();
+    if (force == 128 && row_bytes > 64) return 128;
+    return row_bytes % 128 == 0 ? 128 : row_bytes % 64 == 0 ? 64 : 32;
+}
+
 static TcLayout tc_layout_for(int row_bytes, int k, int ctas) {
     TcLayout L{};
     L.ctas = ctas;
     L.row_bytes = row_bytes;
     L.k = k;
-    L.cw = row_bytes % 128 == 0 ? 128 : row_bytes % 64 == 0 ? 64 : 32;
+    L.cw = tc_chunk_bytes(row_bytes);
     L.kpad = (row_bytes + L.cw - 1) / L.cw * L.cw;
     L.nch = L.kpad / L.cw;
     const size_t stage = (size_t)kTcRows * L.kpad;
@@ -1004,7 +1015,7 @@ bool encode_row_map(void *map, const void *base, int row_bytes, int64_t n_rows, 
 
 // Encode the two maps the tensor-core scan reads (X_LS tiles, X rows); false if unsupported.
 bool scan_tc_encode(const DevIndex &ix, int64_t ls_rows_pad, void *tm_ls, void *tm_x) {
-    const int cw = ix.row_bytes % 128 == 0 ? 128 : ix.row_bytes % 64 == 0 ? 64 : 32;
+    const int cw = tc_chunk_bytes(ix.row_bytes);
     static const bool gpromote = [] { const char *e = getenv("VF_GATHER_PROMOTE"); return e && atoi(e) == 1; }();
     bool ok = encode_rows(reinterpret_cast<CUtensorMap *>(tm_x), ix.X, ix.row_bytes, ix.n_points, cw, 1, gpromote);
     ok = ok && encode_rows(reinterpret_cast<CUtensorMap *>(tm_ls), ix.Xls, ix.row_bytes,

@@ -831,6 +831,14 @@ vf_status run_compute(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, int *
     if (pl.filter) nl += launch_and_filter(a, ss);
     if (pl.pack) nl += launch_pack(a, ss);
     if (prof) VF_CUDA(cudaEventRecord(sc->ev[8], ss));
+    // VF_GRAPH_AFTER=1 (read per search): the graph kernels start once the pre-filter is done, so
+    // the pre-filter runs on the whole GPU and the graph search shares it with the scan instead
+    const char *ga_e = getenv("VF_GRAPH_AFTER");
+    if (overlap && !graph_first_env && ga_e && atoi(ga_e) == 1) {
+        if (!sc->ev_filt) VF_CUDA(cudaEventCreateWithFlags(&sc->ev_filt, cudaEventDisableTiming));
+        VF_CUDA(cudaEventRecord(sc->ev_filt, ss));
+        VF_CUDA(cudaStreamWaitEvent(gs, sc->ev_filt, 0));
+    }
     const int sl = launch_scans();
     if (sl < 0) return fail(VF_ERR_INTERNAL, "scan kernel dispatch failed");
     nl += sl;
