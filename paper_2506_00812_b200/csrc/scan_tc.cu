@@ -143,6 +143,13 @@ static TcLayout tc_layout_for(int row_bytes, int k, int ctas) {
 
 // two CTAs per SM when the row size leaves >= 2 stages each, else one (nst < 2: k_scan instead)
 static TcLayout tc_layout(int row_bytes, int k) {
+    // VF_TC_LAYOUT_CTAS=1 / 2 forces the layout's CTAs per SM (read once; A/B of pipeline depth:
+    // one CTA holds more stages in flight, two run two independent chains)
+    static const int force = [] { const char *e = getenv("VF_TC_LAYOUT_CTAS"); return e ? atoi(e) : 0; }();
+    if (force == 1 || force == 2) {
+        const TcLayout F = tc_layout_for(row_bytes, k, force);
+        if (F.nst >= 2) return F;
+    }
     const TcLayout L2 = tc_layout_for(row_bytes, k, 2);
     return L2.nst >= 2 ? L2 : tc_layout_for(row_bytes, k, 1);
 }
