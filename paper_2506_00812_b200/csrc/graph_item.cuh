@@ -147,7 +147,11 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
         const int c = tl + j * TEAM;
         qreg[j] = c < chunks ? qrow[c] : make_uint4(0, 0, 0, 0);
     }
-    for (int i = lane; i < H; i += 32) htab[i] = -1;
+    // a label of at most 32 * H points gets a membership BITMAP of its local ids in the same shared
+    // words instead of the hash table: one atomicOr per child, no probing, never a spill (exact)
+    const bool vis_bm = S <= 32 * H && !(a.knobs & KNOB_VIS_HASH_ONLY);
+    const int32_t vis_clear = vis_bm ? 0 : -1;
+    for (int i = lane; i < H; i += 32) htab[i] = vis_clear;
     bool g_used = false;
     int n_smem = 0, nvis = 0, ntop = 0, E = 0, iters = 0;
     ull *cur = topA, *oth = topB;
@@ -158,7 +162,14 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
     auto process = [&](int32_t c, int32_t gid) {
         bool isnew;
         int nnew;
-        if (!g_used && 2 * (n_smem + 32) <= H && !(a.knobs & KNOB_VIS_2PHASE)) {
+        if (vis_bm) {
+            isnew = false;
+            if (c >= 0) {
+                const uint32_t bit = 1u << (c & 31);
+                isnew = !(atomicOr(reinterpret_cast<uint32_t *>(htab) + (c >> 5), bit) & bit);
+            }
+            nnew = __popc(__ballot_sync(FULL, isnew));
+        } else if (!g_used && 2 * (n_smem + 32) <= H && !(a.knobs & KNOB_VIS_2PHASE)) {
             // the whole batch fits the shared table and nothing has spilled: one insert-if-absent
             // probe per lane (atomicCAS; of duplicate ids within the batch exactly one lane inserts,
             // and which one does not matter -- keys are ordered by (distance, id) only)
@@ -370,8 +381,11 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
     }
     // ---- LOOP (Alg. 2)
     for (int iter = 0; iter < a.max_iter; iter++) {
-        int npar = 0;
-        for (int b = 0; b < ntop && npar < a.w; b += 32) {
+        int npar = 0, nnext = 0;
+        // VF_KNOBS bit 5: the w unexpanded entries after this iteration's parents are the next
+        // parents unless a child overtakes them -- their adjacency rows start towards L2 now
+        const int want_next = (a.knobs & KNOB_ADJ_PF_NEXT) ? a.w : 0;
+        for (int b = 0; b < ntop && (npar < a.w || nnext < want_next); b += 32) {
             const int i = b + lane;
             const bool unexp = i < ntop && !(cur[i] & 1ull);
             unsigned m = __ballot_sync(FULL, unexp);
@@ -383,6 +397,13 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
                     cur[i] |= 1ull;                             // mark expanded
                 }
                 npar++;
+            }
+            while (m && nnext < want_next) {
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                if (lane == l)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(ix.G + (base + (int64_t)((uint32_t)cur[i] >> 1)) * R));
+                nnext++;
             }
         }
         __syncwarp();

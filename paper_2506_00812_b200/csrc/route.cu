@@ -255,7 +255,6 @@ constexpr int kFiltThreads = 256;
 constexpr int kFiltBuf = 2048;
 constexpr int kFiltUnion = 64;
 constexpr int kFiltRows = 4;          // rows per thread per round
-constexpr int kFiltListNu = 8;        // more other labels than this: the label-list path (VF_KNOBS bit 5)
 
 template <int MINB>
 __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a) {
@@ -372,10 +371,6 @@ __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a)
         // every label on a bitmap the signature only adds a sector (VF_KNOBS bit 0)
         const bool anynobm = __syncthreads_or(lab_nobm);
         const bool needsig = !(a.knobs & KNOB_FILT_SIG_AUTO) || anynobm;
-        // many other labels (an LS label with many AND queries): one pass over the point's sorted
-        // label list finds all of them at once, instead of one signature test and
-        // bitmap sector per label (VF_KNOBS bit 5; threshold kFiltListNu)
-        const bool bylist = (a.knobs & KNOB_FILT_LIST) && nu > kFiltListNu;
         const int bits_off = s_bits_off;
         if (!compact && bits_off < 0) {          // pool exhausted: the scan verifies this tile
             __syncthreads();
@@ -453,7 +448,7 @@ __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a)
                 }
             } else {
                 unsigned long long lb[kFiltRows];
-                if (allbits && !bylist) {
+                if (allbits) {
                     // membership bitmaps (one bit read per (row, label), independent loads) and
                     // binary searches in the short posting lists of labels without one
                     unsigned long long sg[kFiltRows];

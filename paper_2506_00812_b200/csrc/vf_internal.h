@@ -257,13 +257,14 @@ struct SearchArgs {
     // bit 0 the AND pre-filter reads the point's label signature only when some label of the tile
     // has no membership bitmap; bits 1-2 graph row prefetch into L2 (0 per 128-B line, 1 one bulk
     // prefetch of the row's exact bytes, 2 none); bit 3 no L2 prefetch of adjacency rows; bit 4 the
-    // AND pre-filter at 6 CTAs per SM; bit 5 the pre-filter tests tiles with many other labels by
-    // the point's label list; bit 6 the beam
-    // search's visited set always takes the two-phase path (find, then insert)
+    // AND pre-filter at 6 CTAs per SM; bit 5 L2 prefetch of the adjacency rows of the likely next
+    // parents (the w unexpanded Top entries after this iteration's); bit 6 the beam search's visited set always takes the two-phase path
+    // (find, then insert); bit 7 no visited bitmap for small labels (hash table only)
     int32_t knobs;
 };
 enum : int32_t { KNOB_FILT_SIG_AUTO = 1, KNOB_PF_SHIFT = 1, KNOB_PF_MASK = 3 << 1, KNOB_NO_ADJ_PF = 1 << 3,
-                 KNOB_FILT_OCC6 = 1 << 4, KNOB_FILT_LIST = 1 << 5, KNOB_VIS_2PHASE = 1 << 6 };
+                 KNOB_FILT_OCC6 = 1 << 4, KNOB_ADJ_PF_NEXT = 1 << 5, KNOB_VIS_2PHASE = 1 << 6,
+                 KNOB_VIS_HASH_ONLY = 1 << 7 };
 constexpr int32_t kDefaultKnobs = KNOB_FILT_SIG_AUTO | (1 << KNOB_PF_SHIFT) | KNOB_NO_ADJ_PF;   // r02t A/B
 
 __device__ __forceinline__ bool gate_skip(const SearchArgs &a) {

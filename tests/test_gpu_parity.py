@@ -226,8 +226,11 @@ def test_batch_order_independence(vf, tiny):
     assert (a[perm] == b).all() and (ad[perm] == bd).all()
 
 
-def test_visited_overflow_to_global_table(vf, tiny):
-    """itopk large enough that the shared-memory visited set spills: still bit-exact."""
+@pytest.mark.parametrize("knobs", ["11", "139"])
+def test_visited_overflow_to_global_table(vf, tiny, knobs, monkeypatch):
+    """itopk large enough that the shared-memory visited set spills (139: hash table only -- the
+    tiny labels otherwise take the visited bitmap, which never spills): still bit-exact."""
+    monkeypatch.setenv("VF_KNOBS", knobs)
     w, go, gi = tiny
     g, o = _pair(vf, w.X, w, go, gi)
     ids, d = g.search(w.Q[:200], w.q_off[:201], w.q_lab[:w.q_off[200]], k=10, itopk=1024)
@@ -413,3 +416,29 @@ def test_device_offsets_invalid_queries_get_empty_rows(vf, tiny):
                 assert (ids[i] == -1).all() and np.isinf(dd[i]).all(), (n, i)
             else:
                 assert (ids[i] == oi[i]).all() and (dd[i] == od[i].astype(np.float32)).all(), (n, i)
+
+
+@pytest.mark.parametrize("knobs", ["0", "11", "16", "43", "75", "139", "203"])
+def test_implementation_switches_do_not_change_results(vf, tiny, knobs, monkeypatch):
+    """VF_KNOBS (reading #52; read per search) selects equal-result implementation
+    variants: signature loads in the AND pre-filter, graph row / adjacency prefetch, pre-filter
+    occupancy, next-parent adjacency prefetch, the visited set's one-probe / two-phase / bitmap
+    paths. Every setting returns the oracle's ids, distances and per-item V / E (itopk 512 makes
+    the hash-table settings spill to the global table)."""
+    from workload import gen
+    monkeypatch.setenv("VF_KNOBS", knobs)
+    w, go, gi = tiny
+    g, o = _pair(vf, w.X, w, go, gi)
+    for mode_q, op, mode, thr in [("single", "single", "greedy", 0), ("and2", "and", "greedy", 400),
+                                   ("and2", "and", "parallel", 0), ("or2", "or", "greedy", 0)]:
+        if mode_q == "single":
+            qoff, qlab = w.q_off, w.q_lab
+        else:
+            qoff, qlab = gen.gen_query_labels(w.cfg, w.post_off, w.post_ids, n=len(w.Q), mode=mode_q)
+        for itopk in (32, 512):
+            ids, d = g.search(w.Q, qoff, qlab, k=10, itopk=itopk, op=op, recall_mode=mode, and_scan_threshold=thr,
+                              search_width=2)
+            oi, od, octr = o.search(w.Q, qoff, qlab, k=10, itopk=itopk, op=op, recall_mode=mode,
+                                    and_scan_threshold=thr, search_width=2, counters=True)
+            assert (ids == oi).all() and (d == od.astype(np.float32)).all(), (knobs, op, mode, itopk)
+            _items_match(g, octr)
