@@ -49,7 +49,7 @@ CFG_INDEX = {"tiny": 0, "sift": 1, "yfcc": 2}
 # scan_threshold, recall_mode); the reference arm (the oracle) runs at it so both arms answer the
 # same searches
 OP_POINT = {"tiny": (32, 1, 0, 0, "greedy"), "sift": (16, 2, 0, 0, "greedy"), "yfcc": (32, 2, 1000, 0, "greedy")}
-ITOPK_GRID = (16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512)
+ITOPK_GRID = (16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512)
 METRIC = "QPS at recall@10 >=0.90 and >=0.99 (1/2/4/8 B200); p50 latency at batch 1"
 SHARDED_QUERIES = 1_000_000          # BASELINE.json configs[4]: the 1M-query batch at N > 1
 

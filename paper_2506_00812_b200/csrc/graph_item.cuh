@@ -48,21 +48,24 @@ static inline GraphLayout graph_layout(int itopk, int hash_slots) {
 
 __device__ __forceinline__ uint32_t vis_hash(int32_t c) { return (uint32_t)c * 0x9E3779B1u; }
 
-__device__ __forceinline__ bool smem_find(const int32_t *tab, uint32_t mask, int32_t c) {
-    uint32_t h = vis_hash(c) & mask;
+// the shared table has any number H of slots: a slot is the high word of hash * H, probing wraps
+__device__ __forceinline__ uint32_t vis_slot(int32_t c, uint32_t H) { return __umulhi(vis_hash(c), H); }
+__device__ __forceinline__ uint32_t vis_next(uint32_t h, uint32_t H) { return h + 1 == H ? 0u : h + 1; }
+__device__ __forceinline__ bool smem_find(const int32_t *tab, uint32_t H, int32_t c) {
+    uint32_t h = vis_slot(c, H);
     for (;;) {
         const int32_t v = tab[h];
         if (v == c) return true;
         if (v < 0) return false;
-        h = (h + 1) & mask;
+        h = vis_next(h, H);
     }
 }
-__device__ __forceinline__ void smem_insert(int32_t *tab, uint32_t mask, int32_t c) {
-    uint32_t h = vis_hash(c) & mask;
+__device__ __forceinline__ void smem_insert(int32_t *tab, uint32_t H, int32_t c) {
+    uint32_t h = vis_slot(c, H);
     for (;;) {
         const int32_t old = atomicCAS(tab + h, -1, c);
         if (old == -1 || old == c) return;
-        h = (h + 1) & mask;
+        h = vis_next(h, H);
     }
 }
 __device__ __forceinline__ bool gtab_find(const ull *tab, uint64_t mask, uint32_t epoch, int32_t c) {
@@ -133,7 +136,7 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
     int32_t *htab = reinterpret_cast<int32_t *>(wb + GL.off_hash);
     const int M = GL.itopk, H = GL.hash_slots, R = ix.R;
     const int chunks = ix.chunks, row_bytes = ix.row_bytes;
-    const uint32_t hmask = (uint32_t)H - 1;
+    const uint32_t HU = (uint32_t)H;
     const int r_shift = (R & (R - 1)) == 0 ? __ffs(R) - 1 : -1;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int32_t S = bi.S;
@@ -175,12 +178,12 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
             // and which one does not matter -- keys are ordered by (distance, id) only)
             isnew = false;
             if (c >= 0) {
-                uint32_t h = vis_hash(c) & hmask;
+                uint32_t h = vis_slot(c, HU);
                 for (;;) {
                     const int32_t old = atomicCAS(htab + h, -1, c);
                     if (old == -1) { isnew = true; break; }
                     if (old == c) break;
-                    h = (h + 1) & hmask;
+                    h = vis_next(h, HU);
                 }
             }
             nnew = __popc(__ballot_sync(FULL, isnew));
@@ -191,7 +194,7 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
             if (v && (__ffs(same) - 1) != lane) v = false;      // duplicate within the batch
             bool found = false;
             if (v) {
-                found = smem_find(htab, hmask, c);
+                found = smem_find(htab, HU, c);
                 if (!found && g_used) found = gtab_find(gtab, gmask, epoch, c);
             }
             isnew = v && !found;
@@ -200,7 +203,7 @@ __device__ __forceinline__ BeamOut beam_item(const SearchArgs &a, const DevIndex
             const bool use_smem = 2 * (n_smem + nnew) <= H;
             __syncwarp();
             if (isnew) {
-                if (use_smem) smem_insert(htab, hmask, c);
+                if (use_smem) smem_insert(htab, HU, c);
                 else gtab_insert(gtab, gmask, epoch, c);
             }
             if (nnew) { if (use_smem) n_smem += nnew; else g_used = true; }

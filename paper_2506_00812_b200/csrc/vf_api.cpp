@@ -494,9 +494,12 @@ namespace vf {
 // global overflow table large enough for every vertex the search can visit.
 void beam_sizes(int itopk, int w, int R, int n_init, int max_iter, int *hash_slots, uint64_t *gslots,
                 int warp_bytes) {
-    int hs = 1024;
+    // the visited table takes what the Top buffers leave of the warp's budget, in 32-slot steps
+    // (any count: slots are found by multiply-high, kernels/graph_item.cuh), at least 1,024 slots,
+    // at most 64 * itopk or 8,192
     const int64_t budget = (int64_t)warp_bytes - 16ll * itopk - 1024;
-    while (hs < 64 * itopk && hs < 8192 && (int64_t)hs * 2 * 4 <= budget) hs <<= 1;
+    int hs = (int)std::min<int64_t>(std::min<int64_t>(64ll * itopk, 8192), std::max<int64_t>(1024, budget / 4));
+    hs = std::max(1024, hs & ~31);
     const int64_t v_bound = (int64_t)n_init + (int64_t)max_iter * w * R + 32;
     *hash_slots = hs;
     *gslots = pow2ceil((uint64_t)(2 * v_bound + 64));

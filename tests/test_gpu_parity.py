@@ -56,7 +56,7 @@ def _items_match(g, o_ctr):
 
 
 @pytest.mark.parametrize("dtype", ["f32int", "u8"])
-@pytest.mark.parametrize("itopk", [16, 32, 64, 128])
+@pytest.mark.parametrize("itopk", [16, 20, 28, 32, 40, 56, 64, 100, 128, 160])
 def test_single_label_bit_exact(vf, tiny, dtype, itopk):
     w, go, gi = tiny
     X, Q = _variant(tiny, dtype)
