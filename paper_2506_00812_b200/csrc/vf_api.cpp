@@ -762,7 +762,12 @@ vf_status run_compute(vf_index *ix, Scratch *sc, Plan &pl, cudaStream_t s, int *
     // stream concurrently with the scan; graph CTAs take whatever each SM has left and pull items
     // dynamically. VF_OVERLAP=0 serialises them (A/B knobs: VF_TC_CTAS, VF_GRAPH_FIRST,
     // VF_GRAPH_PER_SM; scripts/ab_overlap.sh).
-    static const int overlap_env = [] { const char *e = getenv("VF_OVERLAP"); return e ? atoi(e) : 1; }();
+    // VF_OVERLAP (read per search): 1 always, 0 never, 2 (default) unless the f3 threshold makes the
+    // AND pre-filter heavy (>= kOverlapMaxF3): the persistent graph CTAs fill the SMs first and the
+    // pre-filter, which the scan waits for, would run in their leftovers (profiles/r02ss)
+    const char *ov_e = getenv("VF_OVERLAP");
+    const int ov_mode = ov_e ? atoi(ov_e) : 2;
+    const int overlap_env = ov_mode == 2 ? (a.and_scan_thr < kOverlapMaxF3 ? 1 : 0) : ov_mode;
     static const int tc_ctas_env = [] { const char *e = getenv("VF_TC_CTAS"); return e ? atoi(e) : 2; }();
     const bool overlap = overlap_env != 0 && pl.tc;
     // Both become runnable at the fork; the scan goes on a high-priority stream so the block

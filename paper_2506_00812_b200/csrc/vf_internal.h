@@ -23,6 +23,7 @@ __host__ __device__ __forceinline__ int graph_class(int32_t size) {
 constexpr int kMaxItopk = 1024;
 constexpr int kScanQG = 64;           // queries per scan segment (query group)
 constexpr int kF3TileRows = 8192;     // rows per tile of f3-only (fully pre-filtered) segments
+constexpr int kOverlapMaxF3 = 20000;  // f3 threshold from which scan / graph run one after the other
 constexpr int kWarpsPerGraphCta = 4;
 
 enum Path : uint32_t { PATH_NONE = 0, PATH_SCAN = 1, PATH_GRAPH = 2 };
