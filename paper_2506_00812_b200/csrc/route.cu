@@ -254,7 +254,10 @@ __global__ void k_scatter(SearchArgs a, int64_t n_slots, int qg) {
 constexpr int kFiltThreads = 256;
 constexpr int kFiltBuf = 2048;
 constexpr int kFiltUnion = 64;
-constexpr int kFiltRows = 4;          // rows per thread per round
+#ifndef VF_FILT_ROWS
+#define VF_FILT_ROWS 4
+#endif
+constexpr int kFiltRows = VF_FILT_ROWS;   // rows per thread per round
 
 template <int MINB>
 __global__ void __launch_bounds__(kFiltThreads, MINB) k_and_filter(SearchArgs a) {
